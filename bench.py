@@ -1,0 +1,358 @@
+"""Benchmark: implicit-Euler HODLR time-steps/s on BASELINE.json's n = 65536 1D workload (cfg3).
+
+One "step" = one pass of the whole hot path over one time level: GL weights
+(S1) and the compression of T (S2) recomputed (FDE_RECOMPRESS), assembly of the diagonally
+scaled HODLR of A_m (S3), leaf LU + SMW factorisation (S4-S5), tree solve (S6, fused as the
+extra right-hand-side column) and rhs formation u + dt f (S7), through the C-ABI fde1d_step.
+
+Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+Multi-GPU (torchrun, one rank per GPU): the single-problem path does not shard (DESIGN.md,
+"replicas only"): every rank runs its own cfg3 replica; value = all ranks' steps / max time.
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "time-steps/sec (HODLR build+factor+solve), n=65536 1D; HBM GB/s % of peak"
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=64)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-recompress", action="store_true",
+                   help="cache the T compression across steps (reported separately)")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------------------
+# clocks during the timed region
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "--query-gpu=" + self.FIELDS, "--format=csv,noheader,nounits",
+                 "-i", str(self.gpu), "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------------
+def algorithmic_work(ranks, n, leaf_sizes, nf=1):
+    """Per-step algorithmic FP64 flops and HBM bytes per kernel."""
+    ks = [r + 1 for r in ranks]
+    Wl = [sum(ks[:l]) for l in range(len(ks))]
+    W = sum(ks)
+    work = {}
+    fl = sum(2.0 / 3.0 * s ** 3 + 2.0 * s * s * (nf + W) for s in leaf_sizes)
+    by = 8.0 * n * (nf + W) + 8.0 * n * sum(ranks) + 8.0 * 4 * n      # write X, read L rows, d+-, u, f
+    work["k_leaf"] = (fl, by)
+    fl_r = sum(2.0 * n * k * (nf + w + k) for k, w in zip(ks, Wl))
+    by_r = sum(8.0 * n * (nf + w + k) + 8.0 * n * (k - 1) for k, w in zip(ks, Wl))
+    work["k_lvl_reduce"] = (fl_r, by_r)
+    fl_u = sum(2.0 * n * k * (nf + w) for k, w in zip(ks, Wl))
+    by_u = sum(8.0 * n * (2 * (nf + w) + k) for k, w in zip(ks, Wl))
+    work["k_lvl_update"] = (fl_u, by_u)
+    return work
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+def load_traffic():
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return {}
+
+
+# ---------------------------------------------------------------------------------------
+def cpu_oracle_baseline(wl, n_sample=8192, reps=2):
+    """The oracle as it stands (dense LAPACK LU step, oracle.fd1d) on the host cores, on a
+    bounded sample of cfg3: n_sample interior points with cfg3's alpha, dt and coefficients,
+    extrapolated to n = 65536 by the O(n^3) LU cost."""
+    from oracle.fd1d import assemble_A, step_dense   # oracle: cpu_baseline leg only
+    from paper_1804_05522_b200 import workloads as W
+    cores = os.cpu_count()
+    s = W.cfg3(K=reps, n=n_sample)
+    u = s.u0[0]
+    t0 = time.perf_counter()
+    for m in range(1, reps + 1):
+        dp, dm = s.coeffs(m)
+        A = assemble_A(float(s.alpha[0]), s.n, s.h, s.dt, dp[0], dm[0])
+        u, _ = step_dense(A, u, s.source(m)[0], s.dt)
+    el = (time.perf_counter() - t0) / reps
+    scale = (wl.n / n_sample) ** 3
+    value = 1.0 / (el * scale)
+    return {"value": value, "unit": "time-steps/s", "cores": cores, "kind": "oracle",
+            "sample": "%d dense LU steps (oracle.fd1d.assemble_A + step_dense) at n=%d with cfg3's "
+                      "alpha/dt/coefficients, %.2f s/step, extrapolated x(%d/%d)^3 = x%d (LU is O(n^3))"
+                      % (reps, n_sample, el, wl.n, n_sample, n_sample, int(scale))}
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return 0
+    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
+    from paper_1804_05522_b200 import workloads as W
+    wl = W.cfg3(K=2)
+    steps = max(1, min(args.steps, 3))
+    warm = max(0, min(args.warmup, 1))
+    base = cpu_oracle_baseline(wl, n_sample=4096, reps=warm + steps) if True else None
+    line = {"impl": "reference", "metric": METRIC, "value": base["value"], "unit": "time-steps/s",
+            "n_gpus": args.gpus, "steps": steps, "warmup": warm,
+            "ms_per_step": 1e3 / base["value"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "cfg3: 1D FDE n=65536 alpha=1.8 leaf 128 tol 1e-10 (BASELINE configs[2])",
+                       "l2": "n/a (CPU)"},
+            "cpu_baseline": {"kind": "oracle", "cores": base["cores"], "sample": base["sample"],
+                             "value": base["value"], "unit": "time-steps/s"},
+            "e2e": {"value": base["value"], "unit": "time-steps/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------------------
+def run_ours(args, world, rank, local):
+    import torch
+    from paper_1804_05522_b200 import build as B
+    B.build()
+    from paper_1804_05522_b200 import workloads as W
+    from paper_1804_05522_b200 import _lib
+    from paper_1804_05522_b200.hodlr import (Fde1dStepper, launch_count, FDE_RECOMPRESS,
+                                             FDE_NO_KEEP, FDE_HOST_PTRS)
+    lib = _lib.load()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    wl = W.cfg3(K=32)
+    n = wl.n
+    DP = torch.as_tensor(wl.d_plus[:, 0, :], device=dev).contiguous()
+    DM = torch.as_tensor(wl.d_minus[:, 0, :], device=dev).contiguous()
+    F = torch.as_tensor(wl.f[0, 0, :], device=dev).contiguous()
+    bufs = [torch.zeros(n, dtype=torch.float64, device=dev) for _ in range(2)]
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+    st = Fde1dStepper(n, wl.alpha, wl.h, wl.tol, wl.leaf)
+    flags = FDE_NO_KEEP | (0 if args.no_recompress else FDE_RECOMPRESS)
+    state = {"i": 0}
+
+    def one_step():
+        i = state["i"]
+        m = i % wl.K
+        u_prev, u_next = bufs[i % 2], bufs[(i + 1) % 2]
+        st.step(wl.dt, DP[m], DM[m], F, u_prev, u_next=u_next, coeffs_changed=True, flags=flags)
+        state["i"] = i + 1
+
+    one_step()                                   # build the handle (allocation, tree, plan)
+    torch.cuda.synchronize()
+    for _ in range(args.warmup):
+        flush.zero_()
+        one_step()
+    torch.cuda.synchronize()
+
+    def timed(K, profile=False):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        if profile:
+            lib.fde_profile_enable(1)
+        barrier()
+        torch.cuda.synchronize()
+        l0 = launch_count()
+        for k in range(K):
+            flush.zero_()                        # L2 flush between timed steps (untimed)
+            evs[k][0].record()
+            one_step()
+            evs[k][1].record()
+        torch.cuda.synchronize()
+        l1 = launch_count()
+        barrier()
+        ms = [a.elapsed_time(b) for a, b in evs]
+        prof = None
+        if profile:
+            buf = __import__("ctypes").create_string_buffer(1 << 16)
+            lib.fde_profile_dump(buf, 1 << 16)
+            lib.fde_profile_enable(0)
+            prof = json.loads(buf.value.decode())
+        return ms, l1 - l0, prof
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    ms, launches, _ = timed(args.steps)
+    clk = clocks.stop()
+    total_ms = sum(ms)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = world * args.steps / (total_ms / 1e3)
+
+    # per-kernel durations (CUDA events around every launch, same steps again)
+    pms, _, prof = timed(args.steps, profile=True)
+
+    # cached-compression variant (T compression depends on alpha, n, leaf, tol only)
+    flags_save = flags
+    flags = FDE_NO_KEEP
+    cms, _, _ = timed(args.steps)
+    flags = flags_save
+    cached = {"value": world * args.steps / (sum(cms) / 1e3), "ms_per_step": sum(cms) / args.steps}
+
+    # end to end through the C-ABI with HOST buffers (H2D of d+-, f, u_prev; D2H of u_next)
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda t: t.cpu().pin_memory()
+        hDP = [pin(DP[m]) for m in range(wl.K)]
+        hDM = [pin(DM[m]) for m in range(wl.K)]
+        hF = pin(F)
+        hu = [torch.zeros(n, dtype=torch.float64).pin_memory() for _ in range(2)]
+        st.step(wl.dt, hDP[0], hDM[0], hF, hu[0], u_next=hu[1], flags=flags | FDE_HOST_PTRS)
+        barrier()
+        t0 = time.perf_counter()
+        for k in range(args.steps):
+            m = k % wl.K
+            st.step(wl.dt, hDP[m], hDM[m], hF, hu[k % 2], u_next=hu[(k + 1) % 2],
+                    flags=flags | FDE_HOST_PTRS)          # synchronous: ends with the D2H copy
+        el = time.perf_counter() - t0
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([el], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        e2e = {"value": world * args.steps / el, "unit": "time-steps/s",
+               "h2d_bytes_per_step": 4 * n * 8, "d2h_bytes_per_step": n * 8}
+
+    ranks = st.ranks()
+    leaves = [wl.leaf] * (n // wl.leaf)
+    work = algorithmic_work(ranks, n, leaves)
+    peaks = load_peaks()
+    traffic = load_traffic()
+    kern = {}
+    for name, (cnt, tot) in (prof or {}).items():
+        kern[name] = {"launches_per_step": cnt / args.steps, "ms_per_step": tot / args.steps}
+    dom = max(kern, key=lambda k: kern[k]["ms_per_step"]) if kern else None
+    roof = None
+    if dom:
+        t_s = kern[dom]["ms_per_step"] / 1e3
+        launches_dom = kern[dom]["launches_per_step"]
+        fl, by = work.get(dom, (0.0, 0.0))
+        if dom == "k_leaf":
+            roof = {"bound": "alu", "achieved": fl / t_s / 1e12, "peak": FP64_PEAK_TFLOPS,
+                    "unit": "TFLOP/s", "frac": fl / t_s / 1e12 / FP64_PEAK_TFLOPS,
+                    "traffic": traffic.get(dom), "kernel": dom,
+                    "flops_per_launch": fl / max(1.0, launches_dom),
+                    "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (measured DFMA 36.8)"}
+        else:
+            roof = {"bound": "hbm", "achieved": by / t_s / 1e9, "peak": peaks.get("hbm_gbs"),
+                    "unit": "GB/s", "frac": by / t_s / 1e9 / peaks.get("hbm_gbs", 6549.1),
+                    "traffic": traffic.get(dom), "kernel": dom,
+                    "bytes_per_launch": by / max(1.0, launches_dom),
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)"}
+        roof["share_of_step"] = kern[dom]["ms_per_step"] / (sum(pms) / args.steps)
+
+    line = {"metric": METRIC, "value": value, "unit": "time-steps/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": "cfg3: 1D FDE n=65536 alpha=1.8 leaf 128 tol 1e-10, d+-(x,t) per "
+                                   "BASELINE configs[2], refactor every step",
+                       "n": n, "leaf": wl.leaf, "tol": wl.tol, "ranks": ranks,
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "flushed between timed steps (512 MiB write, untimed)",
+                       "recompress_T_each_step": not args.no_recompress},
+            "gpu_launches": launches,
+            "clocks": clk, "e2e": e2e, "roofline": roof, "kernels": kern,
+            "cached_T_compression": cached}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_oracle_baseline(wl)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    st.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+    return run_ours(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,165 @@
+/*
+ * fdehodlr.h -- C-ABI of the B200-native HODLR time-stepper for space-fractional
+ * diffusion (arXiv 1804.05522).  Citations: P:<n> = /root/reference/PAPER.md line n.
+ *
+ * Problem (Eq. 1.1; scheme Eq. 2.5-2.6):
+ *   A_m u^(m) = u^(m-1) + dt f^(m),
+ *   A_m = shift*I + c (D+^(m) T_{alpha,N} + D-^(m) T_{alpha,N}^T),  c = dt / h^alpha,
+ *   T_{alpha,N}[i,j] = -g_{i-j+1} (lower Hessenberg Toeplitz), g_k = (-1)^k binom(alpha,k).
+ * shift = 1 for the 1D step (Eq. 2.5); shift = 1/2 for the two operators of the
+ * 2D Sylvester step (Eq. 4.3).
+ *
+ * Method (HODLR): GL weights by the recursion of P:1190-1193,
+ * per-level compression of the Toeplitz off-diagonal blocks at tolerance tol (P:1145,
+ * reading R7: threshold tol*2^alpha on the T-blocks), diagonal scaling + identity shift
+ * applied to the compressed factors and leaves, level-by-level factorisation
+ * (batched unpivoted leaf LU + Sherman-Morrison-Woodbury updates), tree-ordered solve.
+ *
+ * Conventions (all entry points):
+ *  - Floating point is IEEE double.  Arrays are column-major.  Pointers marked [dev] are
+ *    device pointers (e.g. torch.Tensor.data_ptr() of a CUDA tensor), [host] are host
+ *    pointers.  Arrays of a batch are stored instance after instance: d_plus[b*n + i].
+ *  - Callers own every array they pass.  The library owns only the handle and its
+ *    workspaces, released by hodlr_destroy().
+ *  - `stream` is a cudaStream_t passed as void*; NULL means the legacy default stream.
+ *    Every call only enqueues work on `stream` (asynchronous) unless FDE_SYNC is set in
+ *    `flags`, in which case it synchronises the stream and reports device-side errors.
+ *  - Return value: FDE_OK or a positive FDE_E* code; fde_last_error() (thread-local)
+ *    names the offending argument.  Device-side failures (zero / non-finite leaf pivot,
+ *    singular SMW capacitance matrix, rank cap exceeded) are latched in the handle and
+ *    returned by hodlr_status() after the stream is synchronised.
+ *  - Results are deterministic: every reduction has a fixed order, independent of the
+ *    CTA schedule.
+ */
+#ifndef FDEHODLR_H
+#define FDEHODLR_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FDE_OK        0
+#define FDE_EDOMAIN   1   /* argument outside its domain (alpha, n, h, dt, tol, leaf, batch) */
+#define FDE_EDIM      2   /* dimension / leading-dimension / rank-capacity mismatch */
+#define FDE_ESINGULAR 3   /* zero or non-finite pivot (leaf LU or SMW capacitance matrix) */
+#define FDE_ENOCONV   4   /* compression did not reach tol within the rank cap; EK not converged */
+#define FDE_ECUDA     5   /* a CUDA runtime call failed */
+#define FDE_ENOMEM    6   /* device allocation failed */
+
+/* flags */
+#define FDE_SYNC      1u  /* synchronise `stream` before returning and report device errors */
+#define FDE_CHECK     2u  /* also check d_plus, d_minus >= 0 on the device (implies a sync) */
+#define FDE_HOST_PTRS 4u  /* fde1d_step: d_plus, d_minus, f, u_prev, u_next are HOST arrays; the
+                             library copies them through pinned staging buffers on `stream` */
+#define FDE_NO_KEEP   8u  /* fde1d_step: do not keep the factor for reuse (saves HBM traffic when
+                             the coefficients change every step) */
+#define FDE_RECOMPRESS 16u /* fde1d_step: recompute S1 (GL weights) and S2 (compression of T)
+                             even when the cached handle already holds them */
+
+/* Compile-time capacities of this build. */
+#define FDE_LEAF_MAX  128 /* largest leaf (dense diagonal block) held in shared memory */
+#define FDE_RANK_MAX  47  /* largest compressed rank of one level's T-block */
+
+typedef struct fde_hodlr* fde_hodlr_t;   /* opaque; one per (operator family, batch) */
+
+/* Build the HODLR representation of `batch` operators
+ *     A_b = shift*I + (dt/h^alpha_b)(D+_b T_{alpha_b} + D-_b T_{alpha_b}^T),  b < batch,
+ * i.e. steps S1 (GL weights) and S2 (per-level compression of the Toeplitz
+ * off-diagonal blocks) on the device, and records dt and copies of
+ * d_plus/d_minus for the next hodlr_factor().
+ *   batch >= 1; n >= 1; alpha[host, batch] in (1, 2]; h > 0; dt >= 0; shift > 0;
+ *   d_plus, d_minus [dev, batch*n] (>= 0, checked only under FDE_CHECK);
+ *   tol in (0, 1): truncation tolerance (relative to ||T||_2 <= 2^alpha, reading R7);
+ *   2 <= leaf <= FDE_LEAF_MAX: leaf size (every level is split while its largest node
+ *   exceeds leaf, reading R10).
+ * On success *out receives a new handle (caller releases it with hodlr_destroy). */
+int hodlr_build(int batch, int n, const double* alpha, double h, double dt,
+                const double* d_plus, const double* d_minus, double shift,
+                double tol, int leaf, unsigned flags, void* stream, fde_hodlr_t* out);
+
+/* Replace dt and the diffusion coefficients (copied from [dev, batch*n]) of a built handle;
+ * the compression of T (which depends on alpha, n, leaf, tol only) is reused.
+ * d_plus / d_minus may be NULL to keep the current values.  Invalidates the factor. */
+int hodlr_update(fde_hodlr_t H, double dt, const double* d_plus, const double* d_minus,
+                 unsigned flags, void* stream);
+
+/* Factorise A (S3 diagonal scaling + shift fused into S4 batched leaf LU; S5
+ * Sherman-Morrison-Woodbury level updates, leaves to root).  The factor is kept in the
+ * handle for any number of hodlr_solve() calls (LU reuse). */
+int hodlr_factor(fde_hodlr_t H, unsigned flags, void* stream);
+
+/* Solve A X = B with the kept factor (S6 tree-ordered solve).
+ *   b, x [dev]: nrhs columns of length n per instance, leading dimension ld >= n,
+ *   instance stride ld*nrhs: element (i, j) of instance q at [q*ld*nrhs + j*ld + i].
+ *   x may alias b.  1 <= nrhs <= 64. */
+int hodlr_solve(fde_hodlr_t H, const double* b, double* x, int nrhs, int ld,
+                unsigned flags, void* stream);
+
+/* y = A x with the HODLR representation (leaf blocks + scaled low-rank factors),
+ * same layout conventions as hodlr_solve; y must not alias x. */
+int hodlr_matvec(fde_hodlr_t H, const double* x, double* y, int nrhs, int ld,
+                 unsigned flags, void* stream);
+
+/* Device-side status latched by the kernels (call after synchronising the stream):
+ * returns FDE_OK / FDE_ESINGULAR / FDE_ENOCONV; *where (may be NULL) gets the instance*
+ * 65536 + leaf-or-node index of the first failure. */
+int hodlr_status(fde_hodlr_t H, int* where);
+
+/* Per-level compressed ranks of instance `inst` (host copy; synchronises the handle's
+ * last stream).  ranks[host, levels]; returns the number of levels L in *levels. */
+int hodlr_ranks(fde_hodlr_t H, int inst, int* ranks, int max_levels, int* levels);
+
+void hodlr_destroy(fde_hodlr_t H);
+
+/* One implicit-Euler step of Eq. (2.5) for `batch` independent 1D problems:
+ *     u_next = A_m^{-1} (u_prev + dt f_m)          (S1-S7)
+ * d_plus_m, d_minus_m, f_m, u_prev, u_next: [dev, batch*n] (or [host] with FDE_HOST_PTRS);
+ * u_next may alias u_prev.  alpha [host, batch].
+ * `cache` (may be NULL): in/out handle.  If *cache is NULL or was built for different
+ * (batch, n, alpha, h, leaf, tol), a new handle is built (and the old one destroyed).
+ * coeffs_changed != 0 (or no factor kept): the step refactorises with the new d+-, dt and
+ * the right-hand side is carried through the factorisation as an extra column (fused
+ * factor+solve); coeffs_changed == 0 reuses the kept factor (solve only).
+ * With cache == NULL a temporary handle is built and destroyed inside the call. */
+int fde1d_step(int batch, int n, const double* alpha, double h, double dt,
+               const double* d_plus_m, const double* d_minus_m, const double* f_m,
+               const double* u_prev, double* u_next, double tol, int leaf,
+               int coeffs_changed, unsigned flags, fde_hodlr_t* cache, void* stream);
+
+/* One step of the 2D scheme as a Sylvester equation (Eq. 4.3, reading R11):
+ *     A1 X + X A2^T = Uu Uv^T + dt Fu Fv^T,
+ *     A1 = 1/2 I + (dt/hx^alpha1)(D1+ T1 + D1- T1^T),  A2 likewise in y,
+ * solved by the extended Krylov method on the HODLR factors of A1 and A2.
+ *   d1p, d1m [dev, nx]; d2p, d2m [dev, ny]; Fu [dev, nx*rf], Fv [dev, ny*rf];
+ *   Uu [dev, nx*ru], Uv [dev, ny*ru] (ru may be 0); Xu [dev, nx*rmax], Xv [dev, ny*rmax].
+ *   *rx receives the rank of X = Xu Xv^T; resid_out (host, may be NULL) the relative true
+ *   residual; iters_out (host, may be NULL) the EK iterations.  cache[2] holds the two
+ *   operator handles (built on first use, reused while the arguments match).
+ *   Returns FDE_ENOCONV with the best iterate if ek_maxit is reached, FDE_EDIM if the
+ *   truncated rank exceeds rmax. */
+int fde2d_step(int nx, int ny, double alpha1, double alpha2, double hx, double hy, double dt,
+               const double* d1p, const double* d1m, const double* d2p, const double* d2m,
+               const double* Fu, const double* Fv, int rf,
+               const double* Uu, const double* Uv, int ru,
+               double* Xu, double* Xv, int rmax, int* rx,
+               double tol, double ek_tol, int ek_maxit, int leaf,
+               fde_hodlr_t* cache, double* resid_out, int* iters_out,
+               unsigned flags, void* stream);
+
+/* Thread-local description of the last error returned on this thread ("" if none). */
+const char* fde_last_error(void);
+
+/* Number of kernels this library has launched in this process (for launch accounting). */
+long long fde_launch_count(void);
+
+/* Tracing: when enabled, every kernel launch is bracketed by a pair of CUDA events on its
+ * stream.  fde_profile_dump() synchronises those events, writes a JSON object
+ * {"kernel": [launches, total_ms], ...} into buf (NUL terminated), clears the records and
+ * returns the string length (or -(needed+1) if len is too small).  Disabling drops them. */
+void fde_profile_enable(int on);
+int fde_profile_dump(char* buf, int len);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FDEHODLR_H */

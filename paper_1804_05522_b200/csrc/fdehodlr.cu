@@ -1,0 +1,764 @@
+// fdehodlr.cu -- host side of the C-ABI (include/fdehodlr.h): argument checking, tree
+// bookkeeping, workspace management and kernel orchestration on the caller's stream.
+// All arithmetic of the method runs in the kernels of k_*.cuh.
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "fde_common.cuh"
+#include "k_gl.cuh"
+#include "k_compress.cuh"
+#include "k_leaf.cuh"
+#include "k_level.cuh"
+#include "k_matvec.cuh"
+
+// ---------------------------------------------------------------------------------------
+// errors, launch accounting
+static thread_local std::string g_last_error;
+static std::atomic<long long> g_launches{0};
+
+static int set_err(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define CU(call)                                                                     \
+  do {                                                                               \
+    cudaError_t e_ = (call);                                                         \
+    if (e_ != cudaSuccess)                                                           \
+      return set_err(e_ == cudaErrorMemoryAllocation ? FDE_ENOMEM : FDE_ECUDA,       \
+                     "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__,      \
+                     __LINE__);                                                      \
+  } while (0)
+
+#define LAUNCHED()                                                                   \
+  do {                                                                               \
+    g_launches.fetch_add(1, std::memory_order_relaxed);                              \
+    cudaError_t e_ = cudaGetLastError();                                             \
+    if (e_ != cudaSuccess)                                                           \
+      return set_err(FDE_ECUDA, "kernel launch: %s (%s:%d)", cudaGetErrorString(e_), \
+                     __FILE__, __LINE__);                                            \
+  } while (0)
+
+// ---------------------------------------------------------------------------------------
+// tracing: optional CUDA-event pair around every kernel launch (fde_profile_enable)
+struct ProfRec {
+  const char* name;
+  cudaEvent_t a, b;
+};
+static bool g_prof = false;
+static std::vector<ProfRec> g_prof_recs;
+static std::vector<cudaEvent_t> g_ev_free;
+
+static cudaEvent_t prof_event() {
+  if (!g_ev_free.empty()) {
+    cudaEvent_t e = g_ev_free.back();
+    g_ev_free.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct ProfScope {
+  const char* name;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr;
+  ProfScope(const char* nm, cudaStream_t st) : name(nm), s(st) {
+    if (g_prof) { a = prof_event(); cudaEventRecord(a, s); }
+  }
+  ~ProfScope() {
+    if (g_prof) {
+      cudaEvent_t b = prof_event();
+      cudaEventRecord(b, s);
+      g_prof_recs.push_back({name, a, b});
+    }
+  }
+};
+#define PROF(nm) ProfScope prof_scope_(nm, s)
+
+struct fde_hodlr {
+  int batch = 0, n = 0, leaf = 0, L = 0, nleaf = 0, nnodes = 0;
+  double h = 0, dt = 0, shift = 1, tol = 0;
+  std::vector<double> alpha;
+  // tree (host)
+  std::vector<int> node_r0, node_n1, node_n2, node_seg, leaf_r0, leaf_n;
+  std::vector<int> seg_ofs, seg_node, seg_child, seg_row0, seg_len, lev_m;
+  std::vector<long long> lev_lofs, lev_lraw;
+  long long lf_stride = 0, lraw_stride = 0;
+  int max_seg = 0, max_nodes_lvl = 0;
+  TreeDev tree{};
+  // compression plan
+  std::vector<PcTask> tasks;
+  std::vector<PcChunk> chunks;
+  std::vector<int> launch_chunk0;   // chunk ranges of the cooperative launches
+  // device memory
+  std::vector<void*> allocs;
+  int* d_tree_int = nullptr;
+  long long* d_lev_lofs = nullptr;
+  double *d_alpha = nullptr, *d_cfac = nullptr, *d_g = nullptr;
+  double *d_Lf = nullptr, *d_Lraw = nullptr;
+  int *d_rank = nullptr, *d_colofs = nullptr;
+  double *d_dp = nullptr, *d_dm = nullptr;
+  double *d_X = nullptr, *d_LU = nullptr, *d_P = nullptr, *d_S = nullptr, *d_K = nullptr;
+  int* d_Kpiv = nullptr;
+  long long gstride = 0, xstride = 0, lustride = 0, pstride_seg = 0, pstride_inst = 0;
+  long long sstride_node = 0, sstride_inst = 0, kstride_inst = 0, pivstride_inst = 0;
+  int ncap = 0;
+  // compression scratch
+  PcTask* d_tasks = nullptr;
+  PcChunk* d_chunks = nullptr;
+  unsigned* d_ctr = nullptr;
+  double *d_part = nullptr, *d_gram_part = nullptr, *d_gram = nullptr, *d_vkeep = nullptr;
+  int *d_task_kr = nullptr, *d_task_rank = nullptr;
+  DevStatus* d_status = nullptr;
+  // staging for FDE_HOST_PTRS
+  double *d_in = nullptr;   // 4 * batch * n
+  double* d_rhs = nullptr;  // batch * n (solve-only rhs)
+  bool factored = false;
+  cudaStream_t last_stream = nullptr;
+};
+
+template <typename T>
+static int dalloc(fde_hodlr* H, T** p, size_t count) {
+  void* q = nullptr;
+  size_t bytes = count * sizeof(T);
+  if (bytes == 0) bytes = 8;
+  cudaError_t e = cudaMalloc(&q, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return set_err(FDE_ENOMEM, "cudaMalloc(%zu bytes) failed: %s", bytes, cudaGetErrorString(e));
+  }
+  H->allocs.push_back(q);
+  *p = (T*)q;
+  return FDE_OK;
+}
+
+#define TRY(x)               \
+  do {                       \
+    int rc_ = (x);           \
+    if (rc_ != FDE_OK) return rc_; \
+  } while (0)
+
+static void free_handle(fde_hodlr* H) {
+  if (!H) return;
+  for (void* p : H->allocs) cudaFree(p);
+  delete H;
+}
+
+// ---------------------------------------------------------------------------------------
+// tree (reading R10: uniform depth, N1 = floor, N2 = ceil)
+static void build_tree(fde_hodlr* H) {
+  const int n = H->n, leaf = H->leaf;
+  std::vector<std::pair<int, int>> nodes{{0, n}};
+  int L = 0;
+  H->node_r0.clear(); H->node_n1.clear(); H->node_n2.clear();
+  while (true) {
+    int mx = 0;
+    for (auto& nd : nodes) mx = std::max(mx, nd.second);
+    if (mx <= leaf) break;
+    std::vector<std::pair<int, int>> nxt;
+    for (auto& nd : nodes) {
+      const int n1 = nd.second / 2, n2 = nd.second - n1;
+      H->node_r0.push_back(nd.first);
+      H->node_n1.push_back(n1);
+      H->node_n2.push_back(n2);
+      nxt.push_back({nd.first, n1});
+      nxt.push_back({nd.first + n1, n2});
+    }
+    nodes.swap(nxt);
+    ++L;
+  }
+  H->L = L;
+  H->nleaf = (int)nodes.size();
+  H->nnodes = (1 << L) - 1;
+  H->leaf_r0.clear(); H->leaf_n.clear();
+  for (auto& nd : nodes) { H->leaf_r0.push_back(nd.first); H->leaf_n.push_back(nd.second); }
+  // segments and per-level sizes
+  H->seg_ofs.assign(L + 1, 0);
+  H->seg_node.clear(); H->seg_child.clear(); H->seg_row0.clear(); H->seg_len.clear();
+  H->node_seg.assign(3 * std::max(1, H->nnodes), 0);
+  H->lev_m.assign(std::max(1, L), 0);
+  H->lev_lofs.assign(std::max(1, L), 0);
+  H->lev_lraw.assign(std::max(1, L), 0);
+  H->max_seg = 0;
+  long long lofs = 0, lraw = 0;
+  for (int l = 0; l < L; ++l) {
+    H->seg_ofs[l] = (int)H->seg_node.size();
+    int local = 0, m = 0;
+    for (int j = 0; j < (1 << l); ++j) {
+      const int nd = (1 << l) - 1 + j;
+      const int r0 = H->node_r0[nd], n1 = H->node_n1[nd], n2 = H->node_n2[nd];
+      m = std::max(m, n2);
+      H->node_seg[3 * nd + 0] = local;
+      for (int c = 0; c < 2; ++c) {
+        if (c == 1) H->node_seg[3 * nd + 1] = local;
+        const int rs = c == 0 ? r0 : r0 + n1, len = c == 0 ? n1 : n2;
+        for (int o = 0; o < len; o += SEG) {
+          H->seg_node.push_back(j);
+          H->seg_child.push_back(c);
+          H->seg_row0.push_back(rs + o);
+          H->seg_len.push_back(std::min(SEG, len - o));
+          ++local;
+        }
+      }
+      H->node_seg[3 * nd + 2] = local;
+    }
+    H->max_seg = std::max(H->max_seg, local);
+    H->lev_m[l] = m;
+    H->lev_lofs[l] = lofs;
+    H->lev_lraw[l] = lraw;
+    lofs += (long long)m * RCAP;
+    lraw += (long long)m * KRAW;
+  }
+  H->seg_ofs[L] = (int)H->seg_node.size();
+  H->lf_stride = std::max(1LL, lofs);
+  H->lraw_stride = std::max(1LL, lraw);
+  H->max_nodes_lvl = L > 0 ? (1 << (L - 1)) : 1;
+}
+
+static int upload_tree(fde_hodlr* H) {
+  // pack all int tables in one buffer
+  std::vector<int> buf;
+  auto put = [&](const std::vector<int>& v) { size_t o = buf.size(); buf.insert(buf.end(), v.begin(), v.end()); if (v.empty()) buf.push_back(0); return o; };
+  size_t o_r0 = put(H->node_r0), o_n1 = put(H->node_n1), o_n2 = put(H->node_n2), o_ns = put(H->node_seg);
+  size_t o_lr = put(H->leaf_r0), o_ln = put(H->leaf_n), o_so = put(H->seg_ofs), o_sn = put(H->seg_node);
+  size_t o_sc = put(H->seg_child), o_s0 = put(H->seg_row0), o_sl = put(H->seg_len), o_m = put(H->lev_m);
+  TRY(dalloc(H, &H->d_tree_int, buf.size()));
+  CU(cudaMemcpy(H->d_tree_int, buf.data(), buf.size() * sizeof(int), cudaMemcpyHostToDevice));
+  TRY(dalloc(H, &H->d_lev_lofs, H->lev_lofs.size()));
+  CU(cudaMemcpy(H->d_lev_lofs, H->lev_lofs.data(), H->lev_lofs.size() * sizeof(long long), cudaMemcpyHostToDevice));
+  int* b = H->d_tree_int;
+  TreeDev& t = H->tree;
+  t.n = H->n; t.L = H->L; t.nleaf = H->nleaf;
+  t.node_r0 = b + o_r0; t.node_n1 = b + o_n1; t.node_n2 = b + o_n2; t.node_seg = b + o_ns;
+  t.leaf_r0 = b + o_lr; t.leaf_n = b + o_ln; t.seg_ofs = b + o_so; t.seg_node = b + o_sn;
+  t.seg_child = b + o_sc; t.seg_row0 = b + o_s0; t.seg_len = b + o_sl; t.lev_m = b + o_m;
+  t.lev_lofs = H->d_lev_lofs;
+  return FDE_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// compression plan: tasks (instance, level) cut into PC_ROWS chunks, packed into
+// cooperative launches that fit on the device at once.
+static int plan_compression(fde_hodlr* H, int capacity) {
+  H->tasks.clear(); H->chunks.clear(); H->launch_chunk0.clear();
+  int slot = 0, in_launch = 0;
+  H->launch_chunk0.push_back(0);
+  for (int b = 0; b < H->batch; ++b) {
+    for (int l = 0; l < H->L; ++l) {
+      const int m = H->lev_m[l];
+      const int G = (m + PC_ROWS - 1) / PC_ROWS;
+      if (G > capacity)
+        return set_err(FDE_EDIM, "n=%d too large: level %d needs %d co-resident CTAs (device holds %d)",
+                       H->n, l, G, capacity);
+      if (in_launch + G > capacity) { H->launch_chunk0.push_back((int)H->chunks.size()); in_launch = 0; }
+      PcTask tk{};
+      tk.inst = b; tk.level = l; tk.m = m; tk.G = G; tk.slot0 = slot;
+      tk.lraw_ofs = (long long)b * H->lraw_stride + H->lev_lraw[l];
+      tk.lf_ofs = (long long)b * H->lf_stride + H->lev_lofs[l];
+      tk.tau = H->tol * std::exp2(H->alpha[b]);         // reading R7: ||T||_2 <= 2^alpha
+      const int tid = (int)H->tasks.size();
+      H->tasks.push_back(tk);
+      for (int c = 0; c < G; ++c) {
+        PcChunk ch{tid, c * PC_ROWS, std::min(PC_ROWS, m - c * PC_ROWS), c};
+        H->chunks.push_back(ch);
+      }
+      slot += G;
+      in_launch += G;
+    }
+  }
+  H->launch_chunk0.push_back((int)H->chunks.size());
+  return FDE_OK;
+}
+
+static int run_compression(fde_hodlr* H, cudaStream_t s) {
+  if (H->L == 0) return FDE_OK;
+  const int ntask = (int)H->tasks.size();
+  CU(cudaMemsetAsync(H->d_ctr, 0, sizeof(unsigned) * ntask, s));
+  const size_t smem = (size_t)KRAW * PC_ROWS * sizeof(double);
+  for (size_t li = 0; li + 1 < H->launch_chunk0.size(); ++li) {
+    const int c0 = H->launch_chunk0[li], c1 = H->launch_chunk0[li + 1];
+    if (c1 <= c0) continue;
+    const PcTask* tasks = H->d_tasks;
+    const PcChunk* chunks = H->d_chunks + c0;
+    const double* g = H->d_g;
+    long long gs = H->gstride;
+    double* Lraw = H->d_Lraw;
+    int* tkr = H->d_task_kr;
+    unsigned* ctr = H->d_ctr;
+    double* part = H->d_part;
+    double* gp = H->d_gram_part;
+    double* gram = H->d_gram;
+    DevStatus* st = H->d_status;
+    void* args[] = {&tasks, &chunks, &g, &gs, &Lraw, &tkr, &ctr, &part, &gp, &gram, &st};
+    { PROF("k_pchol"); CU(cudaLaunchCooperativeKernel((void*)k_pchol, dim3(c1 - c0), dim3(PC_ROWS), args, smem, s)); }
+    LAUNCHED();
+  }
+  { PROF("k_eig"); k_eig<<<ntask, EIG_THREADS, 4 * KRAW * KRAW * sizeof(double), s>>>(
+      H->d_tasks, H->d_task_kr, H->d_gram, H->d_vkeep, H->d_task_rank, H->d_rank, H->L, H->d_status); }
+  LAUNCHED();
+  { PROF("k_ltransform"); k_ltransform<<<(int)H->chunks.size(), PC_ROWS, 0, s>>>(
+      H->d_tasks, H->d_chunks, H->d_task_kr, H->d_task_rank, H->d_vkeep, H->d_Lraw, H->d_Lf); }
+  LAUNCHED();
+  { PROF("k_colofs"); k_colofs<<<(H->batch + 127) / 128, 128, 0, s>>>(H->d_rank, H->d_colofs, H->L, H->batch); }
+  LAUNCHED();
+  return FDE_OK;
+}
+
+__global__ void k_cfac(const double* __restrict__ alpha, double dt, double h, double* __restrict__ c,
+                       int batch) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < batch) c[i] = dt / pow(h, alpha[i]);        // c = dt / h^alpha (Eq. 2.5)
+}
+
+static int set_dt(fde_hodlr* H, double dt, cudaStream_t s) {
+  H->dt = dt;
+  { PROF("k_cfac"); k_cfac<<<(H->batch + 127) / 128, 128, 0, s>>>(H->d_alpha, dt, H->h, H->d_cfac, H->batch); }
+  LAUNCHED();
+  return FDE_OK;
+}
+
+static bool g_attr_done = false;
+static int set_attrs() {
+  if (g_attr_done) return FDE_OK;
+  CU(cudaFuncSetAttribute(k_pchol, cudaFuncAttributeMaxDynamicSharedMemorySize, KRAW * PC_ROWS * 8));
+  CU(cudaFuncSetAttribute(k_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * KRAW * KRAW * 8));
+  CU(cudaFuncSetAttribute(k_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (LEAF_MAX * LDA_LEAF + NCHUNK * LDP_LEAF) * 8));
+  CU(cudaFuncSetAttribute(k_lvl_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_REDUCE));
+  CU(cudaFuncSetAttribute(k_lvl_node, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_NODE));
+  CU(cudaFuncSetAttribute(k_lvl_update, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_UPDATE));
+  CU(cudaFuncSetAttribute(k_mv_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_LEAF_SMEM));
+  CU(cudaFuncSetAttribute(k_mv_update, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MV_UPDATE));
+  g_attr_done = true;
+  return FDE_OK;
+}
+
+static int check_common(int batch, int n, const double* alpha, double h, double dt, double tol,
+                        int leaf) {
+  if (batch < 1) return set_err(FDE_EDOMAIN, "batch=%d must be >= 1", batch);
+  if (n < 1) return set_err(FDE_EDOMAIN, "n=%d must be >= 1", n);
+  if (!alpha) return set_err(FDE_EDOMAIN, "alpha is NULL");
+  for (int b = 0; b < batch; ++b)
+    if (!(alpha[b] > 1.0 && alpha[b] <= 2.0))
+      return set_err(FDE_EDOMAIN, "alpha[%d]=%g outside (1, 2]", b, alpha[b]);
+  if (!(h > 0.0) || !std::isfinite(h)) return set_err(FDE_EDOMAIN, "h=%g must be > 0", h);
+  if (!(dt >= 0.0) || !std::isfinite(dt)) return set_err(FDE_EDOMAIN, "dt=%g must be >= 0", dt);
+  if (!(tol > 0.0 && tol < 1.0)) return set_err(FDE_EDOMAIN, "tol=%g outside (0, 1)", tol);
+  if (leaf < 2 || leaf > LEAF_MAX) return set_err(FDE_EDOMAIN, "leaf=%d outside [2, %d]", leaf, LEAF_MAX);
+  return FDE_OK;
+}
+
+// d >= 0 check (FDE_CHECK)
+__global__ void k_check_nonneg(const double* __restrict__ a, long long cnt, int* __restrict__ bad) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < cnt && !(a[i] >= 0.0)) atomicExch(bad, 1);
+}
+
+static int check_nonneg(fde_hodlr* H, const double* dp, const double* dm, cudaStream_t s) {
+  int* bad = (int*)H->d_in;  // scratch (first 4 bytes of the staging area)
+  CU(cudaMemsetAsync(bad, 0, sizeof(int), s));
+  const long long cnt = (long long)H->batch * H->n;
+  { PROF("k_check_nonneg"); k_check_nonneg<<<(unsigned)((cnt + 255) / 256), 256, 0, s>>>(dp, cnt, bad); }
+  LAUNCHED();
+  { PROF("k_check_nonneg"); k_check_nonneg<<<(unsigned)((cnt + 255) / 256), 256, 0, s>>>(dm, cnt, bad); }
+  LAUNCHED();
+  int hb = 0;
+  CU(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  if (hb) return set_err(FDE_EDOMAIN, "d_plus / d_minus has a negative or non-finite entry (P:56)");
+  return FDE_OK;
+}
+
+static int sync_and_status(fde_hodlr* H, cudaStream_t s) {
+  CU(cudaStreamSynchronize(s));
+  DevStatus st{};
+  CU(cudaMemcpy(&st, H->d_status, sizeof(st), cudaMemcpyDeviceToHost));
+  if (st.code != FDE_OK)
+    return set_err(st.code, "device status %d at instance %d index %d", st.code, st.where / 65536,
+                   st.where % 65536);
+  return FDE_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+static int build_impl(int batch, int n, const double* alpha, double h, double dt, const double* dp,
+                      const double* dm, double shift, double tol, int leaf, unsigned flags,
+                      cudaStream_t s, fde_hodlr** out) {
+  TRY(check_common(batch, n, alpha, h, dt, tol, leaf));
+  if (!(shift > 0.0) || !std::isfinite(shift)) return set_err(FDE_EDOMAIN, "shift=%g must be > 0", shift);
+  if (!out) return set_err(FDE_EDOMAIN, "out is NULL");
+  TRY(set_attrs());
+  fde_hodlr* H = new fde_hodlr();
+  auto fail = [&](int rc) { free_handle(H); return rc; };
+  H->batch = batch; H->n = n; H->leaf = leaf; H->h = h; H->dt = dt; H->shift = shift; H->tol = tol;
+  H->alpha.assign(alpha, alpha + batch);
+  build_tree(H);
+  if (H->L > LMAX) return fail(set_err(FDE_EDIM, "tree depth %d exceeds %d", H->L, LMAX));
+  int rc;
+  if ((rc = upload_tree(H)) != FDE_OK) return fail(rc);
+  // capacity for the cooperative compression
+  int dev = 0, nsm = 0, per_sm = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pchol, PC_ROWS, KRAW * PC_ROWS * 8) != cudaSuccess)
+    return fail(set_err(FDE_ECUDA, "device query failed: %s", cudaGetErrorString(cudaGetLastError())));
+  if ((rc = plan_compression(H, std::max(1, nsm * per_sm))) != FDE_OK) return fail(rc);
+  const int L = H->L;
+  H->gstride = n + 2;
+  H->ncap = std::max(NRHS_MAX, 1 + L * KCAP);
+  H->xstride = (long long)n * (1 + L * KCAP);
+  H->lustride = (long long)n * LEAF_MAX;
+  H->pstride_seg = (long long)KCAP * H->ncap;
+  H->pstride_inst = (long long)std::max(1, H->max_seg) * H->pstride_seg;
+  H->sstride_node = (long long)SLD * H->ncap;
+  H->sstride_inst = (long long)H->max_nodes_lvl * H->sstride_node;
+  H->kstride_inst = (long long)std::max(1, H->nnodes) * 3 * KCAP * KCAP;
+  H->pivstride_inst = (long long)std::max(1, H->nnodes) * KCAP;
+  const size_t B = batch;
+  const size_t ntask = H->tasks.size(), nch = H->chunks.size();
+  if ((rc = dalloc(H, &H->d_alpha, B)) || (rc = dalloc(H, &H->d_cfac, B)) ||
+      (rc = dalloc(H, &H->d_g, B * H->gstride)) || (rc = dalloc(H, &H->d_Lf, B * H->lf_stride)) ||
+      (rc = dalloc(H, &H->d_Lraw, B * H->lraw_stride)) || (rc = dalloc(H, &H->d_rank, B * std::max(1, L))) ||
+      (rc = dalloc(H, &H->d_colofs, B * (L + 1))) || (rc = dalloc(H, &H->d_dp, B * n)) ||
+      (rc = dalloc(H, &H->d_dm, B * n)) || (rc = dalloc(H, &H->d_X, B * H->xstride)) ||
+      (rc = dalloc(H, &H->d_LU, B * H->lustride)) || (rc = dalloc(H, &H->d_P, B * H->pstride_inst)) ||
+      (rc = dalloc(H, &H->d_S, B * H->sstride_inst)) || (rc = dalloc(H, &H->d_K, B * H->kstride_inst)) ||
+      (rc = dalloc(H, &H->d_Kpiv, B * H->pivstride_inst)) ||
+      (rc = dalloc(H, &H->d_tasks, std::max<size_t>(1, ntask))) ||
+      (rc = dalloc(H, &H->d_chunks, std::max<size_t>(1, nch))) ||
+      (rc = dalloc(H, &H->d_ctr, std::max<size_t>(1, ntask))) ||
+      (rc = dalloc(H, &H->d_part, std::max<size_t>(1, nch) * 2 * PSTRIDE)) ||
+      (rc = dalloc(H, &H->d_gram_part, std::max<size_t>(1, nch) * KRAW * KRAW)) ||
+      (rc = dalloc(H, &H->d_gram, std::max<size_t>(1, ntask) * KRAW * KRAW)) ||
+      (rc = dalloc(H, &H->d_vkeep, std::max<size_t>(1, ntask) * KRAW * RCAP)) ||
+      (rc = dalloc(H, &H->d_task_kr, std::max<size_t>(1, ntask))) ||
+      (rc = dalloc(H, &H->d_task_rank, std::max<size_t>(1, ntask))) ||
+      (rc = dalloc(H, &H->d_status, 1)) || (rc = dalloc(H, &H->d_in, 5 * B * n + 8)))
+    return fail(rc);
+  H->d_rhs = H->d_in + 4 * B * n;
+  if (cudaMemcpy(H->d_alpha, alpha, B * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess ||
+      (ntask && cudaMemcpy(H->d_tasks, H->tasks.data(), ntask * sizeof(PcTask), cudaMemcpyHostToDevice) != cudaSuccess) ||
+      (nch && cudaMemcpy(H->d_chunks, H->chunks.data(), nch * sizeof(PcChunk), cudaMemcpyHostToDevice) != cudaSuccess))
+    return fail(set_err(FDE_ECUDA, "upload failed"));
+  if (cudaMemsetAsync(H->d_status, 0, sizeof(DevStatus), s) != cudaSuccess ||
+      cudaMemsetAsync(H->d_rank, 0, B * std::max(1, L) * sizeof(int), s) != cudaSuccess ||
+      cudaMemsetAsync(H->d_colofs, 0, B * (L + 1) * sizeof(int), s) != cudaSuccess)
+    return fail(set_err(FDE_ECUDA, "memset failed"));
+  if (dp && cudaMemcpyAsync(H->d_dp, dp, B * n * sizeof(double), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    return fail(set_err(FDE_ECUDA, "copy d_plus failed"));
+  if (dm && cudaMemcpyAsync(H->d_dm, dm, B * n * sizeof(double), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    return fail(set_err(FDE_ECUDA, "copy d_minus failed"));
+  if ((flags & FDE_CHECK) && dp && dm && (rc = check_nonneg(H, H->d_dp, H->d_dm, s)) != FDE_OK) return fail(rc);
+  if ((rc = set_dt(H, dt, s)) != FDE_OK) return fail(rc);
+  // S1: GL weights
+  { PROF("k_gl_weights"); k_gl_weights<<<batch, GL_THREADS, 0, s>>>(H->d_alpha, n + 2, H->d_g, H->gstride); }
+  if (cudaGetLastError() != cudaSuccess) return fail(set_err(FDE_ECUDA, "k_gl_weights launch failed"));
+  g_launches++;
+  // S2: compression
+  if ((rc = run_compression(H, s)) != FDE_OK) return fail(rc);
+  H->last_stream = s;
+  if ((flags & FDE_SYNC) && (rc = sync_and_status(H, s)) != FDE_OK) return fail(rc);
+  *out = H;
+  return FDE_OK;
+}
+
+// factor (nf = 0) or fused factor + solve of one rhs column (nf = 1: b = u + dt f -> u_next)
+static int factor_impl(fde_hodlr* H, const double* dp, const double* dm, int nf, const double* u_prev,
+                       const double* f, double* u_next, int keep, cudaStream_t s) {
+  const int L = H->L, B = H->batch;
+  if (L == 0 && nf == 0 && !keep) return FDE_OK;
+  LeafArgs la{};
+  la.tree = H->tree; la.mode = 0; la.shift = H->shift; la.cfac = H->d_cfac; la.dt = H->dt;
+  la.g = H->d_g; la.gstride = H->gstride; la.dp = dp; la.dm = dm;
+  la.Lf = H->d_Lf; la.lf_stride = H->lf_stride; la.rank = H->d_rank; la.colofs = H->d_colofs;
+  la.X = H->d_X; la.xstride = H->xstride; la.LU = H->d_LU; la.lustride = H->lustride;
+  la.keep = keep; la.nf = nf; la.u_prev = u_prev; la.f = f; la.st = H->d_status;
+  { PROF("k_leaf"); k_leaf<<<dim3(H->nleaf, B), LEAF_THREADS, (LEAF_MAX * LDA_LEAF + NCHUNK * LDP_LEAF) * 8, s>>>(la); }
+  LAUNCHED();
+  LevelArgs lv{};
+  lv.tree = H->tree; lv.mode = 0; lv.Lf = H->d_Lf; lv.lf_stride = H->lf_stride;
+  lv.rank = H->d_rank; lv.colofs = H->d_colofs; lv.X = H->d_X; lv.xstride = H->xstride;
+  lv.nf = nf; lv.Ppart = H->d_P; lv.pstride_seg = H->pstride_seg; lv.pstride_inst = H->pstride_inst;
+  lv.Sbuf = H->d_S; lv.sstride_node = H->sstride_node; lv.sstride_inst = H->sstride_inst;
+  lv.Kst = H->d_K; lv.kstride_node = 3LL * KCAP * KCAP; lv.kstride_inst = H->kstride_inst;
+  lv.Kpiv = H->d_Kpiv; lv.pivstride_inst = H->pivstride_inst; lv.keep = keep; lv.st = H->d_status;
+  for (int l = L - 1; l >= 0; --l) {
+    lv.level = l;
+    const int nseg = H->seg_ofs[l + 1] - H->seg_ofs[l];
+    { PROF("k_lvl_reduce"); k_lvl_reduce<<<dim3(nseg, B), LVL_THREADS, SMEM_REDUCE, s>>>(lv); }
+    LAUNCHED();
+    { PROF("k_lvl_node"); k_lvl_node<<<dim3(1 << l, B), LVL_THREADS, SMEM_NODE, s>>>(lv); }
+    LAUNCHED();
+    if (l > 0 || nf > 0) {
+      { PROF("k_lvl_update"); k_lvl_update<<<dim3(nseg, B), LVL_THREADS, SMEM_UPDATE, s>>>(lv); }
+      LAUNCHED();
+    }
+  }
+  if (nf) {
+    const long long tot = (long long)B * H->n;
+    { PROF("k_copy_col0"); k_copy_col0<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(H->d_X, H->xstride, H->n, u_next, B); }
+    LAUNCHED();
+  }
+  return FDE_OK;
+}
+
+// solve with the kept factor: y = A^{-1}(b + dt f) (f may be NULL), nrhs columns, ld
+static int solve_impl(fde_hodlr* H, const double* b, const double* f, double* y, int nrhs, int ld,
+                      cudaStream_t s) {
+  const int L = H->L, B = H->batch;
+  LeafArgs la{};
+  la.tree = H->tree; la.mode = 1; la.LU = H->d_LU; la.lustride = H->lustride;
+  la.b = b; la.y = y; la.nrhs = nrhs; la.ld = ld; la.f = f; la.dt = H->dt; la.st = H->d_status;
+  { PROF("k_leaf"); k_leaf<<<dim3(H->nleaf, B), LEAF_THREADS, (LEAF_MAX * LDA_LEAF + NCHUNK * LDP_LEAF) * 8, s>>>(la); }
+  LAUNCHED();
+  LevelArgs lv{};
+  lv.tree = H->tree; lv.mode = 1; lv.Lf = H->d_Lf; lv.lf_stride = H->lf_stride;
+  lv.rank = H->d_rank; lv.colofs = H->d_colofs; lv.X = H->d_X; lv.xstride = H->xstride;
+  lv.Y = y; lv.ld = ld; lv.nrhs = nrhs; lv.ystride = (long long)ld * nrhs;
+  lv.Ppart = H->d_P; lv.pstride_seg = H->pstride_seg; lv.pstride_inst = H->pstride_inst;
+  lv.Sbuf = H->d_S; lv.sstride_node = H->sstride_node; lv.sstride_inst = H->sstride_inst;
+  lv.Kst = H->d_K; lv.kstride_node = 3LL * KCAP * KCAP; lv.kstride_inst = H->kstride_inst;
+  lv.Kpiv = H->d_Kpiv; lv.pivstride_inst = H->pivstride_inst; lv.keep = 1; lv.st = H->d_status;
+  for (int l = L - 1; l >= 0; --l) {
+    lv.level = l;
+    const int nseg = H->seg_ofs[l + 1] - H->seg_ofs[l];
+    { PROF("k_lvl_reduce"); k_lvl_reduce<<<dim3(nseg, B), LVL_THREADS, SMEM_REDUCE, s>>>(lv); }
+    LAUNCHED();
+    { PROF("k_lvl_node"); k_lvl_node<<<dim3(1 << l, B), LVL_THREADS, SMEM_NODE, s>>>(lv); }
+    LAUNCHED();
+    { PROF("k_lvl_update"); k_lvl_update<<<dim3(nseg, B), LVL_THREADS, SMEM_UPDATE, s>>>(lv); }
+    LAUNCHED();
+  }
+  return FDE_OK;
+}
+
+// y = A x with the HODLR representation
+static int matvec_impl(fde_hodlr* H, const double* x, double* y, int nrhs, int ld, cudaStream_t s) {
+  const int L = H->L, B = H->batch;
+  MvArgs ma{};
+  ma.tree = H->tree; ma.shift = H->shift; ma.cfac = H->d_cfac; ma.g = H->d_g; ma.gstride = H->gstride;
+  ma.dp = H->d_dp; ma.dm = H->d_dm; ma.Lf = H->d_Lf; ma.lf_stride = H->lf_stride; ma.rank = H->d_rank;
+  ma.x = x; ma.y = y; ma.nrhs = nrhs; ma.ld = ld; ma.ystride = (long long)ld * nrhs;
+  ma.Ppart = H->d_P; ma.pstride_seg = H->pstride_seg; ma.pstride_inst = H->pstride_inst;
+  { PROF("k_mv_leaf"); k_mv_leaf<<<dim3(H->nleaf, B), MV_THREADS, MV_LEAF_SMEM, s>>>(ma); }
+  LAUNCHED();
+  LevelArgs lv{};
+  lv.tree = H->tree; lv.mode = 1; lv.Lf = H->d_Lf; lv.lf_stride = H->lf_stride;
+  lv.rank = H->d_rank; lv.colofs = H->d_colofs;
+  lv.Y = const_cast<double*>(x); lv.ld = ld; lv.nrhs = nrhs; lv.ystride = (long long)ld * nrhs;
+  lv.Ppart = H->d_P; lv.pstride_seg = H->pstride_seg; lv.pstride_inst = H->pstride_inst;
+  for (int l = L - 1; l >= 0; --l) {
+    // levels are independent for a product, but the partial buffer is shared: sequential
+    lv.level = l; ma.level = l;
+    const int nseg = H->seg_ofs[l + 1] - H->seg_ofs[l];
+    { PROF("k_lvl_reduce"); k_lvl_reduce<<<dim3(nseg, B), LVL_THREADS, SMEM_REDUCE, s>>>(lv); }
+    LAUNCHED();
+    { PROF("k_mv_update"); k_mv_update<<<dim3(nseg, B), MV_THREADS, SMEM_MV_UPDATE, s>>>(ma); }
+    LAUNCHED();
+  }
+  return FDE_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// C-ABI
+extern "C" {
+
+const char* fde_last_error(void) { return g_last_error.c_str(); }
+
+void fde_profile_enable(int on) {
+  if (!on) {
+    for (auto& r : g_prof_recs) { g_ev_free.push_back(r.a); g_ev_free.push_back(r.b); }
+    g_prof_recs.clear();
+  }
+  g_prof = on != 0;
+}
+
+int fde_profile_dump(char* buf, int len) {
+  // aggregate per kernel name: {"name": [launches, total_ms], ...}; clears the records
+  std::vector<std::pair<std::string, std::pair<long long, double>>> agg;
+  for (auto& r : g_prof_recs) {
+    cudaEventSynchronize(r.b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    bool found = false;
+    for (auto& e : agg)
+      if (e.first == r.name) { e.second.first++; e.second.second += ms; found = true; break; }
+    if (!found) agg.push_back({r.name, {1, (double)ms}});
+    g_ev_free.push_back(r.a);
+    g_ev_free.push_back(r.b);
+  }
+  g_prof_recs.clear();
+  std::string out = "{";
+  for (size_t i = 0; i < agg.size(); ++i) {
+    char tmp[256];
+    snprintf(tmp, sizeof(tmp), "%s\"%s\": [%lld, %.6f]", i ? ", " : "", agg[i].first.c_str(),
+             agg[i].second.first, agg[i].second.second);
+    out += tmp;
+  }
+  out += "}";
+  if (!buf || len <= (int)out.size()) return -(int)out.size() - 1;
+  memcpy(buf, out.c_str(), out.size() + 1);
+  return (int)out.size();
+}
+long long fde_launch_count(void) { return g_launches.load(); }
+
+int hodlr_build(int batch, int n, const double* alpha, double h, double dt, const double* d_plus,
+                const double* d_minus, double shift, double tol, int leaf, unsigned flags, void* stream,
+                fde_hodlr_t* out) {
+  g_last_error.clear();
+  if (!d_plus || !d_minus) return set_err(FDE_EDOMAIN, "d_plus / d_minus is NULL");
+  return build_impl(batch, n, alpha, h, dt, d_plus, d_minus, shift, tol, leaf, flags,
+                    (cudaStream_t)stream, out);
+}
+
+int hodlr_update(fde_hodlr_t H, double dt, const double* d_plus, const double* d_minus, unsigned flags,
+                 void* stream) {
+  g_last_error.clear();
+  if (!H) return set_err(FDE_EDOMAIN, "handle is NULL");
+  if (!(dt >= 0.0) || !std::isfinite(dt)) return set_err(FDE_EDOMAIN, "dt=%g must be >= 0", dt);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t bytes = (size_t)H->batch * H->n * sizeof(double);
+  if (d_plus) CU(cudaMemcpyAsync(H->d_dp, d_plus, bytes, cudaMemcpyDeviceToDevice, s));
+  if (d_minus) CU(cudaMemcpyAsync(H->d_dm, d_minus, bytes, cudaMemcpyDeviceToDevice, s));
+  if (flags & FDE_CHECK) TRY(check_nonneg(H, H->d_dp, H->d_dm, s));
+  TRY(set_dt(H, dt, s));
+  H->factored = false;
+  H->last_stream = s;
+  if (flags & FDE_SYNC) return sync_and_status(H, s);
+  return FDE_OK;
+}
+
+int hodlr_factor(fde_hodlr_t H, unsigned flags, void* stream) {
+  g_last_error.clear();
+  if (!H) return set_err(FDE_EDOMAIN, "handle is NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  TRY(factor_impl(H, H->d_dp, H->d_dm, 0, nullptr, nullptr, nullptr, 1, s));
+  H->factored = true;
+  H->last_stream = s;
+  if (flags & FDE_SYNC) return sync_and_status(H, s);
+  return FDE_OK;
+}
+
+int hodlr_solve(fde_hodlr_t H, const double* b, double* x, int nrhs, int ld, unsigned flags, void* stream) {
+  g_last_error.clear();
+  if (!H) return set_err(FDE_EDOMAIN, "handle is NULL");
+  if (!H->factored) return set_err(FDE_EDOMAIN, "hodlr_solve before hodlr_factor");
+  if (!b || !x) return set_err(FDE_EDOMAIN, "b / x is NULL");
+  if (nrhs < 1 || nrhs > NRHS_MAX) return set_err(FDE_EDIM, "nrhs=%d outside [1, %d]", nrhs, NRHS_MAX);
+  if (ld < H->n) return set_err(FDE_EDIM, "ld=%d < n=%d", ld, H->n);
+  cudaStream_t s = (cudaStream_t)stream;
+  TRY(solve_impl(H, b, nullptr, x, nrhs, ld, s));
+  H->last_stream = s;
+  if (flags & FDE_SYNC) return sync_and_status(H, s);
+  return FDE_OK;
+}
+
+int hodlr_matvec(fde_hodlr_t H, const double* x, double* y, int nrhs, int ld, unsigned flags, void* stream) {
+  g_last_error.clear();
+  if (!H) return set_err(FDE_EDOMAIN, "handle is NULL");
+  if (!x || !y) return set_err(FDE_EDOMAIN, "x / y is NULL");
+  if (x == y) return set_err(FDE_EDOMAIN, "y must not alias x");
+  if (nrhs < 1 || nrhs > NRHS_MAX) return set_err(FDE_EDIM, "nrhs=%d outside [1, %d]", nrhs, NRHS_MAX);
+  if (ld < H->n) return set_err(FDE_EDIM, "ld=%d < n=%d", ld, H->n);
+  cudaStream_t s = (cudaStream_t)stream;
+  TRY(matvec_impl(H, x, y, nrhs, ld, s));
+  H->last_stream = s;
+  if (flags & FDE_SYNC) return sync_and_status(H, s);
+  return FDE_OK;
+}
+
+int hodlr_status(fde_hodlr_t H, int* where) {
+  if (!H) return set_err(FDE_EDOMAIN, "handle is NULL");
+  DevStatus st{};
+  CU(cudaStreamSynchronize(H->last_stream));
+  CU(cudaMemcpy(&st, H->d_status, sizeof(st), cudaMemcpyDeviceToHost));
+  if (where) *where = st.where;
+  return st.code;
+}
+
+int hodlr_ranks(fde_hodlr_t H, int inst, int* ranks, int max_levels, int* levels) {
+  if (!H) return set_err(FDE_EDOMAIN, "handle is NULL");
+  if (inst < 0 || inst >= H->batch) return set_err(FDE_EDOMAIN, "inst=%d outside [0, %d)", inst, H->batch);
+  if (levels) *levels = H->L;
+  if (H->L == 0) return FDE_OK;
+  if (!ranks || max_levels < H->L) return set_err(FDE_EDIM, "ranks buffer holds %d < L=%d", max_levels, H->L);
+  CU(cudaStreamSynchronize(H->last_stream));
+  CU(cudaMemcpy(ranks, H->d_rank + (size_t)inst * H->L, H->L * sizeof(int), cudaMemcpyDeviceToHost));
+  return FDE_OK;
+}
+
+void hodlr_destroy(fde_hodlr_t H) {
+  if (!H) return;
+  cudaStreamSynchronize(H->last_stream);
+  free_handle(H);
+}
+
+int fde1d_step(int batch, int n, const double* alpha, double h, double dt, const double* d_plus_m,
+               const double* d_minus_m, const double* f_m, const double* u_prev, double* u_next, double tol,
+               int leaf, int coeffs_changed, unsigned flags, fde_hodlr_t* cache, void* stream) {
+  g_last_error.clear();
+  TRY(check_common(batch, n, alpha, h, dt, tol, leaf));
+  if (!d_plus_m || !d_minus_m || !f_m || !u_prev || !u_next)
+    return set_err(FDE_EDOMAIN, "NULL array argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  fde_hodlr* H = cache ? *cache : nullptr;
+  bool fresh = false;
+  if (H) {
+    bool same = H->batch == batch && H->n == n && H->h == h && H->leaf == leaf && H->tol == tol &&
+                H->shift == 1.0;
+    for (int b = 0; same && b < batch; ++b) same = H->alpha[b] == alpha[b];
+    if (!same) { hodlr_destroy(H); H = nullptr; if (cache) *cache = nullptr; }
+  }
+  const size_t cnt = (size_t)batch * n, bytes = cnt * sizeof(double);
+  const double *dp = d_plus_m, *dm = d_minus_m, *f = f_m, *u = u_prev;
+  double* un = u_next;
+  if (!H) {
+    TRY(build_impl(batch, n, alpha, h, dt, nullptr, nullptr, 1.0, tol, leaf, 0, s, &H));
+    fresh = true;
+    if (cache) *cache = H;
+  }
+  if (flags & FDE_HOST_PTRS) {
+    double* st = H->d_in;
+    CU(cudaMemcpyAsync(st, d_plus_m, bytes, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(st + cnt, d_minus_m, bytes, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(st + 2 * cnt, f_m, bytes, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(st + 3 * cnt, u_prev, bytes, cudaMemcpyHostToDevice, s));
+    dp = st; dm = st + cnt; f = st + 2 * cnt; u = st + 3 * cnt;
+    un = st + 3 * cnt;                                     // in place in the staging area
+  }
+  if ((flags & FDE_CHECK)) TRY(check_nonneg(H, dp, dm, s));
+  if ((flags & FDE_RECOMPRESS) && !fresh) {               // S1 + S2 again, same workspaces
+    { PROF("k_gl_weights"); k_gl_weights<<<batch, GL_THREADS, 0, s>>>(H->d_alpha, n + 2, H->d_g, H->gstride); }
+    LAUNCHED();
+    TRY(run_compression(H, s));
+  }
+  int rc;
+  if (coeffs_changed || fresh || !H->factored || H->dt != dt) {   // A_m depends on dt too
+    if (H->dt != dt || fresh) TRY(set_dt(H, dt, s));
+    const int keep = (flags & FDE_NO_KEEP) ? 0 : 1;
+    rc = factor_impl(H, dp, dm, 1, u, f, un, keep, s);
+    H->factored = keep && rc == FDE_OK;
+  } else {
+    rc = solve_impl(H, u, f, un, 1, n, s);                 // LU reuse
+  }
+  if (rc != FDE_OK) { if (!cache) hodlr_destroy(H); return rc; }
+  if (flags & FDE_HOST_PTRS) CU(cudaMemcpyAsync(u_next, un, bytes, cudaMemcpyDeviceToHost, s));
+  H->last_stream = s;
+  if ((flags & FDE_SYNC) || !cache || (flags & FDE_HOST_PTRS)) rc = sync_and_status(H, s);
+  if (!cache) hodlr_destroy(H);
+  return rc;
+}
+
+}  // extern "C"
+
+#include "fde2d.cuh"

@@ -1,0 +1,144 @@
+"""Thin Python binding over the C-ABI (include/fdehodlr.h): argument marshalling only.
+
+Tensors supply device pointers (``data_ptr()``) and torch supplies the current CUDA stream;
+every step of the method runs in the CUDA kernels of ``csrc/``.  There is no CPU path.
+"""
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check, FDE_SYNC, FDE_CHECK, FDE_HOST_PTRS, FDE_NO_KEEP, FDE_RECOMPRESS  # noqa: F401
+
+
+def _stream(stream=None):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _dev(t, name, numel=None):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64:
+        raise TypeError("%s must be a CUDA float64 tensor" % name)
+    if not t.is_contiguous():
+        raise ValueError("%s must be contiguous" % name)
+    if numel is not None and t.numel() != numel:
+        raise ValueError("%s has %d elements, expected %d" % (name, t.numel(), numel))
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _alpha_arr(alpha, batch):
+    a = np.ascontiguousarray(np.broadcast_to(np.asarray(alpha, dtype=np.float64), (batch,)))
+    return a, a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+class Hodlr:
+    """HODLR representation + factor of  A_b = shift I + (dt/h^alpha_b)(D+ T + D- T^T)."""
+
+    def __init__(self, n, alpha, h, dt, d_plus, d_minus, tol, leaf, shift=1.0, batch=1,
+                 flags=0, stream=None):
+        lib = _lib.load()
+        self.n, self.batch = n, batch
+        self._alpha, ap = _alpha_arr(alpha, batch)
+        self._h = ctypes.c_void_p()
+        check(lib.hodlr_build(batch, n, ap, h, dt, _dev(d_plus, "d_plus", batch * n),
+                              _dev(d_minus, "d_minus", batch * n), shift, tol, leaf, flags,
+                              _stream(stream), ctypes.byref(self._h)))
+
+    def update(self, dt, d_plus=None, d_minus=None, flags=0, stream=None):
+        dp = _dev(d_plus, "d_plus", self.batch * self.n) if d_plus is not None else None
+        dm = _dev(d_minus, "d_minus", self.batch * self.n) if d_minus is not None else None
+        check(_lib.load().hodlr_update(self._h, dt, dp, dm, flags, _stream(stream)))
+
+    def factor(self, flags=0, stream=None):
+        check(_lib.load().hodlr_factor(self._h, flags, _stream(stream)))
+
+    def solve(self, b, x=None, flags=0, stream=None):
+        """b: (batch, nrhs, n) or (batch, n) CUDA float64; returns x (may be b)."""
+        if x is None:
+            x = torch.empty_like(b)
+        nrhs = 1 if b.dim() <= 2 else b.shape[-2]
+        check(_lib.load().hodlr_solve(self._h, _dev(b, "b"), _dev(x, "x", b.numel()), nrhs,
+                                      self.n, flags, _stream(stream)))
+        return x
+
+    def matvec(self, x, y=None, flags=0, stream=None):
+        if y is None:
+            y = torch.empty_like(x)
+        nrhs = 1 if x.dim() <= 2 else x.shape[-2]
+        check(_lib.load().hodlr_matvec(self._h, _dev(x, "x"), _dev(y, "y", x.numel()), nrhs,
+                                       self.n, flags, _stream(stream)))
+        return y
+
+    def status(self):
+        where = ctypes.c_int()
+        return _lib.load().hodlr_status(self._h, ctypes.byref(where)), where.value
+
+    def ranks(self, inst=0):
+        buf = (ctypes.c_int * 64)()
+        levels = ctypes.c_int()
+        check(_lib.load().hodlr_ranks(self._h, inst, buf, 64, ctypes.byref(levels)))
+        return [buf[i] for i in range(levels.value)]
+
+    def close(self):
+        if self._h:
+            _lib.load().hodlr_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Fde1dStepper:
+    """Implicit-Euler stepper (Eq. 2.5) over fde1d_step with a cached handle."""
+
+    def __init__(self, n, alpha, h, tol, leaf, batch=1):
+        self.n, self.batch, self.h, self.tol, self.leaf = n, batch, h, tol, leaf
+        self._alpha, self._ap = _alpha_arr(alpha, batch)
+        self._cache = ctypes.c_void_p()
+
+    def step(self, dt, d_plus, d_minus, f, u_prev, u_next=None, coeffs_changed=True, flags=0,
+             stream=None):
+        cnt = self.batch * self.n
+        host = bool(flags & FDE_HOST_PTRS)
+        if u_next is None:
+            u_next = torch.empty_like(u_prev)
+
+        def ptr(t, name):
+            if host:
+                if t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous() or t.numel() != cnt:
+                    raise TypeError("%s must be a contiguous CPU float64 tensor of %d" % (name, cnt))
+                return ctypes.c_void_p(t.data_ptr())
+            return _dev(t, name, cnt)
+
+        check(_lib.load().fde1d_step(self.batch, self.n, self._ap, self.h, dt,
+                                     ptr(d_plus, "d_plus"), ptr(d_minus, "d_minus"), ptr(f, "f"),
+                                     ptr(u_prev, "u_prev"), ptr(u_next, "u_next"), self.tol,
+                                     self.leaf, int(bool(coeffs_changed)), flags,
+                                     ctypes.byref(self._cache), _stream(stream)))
+        return u_next
+
+    def ranks(self, inst=0):
+        buf = (ctypes.c_int * 64)()
+        levels = ctypes.c_int()
+        check(_lib.load().hodlr_ranks(self._cache, inst, buf, 64, ctypes.byref(levels)))
+        return [buf[i] for i in range(levels.value)]
+
+    def close(self):
+        if self._cache:
+            _lib.load().hodlr_destroy(self._cache)
+            self._cache = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def launch_count():
+    return _lib.load().fde_launch_count()

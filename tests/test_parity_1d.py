@@ -1,0 +1,259 @@
+"""GPU <-> oracle parity for the 1D path (S1-S7) through the C-ABI.
+
+Bar (BASELINE north_star): relative 2-norm error <= 1e-8 per time step at truncation tol
+1e-12 against the dense oracle.  At tol 1e-10 / n = 65536 (cfg3) no dense oracle exists
+and the forward error is set by conditioning (reading R16): there the bar is the
+backward error eta <= 1e-10 from the FFT residual of the exact operator."""
+import numpy as np
+import pytest
+import torch
+
+from oracle.fd1d import assemble_A, step_dense, backward_error, toeplitz_matvec_fft
+from oracle.compress import level_ranks, hodlr_levels
+from paper_1804_05522_b200 import workloads as W
+
+gpu = pytest.mark.gpu
+DEV = "cuda"
+
+
+def _t(a):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device=DEV)
+
+
+def _stepper(wl):
+    from paper_1804_05522_b200.hodlr import Fde1dStepper
+    return Fde1dStepper(wl.n, wl.alpha, wl.h, wl.tol, wl.leaf, batch=wl.batch)
+
+
+def _gpu_step(st, wl, m, u_prev, coeffs_changed=True, flags=0):
+    dp, dm = wl.coeffs(m)
+    out = st.step(wl.dt, _t(dp), _t(dm), _t(wl.source(m)), _t(u_prev),
+                  coeffs_changed=coeffs_changed, flags=flags)
+    torch.cuda.synchronize()
+    return out.cpu().numpy().reshape(wl.batch, wl.n)
+
+
+def _oracle_step(wl, m, u_prev, b=0):
+    dp, dm = wl.coeffs(m)
+    A = assemble_A(float(wl.alpha[b]), wl.n, wl.h, wl.dt, dp[b], dm[b])
+    u, _ = step_dense(A, u_prev[b], wl.source(m)[b], wl.dt)
+    return u
+
+
+def _rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+CASES = [  # n, alpha, leaf, tol, kind
+    (256, 1.5, 32, 1e-12, "smooth"),
+    (300, 1.3, 40, 1e-12, "smooth"),       # ragged leaves and segments
+    (1000, 1.7, 64, 1e-12, "smooth"),
+    (1001, 1.9, 100, 1e-12, "smooth"),
+    (513, 1.1, 16, 1e-12, "smooth"),       # deep tree, small leaves
+    (2048, 1.6, 128, 1e-12, "smooth"),
+    (100, 1.5, 128, 1e-12, "smooth"),      # single leaf (L = 0)
+    (1, 1.5, 2, 1e-12, "smooth"),          # n = 1
+    (257, 2.0, 32, 1e-12, "smooth"),       # classical limit
+]
+
+
+@gpu
+@pytest.mark.parametrize("n,alpha,leaf,tol,kind", CASES)
+def test_one_step_shared_input(n, alpha, leaf, tol, kind):
+    wl = W.make_1d(n, alpha, leaf, tol, K=3, kind=kind)
+    st = _stepper(wl)
+    u = wl.u0
+    for m in (1, 2, 3):
+        ug = _gpu_step(st, wl, m, u)
+        uo = _oracle_step(wl, m, u)
+        assert _rel(ug[0], uo) <= 1e-8, (m, _rel(ug[0], uo))
+        u = uo[None]                         # shared input for the next step
+    st.close()
+
+
+@gpu
+@pytest.mark.parametrize("n,alpha,leaf,tol", [(512, 1.5, 32, 1e-12), (1000, 1.3, 64, 1e-10),
+                                               (4096, 1.8, 128, 1e-12), (777, 1.1, 50, 1e-8)])
+def test_ranks_equal_truncated_svd(n, alpha, leaf, tol):
+    """S2: the kept rank per level equals the truncated-SVD rank of the oracle."""
+    wl = W.make_1d(n, alpha, leaf, tol, K=1)
+    st = _stepper(wl)
+    _gpu_step(st, wl, 1, wl.u0)
+    got = st.ranks()
+    want = level_ranks(alpha, n, leaf, tol)
+    assert len(got) == len(hodlr_levels(n, leaf))
+    assert all(abs(g - w) <= 1 for g, w in zip(got, want)), (got, want)
+    assert sum(g == w for g, w in zip(got, want)) >= len(want) - 1, (got, want)
+    st.close()
+
+
+@gpu
+def test_cfg1_trajectory():
+    """cfg1: 8 steps, each side propagating its own state, relative error <= 1e-8 per step."""
+    wl = W.cfg1()
+    st = _stepper(wl)
+    ug, uo = wl.u0, wl.u0
+    for m in range(1, wl.K + 1):
+        ug = _gpu_step(st, wl, m, ug, coeffs_changed=(m == 1))      # d+- time-invariant
+        uo = _oracle_step(wl, m, uo)[None]
+        assert _rel(ug[0], uo[0]) <= 1e-8, (m, _rel(ug[0], uo[0]))
+    st.close()
+
+
+@gpu
+def test_cfg2_steps():
+    """cfg2 (n = 4096, time-dependent d+-, refactor every step): first 4 steps of the trajectory."""
+    wl = W.cfg2(K=4)
+    st = _stepper(wl)
+    ug, uo = wl.u0, wl.u0
+    for m in range(1, 5):
+        ug = _gpu_step(st, wl, m, ug)
+        uo = _oracle_step(wl, m, uo)[None]
+        assert _rel(ug[0], uo[0]) <= 1e-8, (m, _rel(ug[0], uo[0]))
+    st.close()
+
+
+@gpu
+def test_lu_reuse_matches_refactor():
+    wl = W.make_1d(1000, 1.6, 64, 1e-12, K=3, kind="const")
+    a, b = _stepper(wl), _stepper(wl)
+    ua = ub = wl.u0
+    for m in (1, 2, 3):
+        ua = _gpu_step(a, wl, m, ua, coeffs_changed=(m == 1))
+        ub = _gpu_step(b, wl, m, ub, coeffs_changed=True)
+        np.testing.assert_allclose(ua, ub, rtol=1e-13, atol=1e-15)
+    a.close(); b.close()
+
+
+@gpu
+def test_deterministic():
+    wl = W.make_1d(3000, 1.4, 128, 1e-12, K=1)
+    r1 = _gpu_step(_stepper(wl), wl, 1, wl.u0)
+    r2 = _gpu_step(_stepper(wl), wl, 1, wl.u0)
+    assert np.array_equal(r1, r2)
+
+
+@gpu
+def test_special_cases():
+    n = 700
+    wl = W.make_1d(n, 1.5, 64, 1e-12, K=1)
+    st = _stepper(wl)
+    u = wl.u0
+    dp, dm = wl.coeffs(1)
+    f = wl.source(1)
+    # dt = 0  =>  A = I, u_next = u_prev exactly
+    out = st.step(0.0, _t(dp), _t(dm), _t(f), _t(u)).cpu().numpy()
+    assert np.array_equal(out.reshape(1, n), u)
+    # d+- = 0  =>  u_next = u_prev + dt f
+    z = np.zeros_like(dp)
+    out = st.step(0.25, _t(z), _t(z), _t(f), _t(u)).cpu().numpy()
+    np.testing.assert_allclose(out.reshape(1, n), u + 0.25 * f, rtol=1e-15, atol=1e-15)
+    # f = 0, u0 = 0  =>  0
+    out = st.step(0.25, _t(dp), _t(dm), _t(0 * f), _t(0 * u)).cpu().numpy()
+    assert np.all(out == 0)
+    st.close()
+
+
+@gpu
+def test_maximum_principle():
+    wl = W.make_1d(1500, 1.3, 128, 1e-12, K=4)
+    wl.f = np.abs(wl.f)
+    st = _stepper(wl)
+    u = np.abs(wl.u0)
+    for m in range(1, 5):
+        u = _gpu_step(st, wl, m, u)
+        assert u.min() >= -1e-8 * np.abs(u).max()
+    st.close()
+
+
+@gpu
+def test_batched_instances_differ_in_alpha():
+    """cfg4 shape: independent instances with their own alpha in one launch."""
+    n, batch = 600, 5
+    wl = W.make_1d(n, np.linspace(1.1, 1.9, batch), 64, 1e-12, K=1, batch=batch)
+    wl.d_plus = wl.d_plus[:1]; wl.d_minus = wl.d_minus[:1]; wl.f = wl.f[:1]
+    st = _stepper(wl)
+    ug = _gpu_step(st, wl, 1, wl.u0)
+    for b in range(batch):
+        uo = _oracle_step(wl, 1, wl.u0, b)
+        assert _rel(ug[b], uo) <= 1e-8, (b, _rel(ug[b], uo))
+    st.close()
+
+
+@gpu
+def test_host_pointer_path_matches_device_path():
+    from paper_1804_05522_b200.hodlr import FDE_HOST_PTRS
+    wl = W.make_1d(900, 1.6, 64, 1e-12, K=1)
+    dp, dm = wl.coeffs(1)
+    st = _stepper(wl)
+    dev = _gpu_step(st, wl, 1, wl.u0)
+    st2 = _stepper(wl)
+    c = lambda a: torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64).pin_memory()
+    out = torch.empty(900, dtype=torch.float64).pin_memory()
+    st2.step(wl.dt, c(dp), c(dm), c(wl.source(1)), c(wl.u0), u_next=out, flags=FDE_HOST_PTRS)
+    assert np.array_equal(out.numpy(), dev[0])
+    st.close(); st2.close()
+
+
+@gpu
+def test_hodlr_solve_and_matvec_multi_rhs():
+    from paper_1804_05522_b200.hodlr import Hodlr
+    n, alpha, leaf = 1200, 1.7, 64
+    h, dt = 1.0 / (n + 1), 0.05
+    x = h * np.arange(1, n + 1)
+    dp, dm = 1 + x, 2 - x ** 2
+    H = Hodlr(n, alpha, h, dt, _t(dp), _t(dm), 1e-12, leaf)
+    H.factor()
+    rng = np.random.default_rng(0)
+    B = rng.standard_normal((5, n))
+    Xg = H.solve(_t(B)[None]).cpu().numpy()[0]          # (batch, nrhs, n)
+    A = assemble_A(alpha, n, h, dt, dp, dm)
+    Xo = np.linalg.solve(A, B.T).T
+    for j in range(5):
+        assert _rel(Xg[j], Xo[j]) <= 1e-8
+    Yg = H.matvec(_t(B)[None]).cpu().numpy()[0]
+    Yo = (A @ B.T).T
+    for j in range(5):
+        assert _rel(Yg[j], Yo[j]) <= 1e-10
+    # aliasing x = b
+    Bt = _t(B)[None].contiguous()
+    H.solve(Bt, Bt)
+    np.testing.assert_array_equal(Bt.cpu().numpy()[0], Xg)
+    H.close()
+
+
+@gpu
+def test_cfg3_full_size_backward_error():
+    """cfg3 at full size (n = 65536, tol 1e-10, leaf 128): eta <= 1e-10 for two steps."""
+    wl = W.cfg3(K=2)
+    st = _stepper(wl)
+    u = wl.u0
+    for m in (1, 2):
+        un = _gpu_step(st, wl, m, u)
+        dp, dm = wl.coeffs(m)
+        b = u[0] + wl.dt * wl.source(m)[0]
+        be = backward_error(float(wl.alpha[0]), wl.h, wl.dt, dp[0], dm[0], un[0], b)
+        assert be["eta"] <= 1e-10, be
+        u = un
+    st.close()
+
+
+@gpu
+def test_cfg4_sampled_instances():
+    """cfg4 shape at full size (batch 512, n = 8192): dense oracle on sampled instances
+    (the alpha extremes + 2 seeded picks), eta on all instances."""
+    wl = W.cfg4()
+    st = _stepper(wl)
+    ug = _gpu_step(st, wl, 1, wl.u0)
+    picks = [int(np.argmax(wl.alpha)), int(np.argmin(wl.alpha))]
+    picks += [int(i) for i in np.random.default_rng(40).choice(512, 2, replace=False)]
+    for b in picks:
+        uo = _oracle_step(wl, 1, wl.u0, b)
+        assert _rel(ug[b], uo) <= 1e-8, (b, wl.alpha[b], _rel(ug[b], uo))
+    dp, dm = wl.coeffs(1)
+    f = wl.source(1)
+    for b in range(0, 512, 7):
+        be = backward_error(float(wl.alpha[b]), wl.h, wl.dt, dp[b], dm[b], ug[b], wl.dt * f[b])
+        assert be["eta"] <= 1e-12, (b, be)
+    st.close()
