@@ -14,6 +14,7 @@
 #include "k_compress.cuh"
 #include "k_leaf.cuh"
 #include "k_level.cuh"
+#include "k_levels.cuh"
 #include "k_matvec.cuh"
 
 // ---------------------------------------------------------------------------------------
@@ -110,11 +111,19 @@ struct fde_hodlr {
   double *d_Lf = nullptr, *d_Lraw = nullptr;
   int *d_rank = nullptr, *d_colofs = nullptr;
   double *d_dp = nullptr, *d_dm = nullptr;
-  double *d_X = nullptr, *d_LU = nullptr, *d_P = nullptr, *d_S = nullptr, *d_K = nullptr;
-  int* d_Kpiv = nullptr;
+  double *d_X = nullptr, *d_LU = nullptr, *d_P = nullptr;
   long long gstride = 0, xstride = 0, lustride = 0, pstride_seg = 0, pstride_inst = 0;
-  long long sstride_node = 0, sstride_inst = 0, kstride_inst = 0, pivstride_inst = 0;
   int ncap = 0;
+  // level layout (host-known after the compression): k_l = max rank over the batch + 1
+  bool layout_done = false;
+  std::vector<int> kl, xcol;
+  std::vector<long long> kofs;
+  long long kstride_inst = 0, sum_half = 0;
+  int sum_nc = 0, kmax = 0, p = 0, P = 1, coop_capacity = 1;
+  double *d_Kst = nullptr, *d_sums = nullptr, *d_lvpart = nullptr;
+  unsigned* d_bar = nullptr;
+  int* d_post = nullptr;
+  int npost = 0;
   // compression scratch
   PcTask* d_tasks = nullptr;
   PcChunk* d_chunks = nullptr;
@@ -341,6 +350,9 @@ static int set_attrs() {
   CU(cudaFuncSetAttribute(k_lvl_update, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_UPDATE));
   CU(cudaFuncSetAttribute(k_mv_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_LEAF_SMEM));
   CU(cudaFuncSetAttribute(k_mv_update, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MV_UPDATE));
+  CU(cudaFuncSetAttribute(k_levels<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, LV_SMEM_MAX));
+  CU(cudaFuncSetAttribute(k_levels<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, LV_SMEM_MAX));
+  CU(cudaFuncSetAttribute(k_levels<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, LV_SMEM_MAX));
   g_attr_done = true;
   return FDE_OK;
 }
@@ -392,6 +404,174 @@ static int sync_and_status(fde_hodlr* H, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------------------------------
+// Level layout and the persistent level kernel's configuration
+struct LvCfg {
+  int CR, ldx, lds, ldk, ldm, offs[10], xbuf, wbuf, vbuf;
+  size_t bytes;
+};
+
+static int lv_config(const fde_hodlr* H, int mode, int nrhs, LvCfg* cfg) {
+  const int L = H->L;
+  const int NCPX = round_up(mode == 0 ? H->xcol[L] : nrhs, 8);
+  const int KP8 = round_up(H->kmax, 8), KP4 = round_up(H->kmax, 4);
+  if ((KP8 / 8) * (NCPX / 8) > MT_RED * LV_WARPS)
+    return set_err(FDE_EDIM, "level width %d x %d exceeds the reduce tile budget", KP8, NCPX);
+  const int lds = NCPX + ((NCPX % 16 == 0) ? 20 : 28);   // >= NCPX + 16 (padded views), = 4 mod 16
+  const int ldk = KP8 + 1, ldm = 2 * KP8 + 1;
+  for (int CR = 64; CR >= 8; CR /= 2) {
+    const int ldx = CR + 4;
+    long long o = 0;
+    int offs[10];
+    const int xb = NCPX * ldx, wb = KP4 * ldx, vb = KP8 * ldx;   // one pipeline buffer each
+    offs[0] = (int)o; o += 2LL * xb;                         // Xc x 2
+    offs[1] = (int)o; o += 2LL * wb;                         // Wn x 2
+    offs[2] = (int)o; o += 2LL * vb;                         // Vc x 2
+    offs[3] = (int)o; o += (long long)KP8 * lds;             // Pt
+    offs[4] = (int)o; o += (long long)KP8 * lds;             // Pb
+    if ((long long)KP8 * lds <= 2LL * xb) offs[5] = offs[0];   // T aliases Xc
+    else { offs[5] = (int)o; o += (long long)KP8 * lds; }
+    offs[6] = (int)o; o += (long long)KP8 * ldk;             // B
+    offs[7] = (int)o; o += (long long)KP8 * ldk;             // C
+    offs[8] = (int)o; o += (long long)KP8 * ldk;             // Sci
+    offs[9] = (int)o; o += (long long)KP8 * ldm;             // GJ workspace
+    const size_t bytes = (size_t)o * sizeof(double);
+    if (bytes <= LV_SMEM_MAX) {
+      cfg->CR = CR; cfg->ldx = ldx; cfg->lds = lds; cfg->ldk = ldk; cfg->ldm = ldm; cfg->bytes = bytes;
+      cfg->xbuf = xb; cfg->wbuf = wb; cfg->vbuf = vb;
+      for (int i = 0; i < 10; ++i) cfg->offs[i] = offs[i];
+      return FDE_OK;
+    }
+  }
+  return set_err(FDE_EDIM, "level kernel workspace does not fit in shared memory (k=%d, cols=%d)",
+                 H->kmax, NCPX);
+}
+
+static void post_order(int d, int j, int D, std::vector<int>& out) {
+  if (d + 1 < D) { post_order(d + 1, 2 * j, D, out); post_order(d + 1, 2 * j + 1, D, out); }
+  out.push_back(d);
+  out.push_back(j);
+}
+
+static int finalize_layout(fde_hodlr* H, cudaStream_t s) {
+  const int L = H->L, B = H->batch, n = H->n;
+  std::vector<int> rk((size_t)B * std::max(1, L), 0);
+  if (L > 0) {
+    CU(cudaStreamSynchronize(s));
+    CU(cudaMemcpy(rk.data(), H->d_rank, rk.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    DevStatus st{};
+    CU(cudaMemcpy(&st, H->d_status, sizeof(st), cudaMemcpyDeviceToHost));
+    if (st.code != FDE_OK)
+      return set_err(st.code, "compression failed (status %d) at instance %d level %d", st.code,
+                     st.where / 65536, st.where % 65536);
+  }
+  H->kl.assign(std::max(1, L), 1);
+  H->xcol.assign(L + 1, 1);
+  H->kofs.assign(std::max(1, L), 0);
+  H->kmax = 1;
+  long long ko = 0;
+  for (int l = 0; l < L; ++l) {
+    int R = 0;
+    for (int b = 0; b < B; ++b) R = std::max(R, rk[(size_t)b * L + l]);
+    H->kl[l] = R + 1;
+    H->kmax = std::max(H->kmax, R + 1);
+    H->xcol[l + 1] = H->xcol[l] + R + 1;
+    H->kofs[l] = ko;
+    ko += (1LL << l) * 3LL * (R + 1) * (R + 1);
+  }
+  H->kstride_inst = std::max(1LL, ko);
+  H->xstride = (long long)n * H->xcol[L];
+  H->sum_nc = std::max(H->xcol[L], NRHS_MAX);
+  H->sum_half = (long long)round_up(H->kmax, 8) * H->sum_nc;
+  // CTAs per instance for the persistent level kernel: P = 2^p co-resident with the batch
+  LvCfg cfg;
+  TRY(lv_config(H, 0, 1, &cfg));
+  int dev = 0, nsm = 0, per_sm = 0;
+  CU(cudaGetDevice(&dev));
+  CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_levels<16>, LV_THREADS, cfg.bytes));
+  H->coop_capacity = std::max(1, nsm * per_sm);
+  int p = 0;
+  while (p < L && ((long long)B << (p + 1)) <= H->coop_capacity) ++p;
+  H->p = p;
+  H->P = 1 << p;
+  std::vector<int> post;
+  if (p < L) post_order(0, 0, L - p, post);
+  H->npost = (int)post.size() / 2;
+  const size_t nn = std::max(1, H->nnodes);
+  TRY(dalloc(H, &H->d_X, (size_t)B * H->xstride));
+  TRY(dalloc(H, &H->d_Kst, (size_t)B * H->kstride_inst));
+  TRY(dalloc(H, &H->d_sums, (size_t)B * nn * 2 * H->sum_half));
+  TRY(dalloc(H, &H->d_lvpart, (size_t)2 * B * H->P * H->sum_half));
+  TRY(dalloc(H, &H->d_bar, 1));
+  TRY(dalloc(H, &H->d_post, std::max<size_t>(2, post.size())));
+  if (!post.empty())
+    CU(cudaMemcpy(H->d_post, post.data(), post.size() * sizeof(int), cudaMemcpyHostToDevice));
+  H->layout_done = true;
+  return FDE_OK;
+}
+
+static int launch_levels(fde_hodlr* H, int mode, int nf, double* Y, int ld, int nrhs, cudaStream_t s) {
+  const int L = H->L;
+  if (L == 0) return FDE_OK;
+  LvCfg cfg;
+  TRY(lv_config(H, mode, nrhs, &cfg));
+  LvArgs a{};
+  a.tree = H->tree; a.mode = mode; a.L = L; a.p = H->p; a.P = H->P; a.nf = nf; a.CR = cfg.CR;
+  a.lgCR = 0;
+  while ((1 << a.lgCR) < cfg.CR) ++a.lgCR;
+  a.ldx = cfg.ldx; a.lds = cfg.lds; a.ldk = cfg.ldk; a.ldm = cfg.ldm;
+  a.off_Xc = cfg.offs[0]; a.off_Wn = cfg.offs[1]; a.off_Vc = cfg.offs[2]; a.off_Pt = cfg.offs[3];
+  a.off_Pb = cfg.offs[4]; a.off_T = cfg.offs[5]; a.off_B = cfg.offs[6]; a.off_C = cfg.offs[7];
+  a.off_Si = cfg.offs[8]; a.off_M = cfg.offs[9];
+  a.xbuf = cfg.xbuf; a.wbuf = cfg.wbuf; a.vbuf = cfg.vbuf;
+  for (int l = 0; l < L; ++l) { a.kl[l] = H->kl[l]; a.xcol[l] = H->xcol[l]; a.kofs[l] = H->kofs[l]; }
+  a.xcol[L] = H->xcol[L];
+  a.kstride_inst = H->kstride_inst;
+  a.Lf = H->d_Lf; a.lf_stride = H->lf_stride; a.rank = H->d_rank;
+  a.X = H->d_X; a.xstride = H->xstride;
+  a.Y = Y; a.ld = ld; a.nrhs = nrhs; a.ystride = (long long)ld * nrhs;
+  a.Kst = H->d_Kst; a.sums = H->d_sums; a.sum_half = H->sum_half; a.sum_nc = H->sum_nc;
+  a.part = H->d_lvpart; a.bar = H->d_bar; a.post = H->d_post; a.npost = H->npost; a.st = H->d_status;
+  static unsigned long long* d_trace = nullptr;          // debug: FDE_TRACE_LEVELS=1
+  const bool trace = getenv("FDE_TRACE_LEVELS") != nullptr;
+  if (trace) {
+    if (!d_trace) CU(cudaMalloc(&d_trace, 1024 * sizeof(unsigned long long)));
+    CU(cudaMemsetAsync(d_trace, 0, 1024 * sizeof(unsigned long long), s));
+    a.trace = d_trace;
+  }
+  const int grid = H->P * H->batch;
+  // reduce tiles per warp: (round8(k)/8) x (cols/8) tiles over LV_WARPS warps
+  const int ntile = (round_up(H->kmax, 8) / 8) * (round_up(mode == 0 ? H->xcol[L] : nrhs, 8) / 8);
+  const int mt = ntile <= 4 * LV_WARPS ? 4 : (ntile <= 8 * LV_WARPS ? 8 : 16);
+  void* fn = mt == 4 ? (void*)k_levels<4> : (mt == 8 ? (void*)k_levels<8> : (void*)k_levels<16>);
+  void* args[] = {&a};
+  if (H->P > 1) {
+    CU(cudaMemsetAsync(H->d_bar, 0, sizeof(unsigned), s));
+    { PROF("k_levels"); CU(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(LV_THREADS), args, cfg.bytes, s)); }
+  } else {
+    { PROF("k_levels"); CU(cudaLaunchKernel(fn, dim3(grid), dim3(LV_THREADS), args, cfg.bytes, s)); }
+  }
+  LAUNCHED();
+  if (trace) {
+    unsigned long long h[1024];
+    CU(cudaStreamSynchronize(s));
+    CU(cudaMemcpy(h, d_trace, sizeof(h), cudaMemcpyDeviceToHost));
+    for (int b = 0; b < 2; ++b) {
+      fprintf(stderr, "k_levels trace CTA %s:", b ? "last" : "0");
+      for (int i = 0; i < 255 && h[b * 512 + 2 * i + 1]; ++i)
+        fprintf(stderr, " %llu:%.2f", h[b * 512 + 2 * i],
+                (h[b * 512 + 2 * i + 1] - h[b * 512 + 1]) * 1e-3);
+      fprintf(stderr, "\n");
+    }
+    fprintf(stderr, "k_levels pass cycles CTA 0: sync %llu load %llu update %llu reduce %llu store %llu\n",
+            h[800], h[801], h[802], h[803], h[804]);
+    fprintf(stderr, "k_levels node cycles CTA 0: prep %llu GJ %llu Si %llu store %llu solves %llu\n",
+            h[810], h[811], h[812], h[813], h[814]);
+  }
+  return FDE_OK;
+}
+
+// ---------------------------------------------------------------------------------------
 static int build_impl(int batch, int n, const double* alpha, double h, double dt, const double* dp,
                       const double* dm, double shift, double tol, int leaf, unsigned flags,
                       cudaStream_t s, fde_hodlr** out) {
@@ -415,25 +595,18 @@ static int build_impl(int batch, int n, const double* alpha, double h, double dt
   if ((rc = plan_compression(H, std::max(1, nsm * per_sm))) != FDE_OK) return fail(rc);
   const int L = H->L;
   H->gstride = n + 2;
-  H->ncap = std::max(NRHS_MAX, 1 + L * KCAP);
-  H->xstride = (long long)n * (1 + L * KCAP);
+  H->ncap = NRHS_MAX;                                   // matvec partials (k_lvl_reduce)
   H->lustride = (long long)n * LEAF_MAX;
   H->pstride_seg = (long long)KCAP * H->ncap;
   H->pstride_inst = (long long)std::max(1, H->max_seg) * H->pstride_seg;
-  H->sstride_node = (long long)SLD * H->ncap;
-  H->sstride_inst = (long long)H->max_nodes_lvl * H->sstride_node;
-  H->kstride_inst = (long long)std::max(1, H->nnodes) * 3 * KCAP * KCAP;
-  H->pivstride_inst = (long long)std::max(1, H->nnodes) * KCAP;
   const size_t B = batch;
   const size_t ntask = H->tasks.size(), nch = H->chunks.size();
   if ((rc = dalloc(H, &H->d_alpha, B)) || (rc = dalloc(H, &H->d_cfac, B)) ||
       (rc = dalloc(H, &H->d_g, B * H->gstride)) || (rc = dalloc(H, &H->d_Lf, B * H->lf_stride)) ||
       (rc = dalloc(H, &H->d_Lraw, B * H->lraw_stride)) || (rc = dalloc(H, &H->d_rank, B * std::max(1, L))) ||
       (rc = dalloc(H, &H->d_colofs, B * (L + 1))) || (rc = dalloc(H, &H->d_dp, B * n)) ||
-      (rc = dalloc(H, &H->d_dm, B * n)) || (rc = dalloc(H, &H->d_X, B * H->xstride)) ||
+      (rc = dalloc(H, &H->d_dm, B * n)) ||
       (rc = dalloc(H, &H->d_LU, B * H->lustride)) || (rc = dalloc(H, &H->d_P, B * H->pstride_inst)) ||
-      (rc = dalloc(H, &H->d_S, B * H->sstride_inst)) || (rc = dalloc(H, &H->d_K, B * H->kstride_inst)) ||
-      (rc = dalloc(H, &H->d_Kpiv, B * H->pivstride_inst)) ||
       (rc = dalloc(H, &H->d_tasks, std::max<size_t>(1, ntask))) ||
       (rc = dalloc(H, &H->d_chunks, std::max<size_t>(1, nch))) ||
       (rc = dalloc(H, &H->d_ctr, std::max<size_t>(1, ntask))) ||
@@ -466,6 +639,8 @@ static int build_impl(int batch, int n, const double* alpha, double h, double dt
   g_launches++;
   // S2: compression
   if ((rc = run_compression(H, s)) != FDE_OK) return fail(rc);
+  // one synchronisation per build: the ranks fix the column layout of the factorisation
+  if ((rc = finalize_layout(H, s)) != FDE_OK) return fail(rc);
   H->last_stream = s;
   if ((flags & FDE_SYNC) && (rc = sync_and_status(H, s)) != FDE_OK) return fail(rc);
   *out = H;
@@ -480,30 +655,14 @@ static int factor_impl(fde_hodlr* H, const double* dp, const double* dm, int nf,
   LeafArgs la{};
   la.tree = H->tree; la.mode = 0; la.shift = H->shift; la.cfac = H->d_cfac; la.dt = H->dt;
   la.g = H->d_g; la.gstride = H->gstride; la.dp = dp; la.dm = dm;
-  la.Lf = H->d_Lf; la.lf_stride = H->lf_stride; la.rank = H->d_rank; la.colofs = H->d_colofs;
+  la.Lf = H->d_Lf; la.lf_stride = H->lf_stride; la.rank = H->d_rank;
+  for (int l = 0; l < L; ++l) { la.kl[l] = H->kl[l]; la.xcol[l] = H->xcol[l]; }
+  la.xcol[L] = H->xcol[L];
   la.X = H->d_X; la.xstride = H->xstride; la.LU = H->d_LU; la.lustride = H->lustride;
   la.keep = keep; la.nf = nf; la.u_prev = u_prev; la.f = f; la.st = H->d_status;
   { PROF("k_leaf"); k_leaf<<<dim3(H->nleaf, B), LEAF_THREADS, (LEAF_MAX * LDA_LEAF + NCHUNK * LDP_LEAF) * 8, s>>>(la); }
   LAUNCHED();
-  LevelArgs lv{};
-  lv.tree = H->tree; lv.mode = 0; lv.Lf = H->d_Lf; lv.lf_stride = H->lf_stride;
-  lv.rank = H->d_rank; lv.colofs = H->d_colofs; lv.X = H->d_X; lv.xstride = H->xstride;
-  lv.nf = nf; lv.Ppart = H->d_P; lv.pstride_seg = H->pstride_seg; lv.pstride_inst = H->pstride_inst;
-  lv.Sbuf = H->d_S; lv.sstride_node = H->sstride_node; lv.sstride_inst = H->sstride_inst;
-  lv.Kst = H->d_K; lv.kstride_node = 3LL * KCAP * KCAP; lv.kstride_inst = H->kstride_inst;
-  lv.Kpiv = H->d_Kpiv; lv.pivstride_inst = H->pivstride_inst; lv.keep = keep; lv.st = H->d_status;
-  for (int l = L - 1; l >= 0; --l) {
-    lv.level = l;
-    const int nseg = H->seg_ofs[l + 1] - H->seg_ofs[l];
-    { PROF("k_lvl_reduce"); k_lvl_reduce<<<dim3(nseg, B), LVL_THREADS, SMEM_REDUCE, s>>>(lv); }
-    LAUNCHED();
-    { PROF("k_lvl_node"); k_lvl_node<<<dim3(1 << l, B), LVL_THREADS, SMEM_NODE, s>>>(lv); }
-    LAUNCHED();
-    if (l > 0 || nf > 0) {
-      { PROF("k_lvl_update"); k_lvl_update<<<dim3(nseg, B), LVL_THREADS, SMEM_UPDATE, s>>>(lv); }
-      LAUNCHED();
-    }
-  }
+  TRY(launch_levels(H, 0, nf, nullptr, 0, 1, s));
   if (nf) {
     const long long tot = (long long)B * H->n;
     { PROF("k_copy_col0"); k_copy_col0<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(H->d_X, H->xstride, H->n, u_next, B); }
@@ -521,24 +680,8 @@ static int solve_impl(fde_hodlr* H, const double* b, const double* f, double* y,
   la.b = b; la.y = y; la.nrhs = nrhs; la.ld = ld; la.f = f; la.dt = H->dt; la.st = H->d_status;
   { PROF("k_leaf"); k_leaf<<<dim3(H->nleaf, B), LEAF_THREADS, (LEAF_MAX * LDA_LEAF + NCHUNK * LDP_LEAF) * 8, s>>>(la); }
   LAUNCHED();
-  LevelArgs lv{};
-  lv.tree = H->tree; lv.mode = 1; lv.Lf = H->d_Lf; lv.lf_stride = H->lf_stride;
-  lv.rank = H->d_rank; lv.colofs = H->d_colofs; lv.X = H->d_X; lv.xstride = H->xstride;
-  lv.Y = y; lv.ld = ld; lv.nrhs = nrhs; lv.ystride = (long long)ld * nrhs;
-  lv.Ppart = H->d_P; lv.pstride_seg = H->pstride_seg; lv.pstride_inst = H->pstride_inst;
-  lv.Sbuf = H->d_S; lv.sstride_node = H->sstride_node; lv.sstride_inst = H->sstride_inst;
-  lv.Kst = H->d_K; lv.kstride_node = 3LL * KCAP * KCAP; lv.kstride_inst = H->kstride_inst;
-  lv.Kpiv = H->d_Kpiv; lv.pivstride_inst = H->pivstride_inst; lv.keep = 1; lv.st = H->d_status;
-  for (int l = L - 1; l >= 0; --l) {
-    lv.level = l;
-    const int nseg = H->seg_ofs[l + 1] - H->seg_ofs[l];
-    { PROF("k_lvl_reduce"); k_lvl_reduce<<<dim3(nseg, B), LVL_THREADS, SMEM_REDUCE, s>>>(lv); }
-    LAUNCHED();
-    { PROF("k_lvl_node"); k_lvl_node<<<dim3(1 << l, B), LVL_THREADS, SMEM_NODE, s>>>(lv); }
-    LAUNCHED();
-    { PROF("k_lvl_update"); k_lvl_update<<<dim3(nseg, B), LVL_THREADS, SMEM_UPDATE, s>>>(lv); }
-    LAUNCHED();
-  }
+  (void)L;
+  TRY(launch_levels(H, 1, 0, y, ld, nrhs, s));
   return FDE_OK;
 }
 

@@ -27,6 +27,8 @@
 
 #define PC_ROWS 256
 #define PSTRIDE (KRAW + 4)
+#define PC_STOP 1e-3          // pivoted-Cholesky trace stop = tau * PC_STOP ...
+#define PC_EPS_TRACE 3.2e-14  // ... but never below ~144 ulps of the initial trace
 
 struct PcTask {            // one (instance, level)
   int inst, level, m, G;   // G chunks (CTAs)
@@ -137,6 +139,10 @@ k_pchol(const PcTask* __restrict__ tasks, const PcChunk* __restrict__ chunks,
   double d = valid ? gi[2 + 2 * i] : 0.0;            // diag of H_m: g_{2+2i}
   int k = 0;
   unsigned step = 0;
+  // Stopping threshold of the pivoted Cholesky: tau * PC_STOP (floored at the rounding level
+  // of the residual trace).  Stopping well below tau lets the optimal recompression below
+  // reproduce the truncated-SVD approximant (same rank, same accuracy; tests/ and DESIGN.md).
+  double stop_tau = tk.tau;
   for (;;) {
     // ---- local partials of the residual diagonal
     double s = block_sum(d, redv);
@@ -166,14 +172,16 @@ k_pchol(const PcTask* __restrict__ tasks, const PcChunk* __restrict__ chunks,
         if (v2 > bv || (v2 == bv && i2 < bi)) { bv = v2; bi = i2; bs = s2; }
       }
       if (t == 0) {
-        s_total = tot; s_pmax = bv; s_p = bi; s_wslot = bs;
-        int stop = (tot <= tk.tau) || !(bv > 0.0) || (k == KRAW);
+        if (k == 0) s_total = fmax(tk.tau * PC_STOP, PC_EPS_TRACE * tot);   // initial trace
+        s_pmax = bv; s_p = bi; s_wslot = bs;
+        int stop = (tot <= s_total) || !(bv > 0.0) || (k == KRAW);
         if (k == KRAW && tot > tk.tau && ch.grank == 0)
           latch_status(st, FDE_ENOCONV, tk.inst * 65536 + tk.level);
         s_stop = stop;
       }
     }
     __syncthreads();
+    stop_tau = s_total;
     if (s_stop) break;
     const int p = s_p;
     const double sp = sqrt(s_pmax);

@@ -32,7 +32,9 @@ struct LeafArgs {
   const double* g; long long gstride;
   const double* dp; const double* dm;        // [batch*n]
   const double* Lf; long long lf_stride;
-  const int* rank; const int* colofs;        // [batch*L], [batch*(L+1)]
+  const int* rank;                           // [batch*L] actual ranks
+  int kl[LMAX];                              // columns per level (max rank over batch + 1)
+  int xcol[LMAX + 1];                        // first X column of each level block; xcol[L] = end
   double* X; long long xstride;              // X[inst*xstride + col*n + row]
   double* LU; long long lustride; int keep;  // leaf LU storage
   int nf;                                    // fused RHS columns (0/1), factor mode
@@ -223,8 +225,7 @@ k_leaf(const LeafArgs a) {
       for (int e = t; e < s * s; e += LEAF_THREADS) LUg[e] = A[(e % s) + (e / s) * LDA_LEAF];
     // ---- panel of X columns [1 - nf, 1 + W)
     const int* rk = a.rank + inst * L;
-    const int* co = a.colofs + inst * (L + 1);
-    const int c_end = 1 + co[L];
+    const int c_end = a.xcol[L];
     const double* Lfi = a.Lf + (long long)inst * a.lf_stride;
     double* Xi = a.X + (long long)inst * a.xstride;
     const double* dpg = a.dp + (long long)inst * n;
@@ -238,10 +239,10 @@ k_leaf(const LeafArgs a) {
         if (cg == 0) {
           v = a.u_prev[(long long)inst * n + R] + a.dt * a.f[(long long)inst * n + R];
         } else {
-          const int cl = cg - 1;
           int l = 0;
-          while (l + 1 < L && co[l + 1] <= cl) ++l;
-          const int q = cl - co[l], r = rk[l];
+          while (l + 1 < L && a.xcol[l + 1] <= cg) ++l;
+          // q < r: scaled low-rank column; r <= q < k-1: zero padding; q = k-1: exact column
+          const int q = cg - a.xcol[l], r = rk[l], kq = a.kl[l];
           const int jn = leaf >> (L - l), child = (leaf >> (L - l - 1)) & 1;
           const int nd = node_index(l, jn);
           const int r0n = tr.node_r0[nd], n1 = tr.node_n1[nd];
@@ -249,12 +250,12 @@ k_leaf(const LeafArgs a) {
           const double* Ll = Lfi + tr.lev_lofs[l];
           if (child == 0) {
             const int j1 = R - r0n;
-            v = (q < r) ? -c * dmg[R] * Ll[(n1 - 1 - j1) + (long long)q * m]
-                        : ((j1 == n1 - 1) ? -c * dpg[R] : 0.0);
+            v = (q == kq - 1) ? ((j1 == n1 - 1) ? -c * dpg[R] : 0.0)
+                : (q < r ? -c * dmg[R] * Ll[(n1 - 1 - j1) + (long long)q * m] : 0.0);
           } else {
             const int i2 = R - r0n - n1;
-            v = (q < r) ? -c * dpg[R] * Ll[i2 + (long long)q * m]
-                        : ((i2 == 0) ? -c * dmg[R] : 0.0);
+            v = (q == kq - 1) ? ((i2 == 0) ? -c * dmg[R] : 0.0)
+                : (q < r ? -c * dpg[R] * Ll[i2 + (long long)q * m] : 0.0);
           }
         }
         P[i + cc * LDP_LEAF] = v;
