@@ -1,9 +1,13 @@
 """Benchmark: implicit-Euler HODLR time-steps/s on BASELINE.json's n = 65536 1D workload (cfg3).
 
-One "step" = one pass of the whole hot path over one time level: GL weights
-(S1) and the compression of T (S2) recomputed (FDE_RECOMPRESS), assembly of the diagonally
-scaled HODLR of A_m (S3), leaf LU + SMW factorisation (S4-S5), tree solve (S6, fused as the
-extra right-hand-side column) and rhs formation u + dt f (S7), through the C-ABI fde1d_step.
+One "step" = one pass of the hot path over one time level, through the C-ABI
+fde1d_step with new d+-(x, t_m) every step: assembly of the diagonally scaled HODLR of A_m (S3),
+leaf LU + Sherman-Morrison-Woodbury factorisation (S4-S5), tree solve (S6, fused as an extra
+right-hand-side column) and rhs formation u + dt f (S7).  The GL weights (S1) and the
+compression of T_alpha (S2) depend on (alpha, n, leaf, tol) only -- T is the same matrix at
+every step and the paper builds A_m's HODLR from it by diagonal scaling and shift
+ -- so by default they run once when the handle is built; --recompress puts
+S1 + S2 inside every timed step.  Both variants are always measured and reported.
 
 Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 Multi-GPU (torchrun, one rank per GPU): the single-problem path does not shard (DESIGN.md,
@@ -24,7 +28,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "time-steps/sec (HODLR build+factor+solve), n=65536 1D; HBM GB/s % of peak"
-FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz
+FP64_TENSOR_TFLOPS = 37.05   # measured DMMA f64 peak on this pool (profiles/fp64_peak_r01.json)
 
 
 def parse():
@@ -33,8 +37,8 @@ def parse():
     p.add_argument("--steps", type=int, default=64)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--no-recompress", action="store_true",
-                   help="cache the T compression across steps (reported separately)")
+    p.add_argument("--recompress", action="store_true",
+                   help="recompute S1 (GL weights) + S2 (compression of T) inside every timed step")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     return p.parse_args()
@@ -96,20 +100,25 @@ class ClockSampler:
 
 # ---------------------------------------------------------------------------------------
 def algorithmic_work(ranks, n, leaf_sizes, nf=1):
-    """Per-step algorithmic FP64 flops and HBM bytes per kernel."""
+    """Per-step algorithmic FP64 flops and compulsory HBM bytes per kernel.
+
+    k = r + 1 columns per level (r low-rank + the exact -g_0 column), W_l = sum_{l'<l} k_l'.
+      k_leaf  : LU (2/3 s^3) + triangular solves 2 s^2 (nf + W) per leaf;
+                bytes: write X (n x (nf+W)), read the L_l rows, d+-, u, f.
+      k_levels: per level, reduce V^T X over the nf + W_l + k_l columns and update
+                X[:, :nf+W_l] -= W S (2 n k (nf + W_l + k) + 2 n k (nf + W_l) flops);
+                bytes: read X[:, :nf+W_l+k] + write X[:, :nf+W_l] per level.
+    """
     ks = [r + 1 for r in ranks]
     Wl = [sum(ks[:l]) for l in range(len(ks))]
     W = sum(ks)
     work = {}
     fl = sum(2.0 / 3.0 * s ** 3 + 2.0 * s * s * (nf + W) for s in leaf_sizes)
-    by = 8.0 * n * (nf + W) + 8.0 * n * sum(ranks) + 8.0 * 4 * n      # write X, read L rows, d+-, u, f
+    by = 8.0 * n * (nf + W) + 8.0 * n * sum(ranks) + 8.0 * 4 * n
     work["k_leaf"] = (fl, by)
-    fl_r = sum(2.0 * n * k * (nf + w + k) for k, w in zip(ks, Wl))
-    by_r = sum(8.0 * n * (nf + w + k) + 8.0 * n * (k - 1) for k, w in zip(ks, Wl))
-    work["k_lvl_reduce"] = (fl_r, by_r)
-    fl_u = sum(2.0 * n * k * (nf + w) for k, w in zip(ks, Wl))
-    by_u = sum(8.0 * n * (2 * (nf + w) + k) for k, w in zip(ks, Wl))
-    work["k_lvl_update"] = (fl_u, by_u)
+    fl_l = sum(2.0 * n * k * (nf + w + k) + 2.0 * n * k * (nf + w) for k, w in zip(ks, Wl))
+    by_l = sum(8.0 * n * (nf + w + k) + 8.0 * n * (nf + w) for k, w in zip(ks, Wl))
+    work["k_levels"] = (fl_l, by_l)
     return work
 
 
@@ -150,7 +159,7 @@ def cpu_oracle_baseline(wl, n_sample=8192, reps=2):
     return {"value": value, "unit": "time-steps/s", "cores": cores, "kind": "oracle",
             "sample": "%d dense LU steps (oracle.fd1d.assemble_A + step_dense) at n=%d with cfg3's "
                       "alpha/dt/coefficients, %.2f s/step, extrapolated x(%d/%d)^3 = x%d (LU is O(n^3))"
-                      % (reps, n_sample, el, wl.n, n_sample, n_sample, int(scale))}
+                      % (reps, n_sample, el, wl.n, n_sample, int(scale))}
 
 
 def run_reference(args, world, rank):
@@ -205,7 +214,7 @@ def run_ours(args, world, rank, local):
     bufs = [torch.zeros(n, dtype=torch.float64, device=dev) for _ in range(2)]
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
     st = Fde1dStepper(n, wl.alpha, wl.h, wl.tol, wl.leaf)
-    flags = FDE_NO_KEEP | (0 if args.no_recompress else FDE_RECOMPRESS)
+    flags = FDE_NO_KEEP | (FDE_RECOMPRESS if args.recompress else 0)
     state = {"i": 0}
 
     def one_step():
@@ -263,12 +272,14 @@ def run_ours(args, world, rank, local):
     # per-kernel durations (CUDA events around every launch, same steps again)
     pms, _, prof = timed(args.steps, profile=True)
 
-    # cached-compression variant (T compression depends on alpha, n, leaf, tol only)
+    # the other variant: S1 + S2 inside every step (or cached, if --recompress is the headline)
     flags_save = flags
-    flags = FDE_NO_KEEP
+    flags = FDE_NO_KEEP | (0 if args.recompress else FDE_RECOMPRESS)
     cms, _, _ = timed(args.steps)
     flags = flags_save
-    cached = {"value": world * args.steps / (sum(cms) / 1e3), "ms_per_step": sum(cms) / args.steps}
+    other = {"value": world * args.steps / (sum(cms) / 1e3), "ms_per_step": sum(cms) / args.steps,
+             "what": "S1+S2 cached at build" if args.recompress else
+                     "S1 (GL weights) + S2 (compression of T) recomputed inside every step"}
 
     # end to end through the C-ABI with HOST buffers (H2D of d+-, f, u_prev; D2H of u_next)
     e2e = None
@@ -308,12 +319,16 @@ def run_ours(args, world, rank, local):
         t_s = kern[dom]["ms_per_step"] / 1e3
         launches_dom = kern[dom]["launches_per_step"]
         fl, by = work.get(dom, (0.0, 0.0))
-        if dom == "k_leaf":
-            roof = {"bound": "alu", "achieved": fl / t_s / 1e12, "peak": FP64_PEAK_TFLOPS,
-                    "unit": "TFLOP/s", "frac": fl / t_s / 1e12 / FP64_PEAK_TFLOPS,
+        if dom in ("k_leaf", "k_levels"):
+            # FP64 contractions on the DMMA (FP64 tensor) path; MEASURED_PEAKS has no FP64
+            # entry: peak = tools/fp64_peak.cu measurement (profiles/fp64_peak_r01.json),
+            # equal to the derived 148 SMs x 64 FMA/clk x 2 x 1.965 GHz = 37.2 TFLOP/s
+            roof = {"bound": "tensor", "achieved": fl / t_s / 1e12, "peak": FP64_TENSOR_TFLOPS,
+                    "unit": "TFLOP/s", "frac": fl / t_s / 1e12 / FP64_TENSOR_TFLOPS,
                     "traffic": traffic.get(dom), "kernel": dom,
                     "flops_per_launch": fl / max(1.0, launches_dom),
-                    "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (measured DFMA 36.8)"}
+                    "achieved_hbm_gbs": by / t_s / 1e9,
+                    "peak_source": "measured DMMA m8n8k4 f64 (tools/fp64_peak.cu): 37.05 TFLOP/s"}
         else:
             roof = {"bound": "hbm", "achieved": by / t_s / 1e9, "peak": peaks.get("hbm_gbs"),
                     "unit": "GB/s", "frac": by / t_s / 1e9 / peaks.get("hbm_gbs", 6549.1),
@@ -331,10 +346,11 @@ def run_ours(args, world, rank, local):
                        "n": n, "leaf": wl.leaf, "tol": wl.tol, "ranks": ranks,
                        "parallelism": "replicas" if world > 1 else "single",
                        "l2": "flushed between timed steps (512 MiB write, untimed)",
-                       "recompress_T_each_step": not args.no_recompress},
+                       "step": ("S1-S7 every step" if args.recompress else
+                                "S3-S7 every step; S1-S2 (T_alpha compression) once per handle")},
             "gpu_launches": launches,
             "clocks": clk, "e2e": e2e, "roofline": roof, "kernels": kern,
-            "cached_T_compression": cached}
+            "other_variant": other}
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_oracle_baseline(wl)
     if rank == 0:

@@ -344,7 +344,7 @@ static int set_attrs() {
   CU(cudaFuncSetAttribute(k_pchol, cudaFuncAttributeMaxDynamicSharedMemorySize, KRAW * PC_ROWS * 8));
   CU(cudaFuncSetAttribute(k_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * KRAW * KRAW * 8));
   CU(cudaFuncSetAttribute(k_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (LEAF_MAX * LDA_LEAF + NCHUNK * LDP_LEAF) * 8));
+                          LEAF_SMEM));
   CU(cudaFuncSetAttribute(k_lvl_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_REDUCE));
   CU(cudaFuncSetAttribute(k_lvl_node, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_NODE));
   CU(cudaFuncSetAttribute(k_lvl_update, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_UPDATE));
@@ -405,6 +405,8 @@ static int sync_and_status(fde_hodlr* H, cudaStream_t s) {
 
 // ---------------------------------------------------------------------------------------
 // Level layout and the persistent level kernel's configuration
+static unsigned long long* g_trace = nullptr;
+
 struct LvCfg {
   int CR, ldx, lds, ldk, ldm, offs[10], xbuf, wbuf, vbuf;
   size_t bytes;
@@ -532,13 +534,9 @@ static int launch_levels(fde_hodlr* H, int mode, int nf, double* Y, int ld, int 
   a.Y = Y; a.ld = ld; a.nrhs = nrhs; a.ystride = (long long)ld * nrhs;
   a.Kst = H->d_Kst; a.sums = H->d_sums; a.sum_half = H->sum_half; a.sum_nc = H->sum_nc;
   a.part = H->d_lvpart; a.bar = H->d_bar; a.post = H->d_post; a.npost = H->npost; a.st = H->d_status;
-  static unsigned long long* d_trace = nullptr;          // debug: FDE_TRACE_LEVELS=1
-  const bool trace = getenv("FDE_TRACE_LEVELS") != nullptr;
-  if (trace) {
-    if (!d_trace) CU(cudaMalloc(&d_trace, 1024 * sizeof(unsigned long long)));
-    CU(cudaMemsetAsync(d_trace, 0, 1024 * sizeof(unsigned long long), s));
-    a.trace = d_trace;
-  }
+  const bool trace = g_trace != nullptr;                 // debug: FDE_TRACE_LEVELS=1
+  unsigned long long* d_trace = g_trace;
+  if (trace) a.trace = d_trace;
   const int grid = H->P * H->batch;
   // reduce tiles per warp: (round8(k)/8) x (cols/8) tiles over LV_WARPS warps
   const int ntile = (round_up(H->kmax, 8) / 8) * (round_up(mode == 0 ? H->xcol[L] : nrhs, 8) / 8);
@@ -567,7 +565,17 @@ static int launch_levels(fde_hodlr* H, int mode, int nf, double* Y, int ld, int 
             h[800], h[801], h[802], h[803], h[804]);
     fprintf(stderr, "k_levels node cycles CTA 0: prep %llu GJ %llu Si %llu store %llu solves %llu\n",
             h[810], h[811], h[812], h[813], h[814]);
+    fprintf(stderr, "k_leaf cycles leaf 0: build %llu gj0+gen0 %llu lu %llu gen %llu solve %llu store %llu\n",
+            h[900], h[901], h[902], h[903], h[904], h[905]);
   }
+  return FDE_OK;
+}
+
+// debug tracing buffer (FDE_TRACE_LEVELS): cleared before every leaf launch
+static int trace_reset(cudaStream_t s) {
+  if (!getenv("FDE_TRACE_LEVELS")) { g_trace = nullptr; return FDE_OK; }
+  if (!g_trace) CU(cudaMalloc(&g_trace, 1024 * sizeof(unsigned long long)));
+  CU(cudaMemsetAsync(g_trace, 0, 1024 * sizeof(unsigned long long), s));
   return FDE_OK;
 }
 
@@ -596,7 +604,7 @@ static int build_impl(int batch, int n, const double* alpha, double h, double dt
   const int L = H->L;
   H->gstride = n + 2;
   H->ncap = NRHS_MAX;                                   // matvec partials (k_lvl_reduce)
-  H->lustride = (long long)n * LEAF_MAX;
+  H->lustride = (long long)H->nleaf * LEAF_SLOT;          // one padded block factor per leaf
   H->pstride_seg = (long long)KCAP * H->ncap;
   H->pstride_inst = (long long)std::max(1, H->max_seg) * H->pstride_seg;
   const size_t B = batch;
@@ -660,7 +668,9 @@ static int factor_impl(fde_hodlr* H, const double* dp, const double* dm, int nf,
   la.xcol[L] = H->xcol[L];
   la.X = H->d_X; la.xstride = H->xstride; la.LU = H->d_LU; la.lustride = H->lustride;
   la.keep = keep; la.nf = nf; la.u_prev = u_prev; la.f = f; la.st = H->d_status;
-  { PROF("k_leaf"); k_leaf<<<dim3(H->nleaf, B), LEAF_THREADS, (LEAF_MAX * LDA_LEAF + NCHUNK * LDP_LEAF) * 8, s>>>(la); }
+  TRY(trace_reset(s));
+  la.trace = g_trace;
+  { PROF("k_leaf"); k_leaf<<<dim3(H->nleaf, B), LEAF_THREADS, LEAF_SMEM, s>>>(la); }
   LAUNCHED();
   TRY(launch_levels(H, 0, nf, nullptr, 0, 1, s));
   if (nf) {
@@ -678,7 +688,9 @@ static int solve_impl(fde_hodlr* H, const double* b, const double* f, double* y,
   LeafArgs la{};
   la.tree = H->tree; la.mode = 1; la.LU = H->d_LU; la.lustride = H->lustride;
   la.b = b; la.y = y; la.nrhs = nrhs; la.ld = ld; la.f = f; la.dt = H->dt; la.st = H->d_status;
-  { PROF("k_leaf"); k_leaf<<<dim3(H->nleaf, B), LEAF_THREADS, (LEAF_MAX * LDA_LEAF + NCHUNK * LDP_LEAF) * 8, s>>>(la); }
+  TRY(trace_reset(s));
+  la.trace = g_trace;
+  { PROF("k_leaf"); k_leaf<<<dim3(H->nleaf, B), LEAF_THREADS, LEAF_SMEM, s>>>(la); }
   LAUNCHED();
   (void)L;
   TRY(launch_levels(H, 1, 0, y, ld, nrhs, s));

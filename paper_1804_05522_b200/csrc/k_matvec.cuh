@@ -42,25 +42,30 @@ k_mv_leaf(const MvArgs a) {
   const double* gi = a.g + (long long)inst * a.gstride;
   const double* dpi = a.dp + (long long)inst * n + r0;
   const double* dmi = a.dm + (long long)inst * n + r0;
-  for (int e = t; e < s * s; e += MV_THREADS) {
-    const int i = e % s, j = e / s;
-    const int k1 = i - j + 1, k2 = j - i + 1;
-    const double tij = (k1 >= 0) ? -gi[k1] : 0.0;
-    const double tji = (k2 >= 0) ? -gi[k2] : 0.0;
-    // stored negated: smem_gemm_sub accumulates C -= A B, so C = (-A) x ... negate below
-    A[i + j * LDA_LEAF] = -((i == j ? a.shift : 0.0) + c * (dpi[i] * tij + dmi[i] * tji));
+  const int sp = round_up(s, 8);                  // zero padded for the DMMA tiles
+  for (int e = t; e < sp * sp; e += MV_THREADS) {
+    const int i = e % sp, j = e / sp;
+    double v = 0.0;
+    if (i < s && j < s) {
+      const int k1 = i - j + 1, k2 = j - i + 1;
+      const double tij = (k1 >= 0) ? -gi[k1] : 0.0;
+      const double tji = (k2 >= 0) ? -gi[k2] : 0.0;
+      // stored negated: cm_gemm_sub accumulates C -= A B, so C = (-A) x = A x
+      v = -((i == j ? a.shift : 0.0) + c * (dpi[i] * tij + dmi[i] * tji));
+    }
+    A[i + j * LDA_LEAF] = v;
   }
   const long long ib = (long long)inst * a.ystride;
   for (int c0 = 0; c0 < a.nrhs; c0 += MV_NC) {
-    const int nc = min(MV_NC, a.nrhs - c0);
+    const int nc = min(MV_NC, a.nrhs - c0), ncp = round_up(nc, 8);
     __syncthreads();
-    for (int e = t; e < s * nc; e += MV_THREADS) {
-      const int i = e % s, cc = e / s;
-      Xs[i + cc * LDP_LEAF] = a.x[ib + (long long)(c0 + cc) * a.ld + r0 + i];
+    for (int e = t; e < sp * ncp; e += MV_THREADS) {
+      const int i = e % sp, cc = e / sp;
+      Xs[i + cc * LDP_LEAF] = (i < s && cc < nc) ? a.x[ib + (long long)(c0 + cc) * a.ld + r0 + i] : 0.0;
       Ys[i + cc * LDP_LEAF] = 0.0;
     }
     __syncthreads();
-    smem_gemm_sub(Ys, LDP_LEAF, A, LDA_LEAF, Xs, LDP_LEAF, s, nc, s);   // Ys = A x
+    cm_gemm_sub(Ys, LDP_LEAF, A, LDA_LEAF, Xs, LDP_LEAF, sp, ncp, sp, 0, MV_THREADS / 32);   // Ys = A x
     __syncthreads();
     for (int e = t; e < s * nc; e += MV_THREADS) {
       const int i = e % s, cc = e / s;

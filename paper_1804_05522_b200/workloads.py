@@ -107,7 +107,10 @@ def cfg4(batch=512, n=8192, K=16):
     alpha, a, b, C = alpha[:batch], a[:batch], b[:batch], C[:batch]
     d = (a[:, None] + b[:, None] * x[None, :])[None]
     f = _sine_series(x, C)[None]
-    return Workload1D("cfg4", batch, n, h, alpha, K, dt, 128, 1e-12, True,
+    # BASELINE configs[3] states no truncation tolerance.  Reading R18: tol 1e-13,
+    # because at 1e-12 even the truncated-SVD definition of the compression (oracle) leaves a
+    # forward error of 1.6e-8 > 1e-8 on the stiffest instance (alpha = 1.899); 1e-13 gives 7.7e-10.
+    return Workload1D("cfg4", batch, n, h, alpha, K, dt, 128, 1e-13, True,
                       np.zeros((batch, n)), d, d.copy(), f, x)
 
 
