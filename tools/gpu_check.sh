@@ -1,0 +1,19 @@
+#!/bin/bash
+# One GPU session: tests, smoke, bench, ncu launch list + full capture of the top kernels.
+set -x
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+mkdir -p gpurun_out
+nvidia-smi > gpurun_out/nvsmi.txt 2>&1
+timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
+if [ "${NCU:-1}" = "1" ]; then
+  CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu"
+  timeout 300 $CMD > gpurun_out/plain.log 2>&1 && \
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+      --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
+  echo "ncu launches rc=$?" >> gpurun_out/ncu_launch.log
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_leaf|k_levels' -s 8 -c 2 \
+      -o gpurun_out/prof $CMD > gpurun_out/ncu_full.log 2>&1
+  echo "ncu full rc=$?" >> gpurun_out/ncu_full.log
+fi
