@@ -480,6 +480,9 @@ static int finalize_layout(fde_hodlr* H, cudaStream_t s) {
     H->kofs[l] = ko;
     ko += (1LL << l) * 3LL * (R + 1) * (R + 1);
   }
+  if (H->xcol[L] > NCOL_MAX)
+    return set_err(FDE_EDIM, "panel width %d exceeds %d columns (ranks too large for this build)",
+                   H->xcol[L], NCOL_MAX);
   H->kstride_inst = std::max(1LL, ko);
   H->xstride = (long long)n * H->xcol[L];
   H->sum_nc = std::max(H->xcol[L], NRHS_MAX);
@@ -565,8 +568,25 @@ static int launch_levels(fde_hodlr* H, int mode, int nf, double* Y, int ld, int 
             h[800], h[801], h[802], h[803], h[804]);
     fprintf(stderr, "k_levels node cycles CTA 0: prep %llu GJ %llu Si %llu store %llu solves %llu\n",
             h[810], h[811], h[812], h[813], h[814]);
-    fprintf(stderr, "k_leaf cycles leaf 0: build %llu gj0+gen0 %llu lu %llu gen %llu solve %llu store %llu\n",
-            h[900], h[901], h[902], h[903], h[904], h[905]);
+    {
+      std::vector<unsigned long long> lt(4096);
+      CU(cudaMemcpy(lt.data(), d_trace + 2048, 4096 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+      double ph[3] = {0, 0, 0};
+      unsigned long long t0 = ~0ULL, t1 = 0;
+      int cnt = 0;
+      for (int l = 0; l < 1024 && lt[l * 4 + 3]; ++l, ++cnt) {
+        for (int q = 0; q < 3; ++q) ph[q] += (double)(lt[l * 4 + q + 1] - lt[l * 4 + q]);
+        t0 = std::min(t0, lt[l * 4]);
+        t1 = std::max(t1, lt[l * 4 + 3]);
+      }
+      fprintf(stderr, "k_leaf LU cycles CTA0: gj0 %llu ovw %llu diagupd %llu gj||trail %llu\n",
+              h[960], h[961], h[962], h[963]);
+      fprintf(stderr, "k_leaf panel cycles CTA0 warp0: gen %llu ld %llu solve %llu store %llu\n",
+              h[970], h[971], h[972], h[973]);
+      if (cnt)
+        fprintf(stderr, "k_leaf per-CTA avg us: build %.2f lu %.2f panel %.2f (%d CTAs, span %.1f us)\n",
+                ph[0] / cnt * 1e-3, ph[1] / cnt * 1e-3, ph[2] / cnt * 1e-3, cnt, (t1 - t0) * 1e-3);
+    }
   }
   return FDE_OK;
 }
@@ -574,8 +594,8 @@ static int launch_levels(fde_hodlr* H, int mode, int nf, double* Y, int ld, int 
 // debug tracing buffer (FDE_TRACE_LEVELS): cleared before every leaf launch
 static int trace_reset(cudaStream_t s) {
   if (!getenv("FDE_TRACE_LEVELS")) { g_trace = nullptr; return FDE_OK; }
-  if (!g_trace) CU(cudaMalloc(&g_trace, 1024 * sizeof(unsigned long long)));
-  CU(cudaMemsetAsync(g_trace, 0, 1024 * sizeof(unsigned long long), s));
+  if (!g_trace) CU(cudaMalloc(&g_trace, 8192 * sizeof(unsigned long long)));
+  CU(cudaMemsetAsync(g_trace, 0, 8192 * sizeof(unsigned long long), s));
   return FDE_OK;
 }
 

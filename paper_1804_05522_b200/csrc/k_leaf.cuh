@@ -24,13 +24,16 @@
 #include "fde_common.cuh"
 #include "fde_dmma.cuh"
 
-#define LEAF_THREADS 256
+#define LEAF_THREADS 256             // 8 warps: 2 per SM sub-partition (DMMA issue is per SMSP)
 #define LEAF_WARPS (LEAF_THREADS / 32)
 #define LDA_LEAF 132                 // column-major leading dims (= 4 mod 16: conflict-free DMMA frags)
 #define LDP_LEAF 132
-#define NCHUNK 64                    // right-hand-side columns per panel chunk
+#define YLD 132                      // warp stripe buffer (128 x 8) leading dim (= 4 mod 16)
 #define LEAF_SLOT (LEAF_MAX * LEAF_MAX)   // doubles per kept leaf factor
-#define LEAF_SMEM ((LEAF_MAX * LDA_LEAF + NCHUNK * LDP_LEAF + 32 * 33 + 2 * LEAF_MAX) * 8)
+#define NCOL_MAX 384                 // panel columns (1 + sum of k_l) held as descriptors in smem
+#define LEAF_SMEM ((LEAF_MAX * LDA_LEAF + 32 * 33 + 3 * LEAF_MAX + LEAF_WARPS * 8 * YLD) * 8 + \
+                   NCOL_MAX * 16)
+#define GJ_WARPS 4                   // warps of the 32 x 32 diagonal-block Gauss-Jordan
 #define LEAF_OVW 8                   // register tiles per warp of an overwrite GEMM
 
 struct LeafArgs {
@@ -57,6 +60,7 @@ struct LeafArgs {
 // ---- DMMA GEMMs on column-major shared-memory operands ---------------------------------
 // C[M x N] -= A[M x K] B[K x N]; tiles round-robin over warps [w0, w0 + nw); M, N % 8 == 0,
 // K % 4 == 0.  Optionally skips the tile block (skip_m0.., skip_n0..) of size 32 x 32.
+template <bool ADD = false>
 __device__ __forceinline__ void cm_gemm_sub(double* C, int ldc, const double* A, int lda,
                                             const double* B, int ldb, int M, int N, int K, int w0,
                                             int nw, int skip_m0 = -1, int skip_n0 = -1) {
@@ -83,7 +87,8 @@ __device__ __forceinline__ void cm_gemm_sub(double* C, int ldc, const double* A,
 #pragma unroll
       for (int u = 0; u < 4; ++u)
         if (ok[u])
-          dmma884(d[u][0], d[u][1], -A[mo[u] + gid + (k0 + tig) * lda],
+          dmma884(d[u][0], d[u][1], ADD ? A[mo[u] + gid + (k0 + tig) * lda]
+                                         : -A[mo[u] + gid + (k0 + tig) * lda],
                   B[k0 + tig + (no[u] + gid) * ldb]);
     }
 #pragma unroll
@@ -129,13 +134,13 @@ __device__ __forceinline__ void ovw_compute(OvwTiles& T, const double* A, int ld
   }
 }
 
-__device__ __forceinline__ void ovw_store(const OvwTiles& T, double* O, int ldo) {
+__device__ __forceinline__ void ovw_store(const OvwTiles& T, double* O, int ldo, double sgn = 1.0) {
   const int lane = threadIdx.x & 31, gid = lane >> 2, tig = lane & 3;
 #pragma unroll
   for (int u = 0; u < LEAF_OVW; ++u)
     if (u < T.cnt) {
-      O[T.mo[u] + gid + (T.no[u] + 2 * tig) * ldo] = T.d[u][0];
-      O[T.mo[u] + gid + (T.no[u] + 2 * tig + 1) * ldo] = T.d[u][1];
+      O[T.mo[u] + gid + (T.no[u] + 2 * tig) * ldo] = sgn * T.d[u][0];
+      O[T.mo[u] + gid + (T.no[u] + 2 * tig + 1) * ldo] = sgn * T.d[u][1];
     }
 }
 
@@ -150,9 +155,8 @@ __device__ void blk_gj_inv32(double* D, int ld, double* S, DevStatus* st, int wh
     const double piv = src[kk + kk * ls];
     if (t == 0 && !(isfinite(piv) && piv != 0.0)) latch_status(st, FDE_ESINGULAR, where);
     const double rp = 1.0 / piv;
-#pragma unroll
-    for (int j = 0; j < 1024 / LEAF_THREADS; ++j) {
-      const int e = t + j * LEAF_THREADS, i = e & 31, c = e >> 5;
+    for (int e = t; e < 1024; e += LEAF_THREADS) {
+      const int i = e & 31, c = e >> 5;
       const double aic = src[i + c * ls], aik = src[i + kk * ls], akc = src[kk + c * ls];
       double v;
       if (i == kk) v = (c == kk) ? rp : akc * rp;
@@ -163,128 +167,236 @@ __device__ void blk_gj_inv32(double* D, int ld, double* S, DevStatus* st, int wh
   }
 }
 
-// Block LU in inverse-diagonal form of A (sp x sp, sp % 32 == 0) in shared memory.
-// On entry the first diagonal block must already be inverted.
-__device__ void leaf_block_lu(double* A, int sp, double* S, DevStatus* st, int where) {
-  const int nb = sp >> 5;
+// Reciprocal to full double precision without the IEEE division routine: hardware
+// approximation + two Newton steps (error well below 1 ulp of the pivots' conditioning).
+__device__ __forceinline__ double fast_rcp(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+
+// In-place inverse of a 32 x 32 column-major block by warps 0..3 (named barrier 1): unpivoted
+// Gauss-Jordan in registers, lane r of warp w owns A[r, 8w .. 8w+7].  Per pivot the pivot
+// row and column are published through a double-buffered shared scratch (buf, 128 doubles)
+// and one 128-thread barrier.  The blocks are diagonal blocks of Schur complements of a
+// strictly diagonally dominant matrix: no pivoting; a zero / non-finite pivot
+// latches FDE_ESINGULAR.
+__device__ __noinline__ void quad_gj_inv32(double* D, int ld, double* buf, DevStatus* st, int where) {
+  const int w = threadIdx.x >> 5, r = threadIdx.x & 31;
+  double col[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) col[c] = D[r + (8 * w + c) * ld];
+  bool bad = false;
+#pragma unroll 1
+  for (int kb8 = 0; kb8 < 4; ++kb8) {
+#pragma unroll
+    for (int k8 = 0; k8 < 8; ++k8) {
+      const int kk = 8 * kb8 + k8;
+      double* pr = buf + (k8 & 1) * 64;              // [0, 32): pivot row ; [32, 64): pivot column
+      if (w == kb8) pr[32 + r] = col[k8];
+      if (r == kk) {
+        double2* pv = reinterpret_cast<double2*>(pr + 8 * w);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) pv[c] = make_double2(col[2 * c], col[2 * c + 1]);
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(GJ_WARPS * 32) : "memory");
+      const double piv = pr[kk];
+      bad |= !(isfinite(piv) && piv != 0.0);
+      const double rp = fast_rcp(piv);
+      const double f = pr[32 + r] * rp;              // A[r, kk] / pivot
+      const bool me = r == kk;
+      const double2* pv = reinterpret_cast<const double2*>(pr + 8 * w);
+#pragma unroll
+      for (int c2 = 0; c2 < 4; ++c2) {
+        const double2 q = pv[c2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = 2 * c2 + h;
+          const double p = h ? q.y : q.x;
+          if (w == kb8 && c == k8) col[c] = me ? rp : -f;
+          else col[c] = me ? p * rp : fma(-f, p, col[c]);
+        }
+      }
+    }
+  }
+  if (bad && threadIdx.x == 0) latch_status(st, FDE_ESINGULAR, where);
+#pragma unroll
+  for (int c = 0; c < 8; ++c) D[r + (8 * w + c) * ld] = col[c];
+}
+
+// Block LU in inverse-diagonal form of A (sp x sp, sp % 32 == 0) in shared memory; the
+// off-diagonal blocks are stored negated (-Lt, -Ut) for the accumulate-only stripe solve:
+//   for kb:  D_k = (A_kk)^{-1} ;  -Lt_ik = -A_ik D_k (i > k) ;  -Ut_jk = -A_jk D_k (j < k)
+//            A_ij += (-Lt_ik) A_kj   (i, j > k)
+// With lookahead: the next diagonal block is updated first and inverted by warps 0..3 while
+// warps 4..7 finish the trailing update (three CTA barriers per block column).
+__device__ void leaf_block_lu(double* A, int sp, double* prow, DevStatus* st, int where,
+                              unsigned long long* trace = nullptr) {
+  const int nb = sp >> 5, warp = threadIdx.x >> 5;
+  const bool tr = trace && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0;
+  long long tl = clock64();
+#define LUT(i) do { if (tr) { const long long t_ = clock64(); trace[960 + (i)] += t_ - tl; tl = t_; } } while (0)
+  if (warp < GJ_WARPS) quad_gj_inv32(A, LDA_LEAF, prow, st, where);
+  __syncthreads();
+  LUT(0);
   for (int kb = 0; kb < nb; ++kb) {
     const int k0 = kb * 32;
-    // Lt / Ut = A(rows != kb, kb) D_k   (overwrite the block column)
     if (nb > 1) {
       OvwTiles T;
       ovw_compute(T, A + k0 * LDA_LEAF, LDA_LEAF, A + k0 + k0 * LDA_LEAF, LDA_LEAF, 0, k0,
                   k0 + 32, sp, 32, 32);
       __syncthreads();
-      ovw_store(T, A + k0 * LDA_LEAF, LDA_LEAF);
+      ovw_store(T, A + k0 * LDA_LEAF, LDA_LEAF, -1.0);
       __syncthreads();
     }
+    LUT(1);
     if (kb + 1 < nb) {
       const int k1 = k0 + 32;
-      // trailing update, then the next diagonal block is inverted
-      cm_gemm_sub(A + k1 + k1 * LDA_LEAF, LDA_LEAF, A + k1 + k0 * LDA_LEAF, LDA_LEAF,
-                  A + k0 + k1 * LDA_LEAF, LDA_LEAF, sp - k1, sp - k1, 32, 0, LEAF_WARPS);
+      double* Akk = A + k1 + k1 * LDA_LEAF;
+      const double* Lk = A + k1 + k0 * LDA_LEAF;
+      const double* Uk = A + k0 + k1 * LDA_LEAF;
+      cm_gemm_sub<true>(Akk, LDA_LEAF, Lk, LDA_LEAF, Uk, LDA_LEAF, 32, 32, 32, 0, LEAF_WARPS);
       __syncthreads();
-      blk_gj_inv32(A + k1 + k1 * LDA_LEAF, LDA_LEAF, S, st, where);
+      LUT(2);
+      if (warp < GJ_WARPS) quad_gj_inv32(Akk, LDA_LEAF, prow, st, where);
+      else if (sp - k1 > 32)
+        cm_gemm_sub<true>(Akk, LDA_LEAF, Lk, LDA_LEAF, Uk, LDA_LEAF, sp - k1, sp - k1, 32, GJ_WARPS,
+                          LEAF_WARPS - GJ_WARPS, 0, 0);
+      __syncthreads();
+      LUT(3);
     }
+  }
+#undef LUT
+}
+
+// ---- warp-stripe block triangular solve -------------------------------------------------
+// One warp solves A_leaf x = p for an 8-column stripe with no CTA barrier: the stripe lives in
+// the warp's registers as DMMA accumulator fragments (tile t = rows 8t..8t+7:
+// acc[t][j] = x[8t + gid][2 tig + j]); finished 32-row blocks z_kb are published through a
+// warp-private 32 x 8 shared buffer (Ys) to serve as the B operand of the block updates.
+// The factor is in inverse-diagonal form with the off-diagonal blocks stored NEGATED
+// (leaf_block_lu): -Lt_ik (i > k), -Ut_jk (j < k), D_k = (U_kk)^{-1}:
+//   forward   z_i += (-Lt_ik) z_k                       (k = 0 .. nb-2, i > k)
+//   backward  x_k  = D_k z_k,  z_j += (-Ut_jk) z_k       (k = nb-1 .. 0, j < k)
+
+__device__ __forceinline__ void ys_publish(double* Ys, const double (&acc)[16][2], int kb) {
+  const int lane = threadIdx.x & 31, gid = lane >> 2, tig = lane & 3;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    Ys[8 * i + gid + (2 * tig) * YLD] = acc[4 * kb + i][0];
+    Ys[8 * i + gid + (2 * tig + 1) * YLD] = acc[4 * kb + i][1];
   }
 }
 
-// P (sp x ncp) <- A^{-1} P with the block factor in A.
-__device__ void leaf_block_solve(const double* A, int sp, double* P, int ncp) {
-  const int nb = sp >> 5;
-  for (int kb = 0; kb + 1 < nb; ++kb) {             // forward: y_i -= Lt_ik y_k
-    const int k0 = kb * 32;
-    cm_gemm_sub(P + k0 + 32, LDP_LEAF, A + k0 + 32 + k0 * LDA_LEAF, LDA_LEAF, P + k0, LDP_LEAF,
-                sp - k0 - 32, ncp, 32, 0, LEAF_WARPS);
-    __syncthreads();
-  }
-  for (int kb = nb - 1; kb >= 0; --kb) {            // backward: x_j -= Ut_jk y_k ; x_k = D_k y_k
-    const int k0 = kb * 32;
-    OvwTiles T;
-    ovw_compute(T, A + k0 + k0 * LDA_LEAF, LDA_LEAF, P + k0, LDP_LEAF, 0, 32, 0, 0, ncp, 32);
-    if (k0 > 0)
-      cm_gemm_sub(P, LDP_LEAF, A + k0 * LDA_LEAF, LDA_LEAF, P + k0, LDP_LEAF, k0, ncp, 32, 0,
-                  LEAF_WARPS);
-    __syncthreads();
-    {
-      // ovw tiles index rows from 0: shift to block row k0
-      const int lane = threadIdx.x & 31, gid = lane >> 2, tig = lane & 3;
+__device__ __forceinline__ void stripe_solve(double (&acc)[16][2], const double* __restrict__ A, int nb,
+                                             double* Ys) {
+  const int lane = threadIdx.x & 31, gid = lane >> 2, tig = lane & 3;
 #pragma unroll
-      for (int u = 0; u < LEAF_OVW; ++u)
-        if (u < T.cnt) {
-          P[k0 + T.mo[u] + gid + (T.no[u] + 2 * tig) * LDP_LEAF] = T.d[u][0];
-          P[k0 + T.mo[u] + gid + (T.no[u] + 2 * tig + 1) * LDP_LEAF] = T.d[u][1];
-        }
-    }
-    __syncthreads();
-  }
-}
-
-// Panel chunk generation (factor mode): X columns [c_first, c_first + nc) of this leaf's rows
-// into P (sp x ncp, zero padded).  Warp per column (level, node and rank are warp-uniform),
-// lanes over rows; d+- of the leaf rows are staged in shared memory (dps, dms).
-//   column 0 (fused rhs): b = u_prev + dt f
-//   level l column q:  q < r: scaled low-rank column; r <= q < k-1: zero padding;
-//                      q = k-1: exact column (the single entry -g_0 of the other triangle)
-__device__ void gen_chunk(const LeafArgs& a, int inst, int leaf, int r0, int s, int sp, int c_first,
-                          int nc, int ncp, double* P, const double* dps, const double* dms, double c) {
-  const TreeDev& tr = a.tree;
-  const int n = tr.n, L = tr.L, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int cc = warp; cc < ncp; cc += LEAF_WARPS) {
-    double* pc = P + cc * LDP_LEAF;
-    const int cg = c_first + cc;
-    if (cc >= nc) {
-      for (int i = lane; i < sp; i += 32) pc[i] = 0.0;
-      continue;
-    }
-    if (cg == 0) {
-      const double* u = a.u_prev + (long long)inst * n + r0;
-      const double* f = a.f + (long long)inst * n + r0;
-      for (int i = lane; i < sp; i += 32) pc[i] = (i < s) ? u[i] + a.dt * f[i] : 0.0;
-      continue;
-    }
-    int l = 0;
-    while (l + 1 < L && a.xcol[l + 1] <= cg) ++l;
-    const int q = cg - a.xcol[l], r = a.rank[inst * L + l], kq = a.kl[l];
-    const int jn = leaf >> (L - l), child = (leaf >> (L - l - 1)) & 1;
-    const int nd = node_index(l, jn);
-    const int r0n = tr.node_r0[nd], n1 = tr.node_n1[nd];
-    const int m = tr.lev_m[l];
-    const double* Lq = a.Lf + (long long)inst * a.lf_stride + tr.lev_lofs[l] + (long long)q * m;
-    // row index into L_l: child 0 -> n1-1-(R-r0n) (decreasing), child 1 -> R-r0n-n1
-    const int li0 = child == 0 ? n1 - 1 - (r0 - r0n) : r0 - r0n - n1, lstep = child == 0 ? -1 : 1;
-    const double* ds = child == 0 ? dms : dps;      // scaling of the low-rank columns
-    const double* de = child == 0 ? dps : dms;      // scaling of the exact column
+  for (int kb = 0; kb < 3; ++kb) {                 // forward
+    if (kb + 1 < nb) {
+      ys_publish(Ys, acc, kb);
+      __syncwarp();
 #pragma unroll
-    for (int u = 0; u < LEAF_MAX / 32; ++u) {
-      const int i = lane + 32 * u;
-      if (i >= sp) break;
-      double v = 0.0;
-      if (i < s) {
-        const int li = li0 + lstep * i;
-        if (q == kq - 1) v = (li == 0) ? -c * de[i] : 0.0;
-        else if (q < r) v = -c * ds[i] * Lq[li];
+      for (int k4 = 0; k4 < 8; ++k4) {
+        const double b = Ys[4 * k4 + tig + gid * YLD];
+        const double* Ak = A + (kb * 32 + 4 * k4 + tig) * LDA_LEAF + gid;
+#pragma unroll
+        for (int t = 4 * (kb + 1); t < 16; ++t)
+          if (t < 4 * nb) dmma884(acc[t][0], acc[t][1], Ak[8 * t], b);
       }
-      pc[i] = v;
+      __syncwarp();
+    }
+  }
+#pragma unroll
+  for (int kb = 3; kb >= 0; --kb) {                // backward
+    if (kb < nb) {
+      ys_publish(Ys, acc, kb);
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { acc[4 * kb + i][0] = 0.0; acc[4 * kb + i][1] = 0.0; }
+#pragma unroll
+      for (int k4 = 0; k4 < 8; ++k4) {
+        const double b = Ys[4 * k4 + tig + gid * YLD];
+        const double* Ak = A + (kb * 32 + 4 * k4 + tig) * LDA_LEAF + gid;
+#pragma unroll
+        for (int t = 0; t < 4 * (kb + 1); ++t) dmma884(acc[t][0], acc[t][1], Ak[8 * t], b);
+      }
+      __syncwarp();
     }
   }
 }
 
-__global__ void __launch_bounds__(LEAF_THREADS)
+// Panel column descriptor (factor mode): X column cg of this leaf's rows.
+//   kind 0: zero (padding) ; 1: fused rhs b = u_prev + dt f ; 2: scaled low-rank column
+//   -c ds[i] L_l[li0 + lstep i, q] ; 3: exact column -c de[i] at the row with li == 0.
+struct PanelCol {        // 16 bytes (NCOL_MAX of them live in shared memory)
+  const double* Lq;      // kind 2: &L_l[0, q]; otherwise any valid address (read, unused)
+  int li0;
+  signed char kind, lstep;
+  signed char sel;       // scaling: 0 -> d+ rows, 1 -> d- rows
+  signed char pad;
+};
+static_assert(sizeof(PanelCol) == 16, "PanelCol layout");
+
+__device__ __forceinline__ PanelCol panel_col(const LeafArgs& a, int inst, int leaf, int r0, int cg,
+                                              int c_end) {
+  PanelCol pc{a.Lf, 0, 0, 0, 0, 0};
+  if (cg >= c_end) return pc;
+  if (cg == 0) { pc.kind = 1; return pc; }
+  const TreeDev& tr = a.tree;
+  const int L = tr.L;
+  int l = 0;
+  while (l + 1 < L && a.xcol[l + 1] <= cg) ++l;
+  const int q = cg - a.xcol[l], r = a.rank[inst * L + l], kq = a.kl[l];
+  const int jn = leaf >> (L - l), child = (leaf >> (L - l - 1)) & 1;
+  const int nd = node_index(l, jn);
+  const int r0n = tr.node_r0[nd], n1 = tr.node_n1[nd];
+  // row index into L_l: child 0 -> n1-1-(R-r0n) (decreasing), child 1 -> R-r0n-n1
+  const int li0 = child == 0 ? n1 - 1 - (r0 - r0n) : r0 - r0n - n1;
+  const int lstep = child == 0 ? -1 : 1;
+  if (q == kq - 1) { pc.kind = 3; pc.sel = child == 0 ? 0 : 1; pc.li0 = li0; pc.lstep = lstep; }
+  else if (q < r) {
+    pc.kind = 2; pc.sel = child == 0 ? 1 : 0; pc.li0 = li0; pc.lstep = lstep;
+    pc.Lq = a.Lf + (long long)inst * a.lf_stride + tr.lev_lofs[l] + (long long)q * tr.lev_m[l];
+  }
+  return pc;
+}
+
+__global__ void __launch_bounds__(LEAF_THREADS, 1)
 k_leaf(const LeafArgs a) {
   extern __shared__ double smem[];
   double* A = smem;                               // [LEAF_MAX cols][LDA_LEAF]
-  double* P = smem + LEAF_MAX * LDA_LEAF;         // [NCHUNK cols][LDP_LEAF]
-  double* S = P + NCHUNK * LDP_LEAF;              // 32 x 33 Gauss-Jordan scratch
+  double* S = A + LEAF_MAX * LDA_LEAF;            // 32 x 33 Gauss-Jordan scratch
   double* dps = S + 32 * 33;                      // d+ / d- of the leaf rows
   double* dms = dps + LEAF_MAX;
   const TreeDev& tr = a.tree;
   const int leaf = blockIdx.x, inst = blockIdx.y, t = threadIdx.x, warp = t >> 5;
+  const int lane = t & 31, gid = lane >> 2, tig = lane & 3;
+  double* Ys = dms + LEAF_MAX + warp * 8 * YLD;   // warp-private 128 x 8 stripe buffer
+  PanelCol* pcd = reinterpret_cast<PanelCol*>(dms + LEAF_MAX + LEAF_WARPS * 8 * YLD);
+  double* bs = reinterpret_cast<double*>(pcd + NCOL_MAX);   // fused rhs b = u + dt f of the leaf
   const int n = tr.n;
   const int r0 = tr.leaf_r0[leaf], s = tr.leaf_n[leaf];
-  const int sp = round_up(s, 32);
+  const int sp = round_up(s, 32), nb = sp >> 5;
   const int where = inst * 65536 + leaf;
   double* LUg = a.LU + (long long)inst * a.lustride + (long long)leaf * LEAF_SLOT;
+  double acc[16][2];
+  // debug (FDE_TRACE_LEVELS): per-CTA globaltimer stamps at the phase boundaries
+  const bool trc = a.trace && t == 0 && leaf < 1024 && inst == 0;
+  auto stamp = [&](int ph) {
+    if (a.trace) {
+      __syncthreads();
+      if (trc) {
+        unsigned long long tm;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm));
+        a.trace[2048 + leaf * 4 + ph] = tm;
+      }
+    }
+  };
+  stamp(0);
 
   if (a.mode == 0) {
     // ---- S3: generate the leaf block from g and d+- (column-major), identity padding
@@ -292,69 +404,156 @@ k_leaf(const LeafArgs a) {
     const double* gi = a.g + (long long)inst * a.gstride;
     const double* dpi = a.dp + (long long)inst * n + r0;
     const double* dmi = a.dm + (long long)inst * n + r0;
+    double* gs = S;                                  // g_0 .. g_sp staged (S is free scratch)
+    for (int k = t; k <= sp; k += LEAF_THREADS) gs[k] = (k <= n + 1) ? gi[k] : 0.0;
+    for (int i = t; i < s; i += LEAF_THREADS) {
+      dps[i] = dpi[i]; dms[i] = dmi[i];
+      if (a.nf) bs[i] = a.u_prev[(long long)inst * n + r0 + i] + a.dt * a.f[(long long)inst * n + r0 + i];
+    }
+    {                                                // panel column descriptors (one per column)
+      const int cb = 1 - a.nf, ce = a.xcol[tr.L];
+      for (int cc = t; cc < ce - cb; cc += LEAF_THREADS) pcd[cc] = panel_col(a, inst, leaf, r0, cb + cc, ce);
+    }
+    __syncthreads();
     for (int j = warp; j < sp; j += LEAF_WARPS)
-      for (int i = t & 31; i < sp; i += 32) {
+      for (int i = lane; i < sp; i += 32) {
         double v;
         if (i < s && j < s) {
           const int k1 = i - j + 1, k2 = j - i + 1;     // T[i,j] = -g_{i-j+1}, T^T[i,j] = T[j,i]
-          const double tij = (k1 >= 0) ? -gi[k1] : 0.0;
-          const double tji = (k2 >= 0) ? -gi[k2] : 0.0;
-          v = (i == j ? a.shift : 0.0) + c * (dpi[i] * tij + dmi[i] * tji);
+          const double tij = (k1 >= 0) ? -gs[k1] : 0.0;
+          const double tji = (k2 >= 0) ? -gs[k2] : 0.0;
+          v = (i == j ? a.shift : 0.0) + c * (dps[i] * tij + dms[i] * tji);
         } else {
           v = (i == j) ? 1.0 : 0.0;
         }
         A[i + j * LDA_LEAF] = v;
       }
-    for (int i = t; i < s; i += LEAF_THREADS) { dps[i] = dpi[i]; dms[i] = dmi[i]; }
     __syncthreads();
-    const bool ldbg = a.trace && blockIdx.x == 0 && blockIdx.y == 0 && t == 0;
-    long long llast = clock64();
-#define LT(i) do { if (ldbg) { const long long t_ = clock64(); a.trace[900 + (i)] += t_ - llast; llast = t_; } } while (0)
-    LT(0);
-    const int c_begin = 1 - a.nf, c_end = a.xcol[tr.L];
-    blk_gj_inv32(A, LDA_LEAF, S, a.st, where);
-    LT(1);
-    leaf_block_lu(A, sp, S, a.st, where);
+    stamp(1);
+    // ---- S4: block LU (inverse-diagonal form, off-diagonal blocks negated)
+    leaf_block_lu(A, sp, S, a.st, where, a.trace);
+    stamp(2);
     if (a.keep)
       for (int j = warp; j < sp; j += LEAF_WARPS)
-        for (int i = t & 31; i < sp; i += 32) LUg[i + j * sp] = A[i + j * LDA_LEAF];
-    LT(2);
-    double* Xi = a.X + (long long)inst * a.xstride;
-    for (int c0 = c_begin; c0 < c_end; c0 += NCHUNK) {
-      const int nc = min(NCHUNK, c_end - c0), ncp = round_up(nc, 8);
-      gen_chunk(a, inst, leaf, r0, s, sp, c0, nc, ncp, P, dps, dms, c);
+        for (int i = lane; i < sp; i += 32) LUg[i + j * sp] = A[i + j * LDA_LEAF];
+    // ---- panel X = A_leaf^{-1} [b | U_0 .. U_{L-1}] by warp stripes of 8 columns
+    const int c_begin = 1 - a.nf, c_end = a.xcol[tr.L];
+    const int nstripe = (c_end - c_begin + 7) >> 3;
+    double* Xi = a.X + (long long)inst * a.xstride + r0;
+    const bool ptr = a.trace && t == 0 && leaf == 0 && inst == 0;
+    long long pt0 = clock64();
+#define PTR(i) do { if (ptr) { const long long t_ = clock64(); a.trace[970 + (i)] += t_ - pt0; pt0 = t_; } } while (0)
+    // software pipeline: the raw L_l gathers of the warp's next stripe are in flight (in
+    // registers) while the current stripe is solved
+    double pv[8][4];
+    auto load_raw = [&](int st) {
+      const int cs = c_begin + 8 * st;
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) {
+        const PanelCol pc = cs + cc < c_end ? pcd[cs + cc - c_begin] : PanelCol{a.Lf, 0, 0, 0, 0, 0};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int i = lane + 32 * q;
+          // branch-free: every descriptor carries a valid pointer (kind != 2: step 0 at a.Lf)
+          const int ic = i < s ? i : s - 1;
+          const double x = __ldg(pc.Lq + pc.li0 + pc.lstep * ic);
+          pv[cc][q] = (i < s && pc.kind == 2) ? x : 0.0;
+        }
+      }
+    };
+    if (warp < nstripe) load_raw(warp);
+    for (int st = warp; st < nstripe; st += LEAF_WARPS) {
+      // scale the 8 panel columns into the warp's stripe buffer, then into registers
+      const int cs = c_begin + 8 * st;
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) {
+        const PanelCol pc = cs + cc < c_end ? pcd[cs + cc - c_begin] : PanelCol{a.Lf, 0, 0, 0, 0, 0};
+        const double* sc = pc.sel ? dms : dps;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int i = lane + 32 * q;
+          double v = 0.0;
+          if (i < s) {
+            if (pc.kind == 2) v = pv[cc][q] * (-c * sc[i]);
+            else if (pc.kind == 3) v = (pc.li0 + pc.lstep * i == 0) ? -c * sc[i] : 0.0;
+            else if (pc.kind == 1) v = bs[i];
+          }
+          Ys[i + cc * YLD] = v;
+        }
+      }
+      __syncwarp();
+      PTR(0);
+#pragma unroll
+      for (int tt = 0; tt < 16; ++tt) {
+        const int i = 8 * tt + gid;
+        acc[tt][0] = tt < 4 * nb ? Ys[i + 2 * tig * YLD] : 0.0;
+        acc[tt][1] = tt < 4 * nb ? Ys[i + (2 * tig + 1) * YLD] : 0.0;
+      }
+      __syncwarp();
+      PTR(1);
+      if (st + LEAF_WARPS < nstripe) load_raw(st + LEAF_WARPS);
+      stripe_solve(acc, A, nb, Ys);
+      PTR(2);
+#pragma unroll
+      for (int tt = 0; tt < 16; ++tt) {
+        if (tt < 4 * nb) {
+          const int i = 8 * tt + gid;
+          Ys[i + 2 * tig * YLD] = acc[tt][0];
+          Ys[i + (2 * tig + 1) * YLD] = acc[tt][1];
+        }
+      }
+      __syncwarp();
+      for (int cc = 0; cc < 8 && cs + cc < c_end; ++cc)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int i = lane + 32 * q;
+          if (i < s) Xi[(long long)(cs + cc) * n + i] = Ys[i + cc * YLD];
+        }
+      __syncwarp();
+      PTR(3);
+    }
+#undef PTR
+    if (a.trace) {                      // (no barrier inside a stamp after divergent loops)
       __syncthreads();
-      LT(3);
-      leaf_block_solve(A, sp, P, ncp);
-      LT(4);
-      for (int cc = warp; cc < nc; cc += LEAF_WARPS)
-        for (int i = t & 31; i < s; i += 32) Xi[(long long)(c0 + cc) * n + r0 + i] = P[i + cc * LDP_LEAF];
-      __syncthreads();
-      LT(5);
+      if (trc) {
+        unsigned long long tm;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm));
+        a.trace[2048 + leaf * 4 + 3] = tm;
+      }
     }
   } else {
     // ---- solve mode: factor from HBM, right-hand sides b (+ dt f) -> y (y may alias b)
     for (int j = warp; j < sp; j += LEAF_WARPS)
-      for (int i = t & 31; i < sp; i += 32) A[i + j * LDA_LEAF] = LUg[i + j * sp];
-    const long long ib = (long long)inst * a.ld * a.nrhs;
-    for (int c0 = 0; c0 < a.nrhs; c0 += NCHUNK) {
-      const int nc = min(NCHUNK, a.nrhs - c0), ncp = round_up(nc, 8);
-      for (int e = t; e < sp * ncp; e += LEAF_THREADS) {
-        const int i = e % sp, cc = e / sp;
-        double v = 0.0;
-        if (i < s && cc < nc) {
-          const long long o = ib + (long long)(c0 + cc) * a.ld + r0 + i;
-          v = a.b[o];
-          if (a.f) v += a.dt * a.f[o];                  // b = u + dt f (S7)
+      for (int i = lane; i < sp; i += 32) A[i + j * LDA_LEAF] = LUg[i + j * sp];
+    __syncthreads();
+    const long long ib = (long long)inst * a.ld * a.nrhs + r0;
+    const int nstripe = (a.nrhs + 7) >> 3;
+    for (int st = warp; st < nstripe; st += LEAF_WARPS) {
+      const int cA = 8 * st + 2 * tig;
+#pragma unroll
+      for (int tt = 0; tt < 16; ++tt) {
+        const int i = 8 * tt + gid;
+        const bool in = tt < 4 * nb && i < s;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          double v = 0.0;
+          if (in && cA + j < a.nrhs) {
+            const long long o = ib + (long long)(cA + j) * a.ld + i;
+            v = a.b[o];
+            if (a.f) v += a.dt * a.f[o];               // b = u + dt f (S7)
+          }
+          acc[tt][j] = v;
         }
-        P[i + cc * LDP_LEAF] = v;
       }
-      __syncthreads();
-      leaf_block_solve(A, sp, P, ncp);
-      for (int cc = warp; cc < nc; cc += LEAF_WARPS)
-        for (int i = t & 31; i < s; i += 32)
-          a.y[ib + (long long)(c0 + cc) * a.ld + r0 + i] = P[i + cc * LDP_LEAF];
-      __syncthreads();
+      stripe_solve(acc, A, nb, Ys);
+#pragma unroll
+      for (int tt = 0; tt < 16; ++tt) {
+        const int i = 8 * tt + gid;
+        if (tt < 4 * nb && i < s) {
+          if (cA < a.nrhs) a.y[ib + (long long)cA * a.ld + i] = acc[tt][0];
+          if (cA + 1 < a.nrhs) a.y[ib + (long long)(cA + 1) * a.ld + i] = acc[tt][1];
+        }
+      }
     }
   }
 }
