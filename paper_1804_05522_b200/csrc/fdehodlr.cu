@@ -16,6 +16,7 @@
 #include "k_level.cuh"
 #include "k_levels.cuh"
 #include "k_matvec.cuh"
+#include "k_tree.cuh"
 
 // ---------------------------------------------------------------------------------------
 // errors, launch accounting
@@ -123,6 +124,14 @@ struct fde_hodlr {
   double *d_Kst = nullptr, *d_sums = nullptr, *d_lvpart = nullptr;
   unsigned* d_bar = nullptr;
   int* d_post = nullptr;
+  // projected-tree path (k_leaf Q phase + k_tree) for the fused factor + solve step
+  bool tree_ok = false;
+  double *d_Q = nullptr, *d_S = nullptr;
+  long long qlev[LMAX + 1] = {}, slev[LMAX] = {}, qinst = 0, sinst = 0;
+  int trc[LMAX] = {};
+  int tr_grid = 0;
+  TrArgs tr_geo{};
+  size_t tr_smem = 0;
   int npost = 0;
   // compression scratch
   PcTask* d_tasks = nullptr;
@@ -448,6 +457,102 @@ static int lv_config(const fde_hodlr* H, int mode, int nrhs, LvCfg* cfg) {
                  H->kmax, NCPX);
 }
 
+// Layout of the projected-tree path (k_tree.cuh): Q stores of levels 1..L (leaves: L), S
+// stores of levels 0..L-1, work split and shared-memory geometry.  Leaves tree_ok = false
+// (the level-pass path is used) when the panel is too wide for the leaf Q phase.
+static int tree_layout(fde_hodlr* H) {
+  const int L = H->L, B = H->batch, NC = H->xcol[L];
+  H->tree_ok = false;
+  if (L < 1 || NC - 1 > 176) return FDE_OK;
+  long long q = 0, sofs = 0;
+  for (int m = 1; m <= L; ++m) {
+    H->qlev[m] = q;
+    q += (1LL << m) * (long long)(H->xcol[m] - 1) * H->xcol[m];
+  }
+  for (int m = 0; m < L; ++m) {
+    H->slev[m] = sofs;
+    sofs += (1LL << m) * 2LL * H->kl[m] * H->xcol[m];
+  }
+  H->qinst = q; H->sinst = sofs;
+  int dev = 0, nsm = 0;
+  CU(cudaGetDevice(&dev));
+  CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  TrArgs& g = H->tr_geo;
+  const int kp = round_up(H->kmax, 8), K4 = round_up(2 * H->kmax, 4);
+  g.kp = kp; g.ldk = kp + 1;
+  g.lds = round_up(NC, 16) + 4;                       // = 4 mod 16: conflict-free B fragments
+  g.lda = K4 + ((4 - K4 % 16) + 16) % 16;
+  int rch_max = 8;
+  for (int m = 0; m < L; ++m) {
+    const int nodes = B << m, rows = H->xcol[m] - 1;
+    int rc = std::max(1, nsm / std::max(1, nodes));
+    rc = std::min(rc, std::max(1, (rows + 15) / 16));
+    H->trc[m] = rc;
+    rch_max = std::max(rch_max, round_up((std::max(rows, 1) + rc - 1) / rc, 8));
+  }
+  g.rch_max = rch_max;
+  long long o = 0;
+  g.off_B = (int)o; o += (long long)kp * g.ldk;
+  g.off_C = (int)o; o += (long long)kp * g.ldk;
+  g.off_M = (int)o; o += (long long)kp * g.ldk;
+  g.off_M2 = (int)o; o += (long long)kp * g.ldk;
+  o = round_up((int)o, 2);
+  g.off_S = (int)o; o += (long long)K4 * g.lds;
+  g.off_T = (int)o; o += (long long)kp * g.lds;
+  g.off_Z = (int)o; o += 2LL * H->kmax * NC;
+  g.off_U = (int)o; o += 2LL * 2 * TR_SUB * NC;
+  // final pass: 4 v vectors + max(4 warps x 2 S buffers, X block + partials)
+  const long long fin = 4LL * round_up(NC, 8) + std::max(8LL * H->kmax * NC, (long long)NC * 128 + 256);
+  const size_t bytes = (size_t)std::max(o, fin) * sizeof(double);
+  if (bytes > 227 * 1024) return FDE_OK;
+  CU(cudaFuncSetAttribute(k_tree, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  int per_sm = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tree, TR_THREADS, bytes));
+  if (per_sm < 1) return FDE_OK;
+  H->tr_grid = nsm * per_sm;
+  H->tr_smem = bytes;
+  TRY(dalloc(H, &H->d_Q, (size_t)B * H->qinst));
+  TRY(dalloc(H, &H->d_S, (size_t)B * H->sinst));
+  H->tree_ok = true;
+  return FDE_OK;
+}
+
+static int launch_tree(fde_hodlr* H, double* u_next, cudaStream_t s) {
+  TrArgs a = H->tr_geo;
+  const int L = H->L;
+  a.L = L; a.NC = H->xcol[L]; a.nleaf = H->nleaf; a.batch = H->batch; a.kmaxc = H->kmax;
+  for (int l = 0; l <= L; ++l) a.xc[l] = H->xcol[l];
+  for (int m = 0; m < L; ++m) { a.rc[m] = H->trc[m]; a.slev[m] = H->slev[m]; }
+  for (int m = 1; m <= L; ++m) a.qlev[m] = H->qlev[m];
+  a.qinst = H->qinst; a.sinst = H->sinst;
+  a.Qleaf = H->d_Q + H->qlev[L]; a.Q = H->d_Q; a.Sst = H->d_S;
+  a.X = H->d_X; a.xstride = H->xstride; a.n = H->n;
+  a.leaf_r0 = H->tree.leaf_r0; a.leaf_n = H->tree.leaf_n;
+  a.u = u_next; a.bar = H->d_bar; a.st = H->d_status;
+  a.trace = g_trace;                                   // (reset by factor_impl)
+  CU(cudaMemsetAsync(H->d_bar, 0, sizeof(unsigned), s));
+  void* args[] = {&a};
+  { PROF("k_tree"); CU(cudaLaunchCooperativeKernel((void*)k_tree, dim3(H->tr_grid), dim3(TR_THREADS), args, H->tr_smem, s)); }
+  LAUNCHED();
+  if (g_trace) {
+    std::vector<unsigned long long> h(64);
+    CU(cudaStreamSynchronize(s));
+    CU(cudaMemcpy(h.data(), g_trace + 1024, 64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    fprintf(stderr, "k_tree CTA0 (us): ");
+    for (int m = 0; m < H->L; ++m)
+      fprintf(stderr, "L%d work %.1f bar %.1f | ", H->L - 1 - m, (h[2 * m + 1] - h[2 * m]) * 1e-3,
+              (h[2 * m + 2] - h[2 * m + 1]) * 1e-3);
+    fprintf(stderr, "final %.1f ; rc:", (h[2 * H->L + 1] - h[2 * H->L]) * 1e-3);
+    for (int m = 0; m < H->L; ++m) fprintf(stderr, " %d", H->trc[m]);
+    fprintf(stderr, " grid %d smem %zu\n", H->tr_grid, H->tr_smem);
+    std::vector<unsigned long long> c(16);
+    CU(cudaMemcpy(c.data(), g_trace + 1100, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    fprintf(stderr, "k_tree CTA0 unit cycles: stage %llu sc+T %llu gj %llu S %llu Qupd %llu | final: vrec %llu xwait %llu gemv %llu\n",
+            c[0], c[1], c[2], c[3], c[4], c[10], c[11], c[12]);
+  }
+  return FDE_OK;
+}
+
 static void post_order(int d, int j, int D, std::vector<int>& out) {
   if (d + 1 < D) { post_order(d + 1, 2 * j, D, out); post_order(d + 1, 2 * j + 1, D, out); }
   out.push_back(d);
@@ -511,6 +616,7 @@ static int finalize_layout(fde_hodlr* H, cudaStream_t s) {
   TRY(dalloc(H, &H->d_post, std::max<size_t>(2, post.size())));
   if (!post.empty())
     CU(cudaMemcpy(H->d_post, post.data(), post.size() * sizeof(int), cudaMemcpyHostToDevice));
+  TRY(tree_layout(H));
   H->layout_done = true;
   return FDE_OK;
 }
@@ -690,8 +796,14 @@ static int factor_impl(fde_hodlr* H, const double* dp, const double* dm, int nf,
   la.keep = keep; la.nf = nf; la.u_prev = u_prev; la.f = f; la.st = H->d_status;
   TRY(trace_reset(s));
   la.trace = g_trace;
+  const bool tree = nf == 1 && !keep && H->tree_ok && !getenv("FDE_LEVEL_PASSES");
+  if (tree) {
+    la.Q = H->d_Q + H->qlev[L]; la.qinst = H->qinst;
+    la.qstride = (long long)(H->xcol[L] - 1) * H->xcol[L];
+  }
   { PROF("k_leaf"); k_leaf<<<dim3(H->nleaf, B), LEAF_THREADS, LEAF_SMEM, s>>>(la); }
   LAUNCHED();
+  if (tree) return launch_tree(H, u_next, s);
   TRY(launch_levels(H, 0, nf, nullptr, 0, 1, s));
   if (nf) {
     const long long tot = (long long)B * H->n;

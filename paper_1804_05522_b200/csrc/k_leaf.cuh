@@ -31,8 +31,9 @@
 #define YLD 132                      // warp stripe buffer (128 x 8) leading dim (= 4 mod 16)
 #define LEAF_SLOT (LEAF_MAX * LEAF_MAX)   // doubles per kept leaf factor
 #define NCOL_MAX 384                 // panel columns (1 + sum of k_l) held as descriptors in smem
-#define LEAF_SMEM ((LEAF_MAX * LDA_LEAF + 32 * 33 + 3 * LEAF_MAX + LEAF_WARPS * 8 * YLD) * 8 + \
-                   NCOL_MAX * 16)
+#define LEAF_FRONT (32 * 33 + 3 * LEAF_MAX + 2 * NCOL_MAX)        // doubles before the LU region
+#define LEAF_BIG (LEAF_MAX * LDA_LEAF + LEAF_WARPS * 8 * YLD)       // LU + stripe buffers (reused by Q)
+#define LEAF_SMEM ((LEAF_FRONT + LEAF_BIG) * 8)
 #define GJ_WARPS 4                   // warps of the 32 x 32 diagonal-block Gauss-Jordan
 #define LEAF_OVW 8                   // register tiles per warp of an overwrite GEMM
 
@@ -53,6 +54,7 @@ struct LeafArgs {
   int nf;                                    // fused RHS columns (0/1), factor mode
   const double* u_prev; const double* f;     // [batch*n], factor mode with nf = 1
   const double* b; double* y; int nrhs; int ld;   // solve mode
+  double* Q; long long qstride, qinst;       // factor mode: Q_leaf = V_all^T X_leaf (or null)
   DevStatus* st;
   unsigned long long* trace;                 // optional phase clocks (FDE_TRACE_LEVELS)
 };
@@ -365,19 +367,79 @@ __device__ __forceinline__ PanelCol panel_col(const LeafArgs& a, int inst, int l
   return pc;
 }
 
+// ---- S5 input: projection of the leaf panel on every ancestor's V factor -----------------
+// Q_leaf = V_all[leaf rows]^T X_leaf  ((NC-1) x NC, row-major, ld NC), where V-column j is
+// the V factor column of X column j+1 (level l, q): child 0 rows of a level-l node carry
+// V21 = [J L_l, e_{n1-1}], child 1 rows V12 = [L_l, e_0] (k_levels.cuh / k_tree.cuh).  Runs
+// after all stripes: the LU + stripe buffers are reused for V (NV x 128 col-major) and
+// chunks of X re-read from L2.  DMMA tiles: warp unit = (m-tile, 2 n-tiles), A reused.
+__device__ void leaf_project(const LeafArgs& a, double* big, const PanelCol* pcd, int c_begin,
+                             int NC, int s, int sp, const double* Xi, double* Qo) {
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31, gid = lane >> 2, tig = lane & 3;
+  const int n = a.tree.n, NV = NC - 1, NVP = round_up(NV, 8), MT = NVP >> 3;
+  double* Vs = big;                                   // [NVP cols][LDA_LEAF]
+  double* Xs = big + NVP * LDA_LEAF;
+  const int XCH = min(((LEAF_BIG - NVP * LDA_LEAF) / LDA_LEAF) & ~15, round_up(NC, 16));
+  __syncthreads();                                    // every warp is done with the LU
+  for (int j = warp; j < NVP; j += LEAF_WARPS) {
+    const PanelCol pc = j < NV ? pcd[j + 1 - c_begin] : PanelCol{a.Lf, 0, 0, 0, 0, 0};
+    for (int q = 0; q < LEAF_MAX / 32; ++q) {
+      const int i = lane + 32 * q;
+      if (pc.kind == 2 && i < s) cp_async8(&Vs[i + j * LDA_LEAF], pc.Lq + pc.li0 + pc.lstep * i);
+      else Vs[i + j * LDA_LEAF] = (pc.kind == 3 && i < s && pc.li0 + pc.lstep * i == 0) ? 1.0 : 0.0;
+    }
+  }
+  cp_async_commit();
+  for (int c0 = 0; c0 < NC; c0 += XCH) {
+    const int ncp = min(XCH, round_up(NC - c0, 16));
+    for (int cc = warp; cc < ncp; cc += LEAF_WARPS)
+      for (int q = 0; q < LEAF_MAX / 32; ++q) {
+        const int i = lane + 32 * q;
+        if (c0 + cc < NC && i < s) cp_async8(&Xs[i + cc * LDA_LEAF], Xi + (long long)(c0 + cc) * n + i);
+        else Xs[i + cc * LDA_LEAF] = 0.0;
+      }
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+    const int NP = ncp >> 4;
+    for (int u = warp; u < MT * NP; u += LEAF_WARPS) {
+      const int mt = u % MT, n0 = (u / MT) * 16;
+      double d0[2] = {0.0, 0.0}, d1[2] = {0.0, 0.0};
+      const double* ap = Vs + (8 * mt + gid) * LDA_LEAF + tig;
+      const double* bp0 = Xs + (n0 + gid) * LDA_LEAF + tig;
+      const double* bp1 = bp0 + 8 * LDA_LEAF;
+#pragma unroll 8
+      for (int k0 = 0; k0 < sp; k0 += 4) {
+        const double av = ap[k0];
+        dmma884(d0[0], d0[1], av, bp0[k0]);
+        dmma884(d1[0], d1[1], av, bp1[k0]);
+      }
+      const int j = 8 * mt + gid, c = c0 + n0 + 2 * tig;
+      if (j < NV) {
+        double* qr = Qo + (long long)j * NC;
+        if (c < NC) qr[c] = d0[0];
+        if (c + 1 < NC) qr[c + 1] = d0[1];
+        if (c + 8 < NC) qr[c + 8] = d1[0];
+        if (c + 9 < NC) qr[c + 9] = d1[1];
+      }
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(LEAF_THREADS, 1)
 k_leaf(const LeafArgs a) {
   extern __shared__ double smem[];
-  double* A = smem;                               // [LEAF_MAX cols][LDA_LEAF]
-  double* S = A + LEAF_MAX * LDA_LEAF;            // 32 x 33 Gauss-Jordan scratch
+  double* S = smem;                               // 32 x 33 scratch (g staging, Gauss-Jordan)
   double* dps = S + 32 * 33;                      // d+ / d- of the leaf rows
   double* dms = dps + LEAF_MAX;
+  double* bs = dms + LEAF_MAX;                    // fused rhs b = u + dt f of the leaf
+  PanelCol* pcd = reinterpret_cast<PanelCol*>(bs + LEAF_MAX);   // panel column descriptors
+  double* A = smem + LEAF_FRONT;                  // [LEAF_MAX cols][LDA_LEAF]
   const TreeDev& tr = a.tree;
   const int leaf = blockIdx.x, inst = blockIdx.y, t = threadIdx.x, warp = t >> 5;
   const int lane = t & 31, gid = lane >> 2, tig = lane & 3;
-  double* Ys = dms + LEAF_MAX + warp * 8 * YLD;   // warp-private 128 x 8 stripe buffer
-  PanelCol* pcd = reinterpret_cast<PanelCol*>(dms + LEAF_MAX + LEAF_WARPS * 8 * YLD);
-  double* bs = reinterpret_cast<double*>(pcd + NCOL_MAX);   // fused rhs b = u + dt f of the leaf
+  double* Ys = A + LEAF_MAX * LDA_LEAF + warp * 8 * YLD;   // warp-private 128 x 8 stripe buffer
   const int n = tr.n;
   const int r0 = tr.leaf_r0[leaf], s = tr.leaf_n[leaf];
   const int sp = round_up(s, 32), nb = sp >> 5;
@@ -513,6 +575,7 @@ k_leaf(const LeafArgs a) {
       PTR(3);
     }
 #undef PTR
+    if (a.Q) leaf_project(a, A, pcd, c_begin, c_end, s, sp, Xi, a.Q + (long long)inst * a.qinst + (long long)leaf * a.qstride);
     if (a.trace) {                      // (no barrier inside a stamp after divergent loops)
       __syncthreads();
       if (trc) {

@@ -1,0 +1,342 @@
+// k_tree.cuh -- S5 + S6 for the fused factor + solve step: the Sherman-Morrison-Woodbury
+// level recursion carried out on small projected matrices instead of passes over the panel.
+//
+// Notation (k_levels.cuh): X^(L) = the leaf-solved panel
+// [A_leaf^{-1} b | A_leaf^{-1} U_0 .. U_{L-1}] (k_leaf), X^(m) = the panel after the SMW updates
+// of levels L-1 .. m; xc[l] = first panel column of level l (xc[0] = 1: column 0 is the rhs),
+// k_l = xc[l+1] - xc[l].  V_l(row) is the level-l V factor row of a row (V21 on child 1 rows,
+// V12 on child 2 rows).  For a node mu of level m (or a leaf, m = L):
+//     Q_mu = V_{<m}[mu rows]^T X^(m)[mu rows, 0:xc[m]]        ((xc[m]-1) x xc[m]).
+// At a node mu of level m with children c1, c2 (level m+1), the level-m rows of Q_c are
+//     B = Q_c2[lvl m, m-cols] = V12^T W2,  C = Q_c1[lvl m, m-cols] = V21^T W1,
+//     R_top = Q_c2[lvl m, <xc[m]] = V12^T X2,  R_bot = Q_c1[lvl m, <xc[m]] = V21^T X1,
+// so the node's K system (K = [[I, B], [C, I]], Sc = I - C B) gives
+//     S_bot = Sc^{-1}(R_bot - C R_top),  S_top = R_top - B S_bot,
+// the update X1 -= W1 S_top, X2 -= W2 S_bot becomes, projected on the ancestors' V,
+//     Q_mu = Q_c1[<, <] + Q_c2[<, <] - Q_c1[<, m-cols] S_top - Q_c2[<, m-cols] S_bot,
+// and the solution is  u[leaf rows] = X^(L)[leaf rows, :] v_leaf,  v = M_{L-1} .. M_0 e_0 with
+// M_m v: v[m-cols] = -S_side(m) v[<xc[m]]  (side = the child of the level-m node holding the
+// leaf).  All arithmetic on (xc x xc)-sized matrices: no pass over the n rows except the
+// final u = X v.  Sc is inverted by unpivoted Gauss-Jordan (reading R17).
+//
+// One persistent cooperative launch: levels L-1 .. 0 separated by grid barriers (work unit
+// = node x row chunk of Q_mu; S is recomputed per chunk, stored by chunk 0), then the per-leaf
+// v recursion and u = X v.  Every reduction has a fixed order (deterministic).
+#pragma once
+#include "fde_common.cuh"
+#include "fde_dmma.cuh"
+
+#define TR_THREADS 256
+#define TR_WARPS (TR_THREADS / 32)
+
+struct TrArgs {
+  int L, NC, nleaf, batch, kmaxc;
+  int xc[LMAX + 1];
+  int rc[LMAX];                  // row chunks per node of level m
+  long long qlev[LMAX + 1];      // per-instance offset of level m's Q store (m = 1..L)
+  long long slev[LMAX];          // per-instance offset of level m's S store
+  long long qinst, sinst;
+  const double* Qleaf;           // level-L (leaf) Q store: Q + qlev[L] == Qleaf
+  double* Q;                     // Q store of all levels 1..L
+  double* Sst;                   // S store: node (m, j): [S_top (k x xc[m]) | S_bot]
+  const double* X; long long xstride; int n;
+  const int* leaf_r0; const int* leaf_n;
+  double* u;                     // [batch * n] output
+  unsigned* bar;
+  DevStatus* st;
+  unsigned long long* trace;     // optional: globaltimer after every level (FDE_TRACE_LEVELS)
+  int kp, lds, ldk, lda, rch_max;  // smem geometry (host computed)
+  int off_B, off_C, off_M, off_M2, off_S, off_T, off_Z, off_U;
+};
+
+__device__ __forceinline__ unsigned tr_ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void tr_grid_barrier(unsigned* bar, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    while (tr_ld_acquire(bar) < target) __nanosleep(20);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+#define TR_SUB 16                // Q_mu rows per streamed sub-chunk (double buffered)
+#define TR_NT 6                  // n-tiles per warp in the Q update (4 warp columns x 6 = 24 n-tiles)
+
+// O[q][c] = Cin[q][c] + sgn * sum_p A[q][p] B[p][c]  (q < M, c < N; Cin may be null = 0).
+// Row-major shared-memory operands; each thread owns 4 consecutive columns of one row (four
+// independent FMA chains).  Reads up to round4(N) - 1 columns of B / Cin (callers pad).
+__device__ __forceinline__ void tr_mm(double* O, int ldo, const double* Cin, int ldci, const double* A,
+                                      int lda, const double* B, int ldb, int M, int N, int K, double sgn) {
+  const int NQ = (N + 3) >> 2;
+  for (int e = threadIdx.x; e < M * NQ; e += TR_THREADS) {
+    const int q = e / NQ, c0 = (e - q * NQ) * 4;
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+    if (Cin) { const double* ci = Cin + q * ldci + c0; v0 = ci[0]; v1 = ci[1]; v2 = ci[2]; v3 = ci[3]; }
+    const double* ar = A + q * lda;
+    const double* bc = B + c0;
+#pragma unroll 4
+    for (int p = 0; p < K; ++p) {
+      const double av = sgn * ar[p];
+      const double* br = bc + p * ldb;
+      v0 = fma(av, br[0], v0); v1 = fma(av, br[1], v1); v2 = fma(av, br[2], v2); v3 = fma(av, br[3], v3);
+    }
+    double* o = O + q * ldo + c0;
+    o[0] = v0;
+    if (c0 + 1 < N) o[1] = v1;
+    if (c0 + 2 < N) o[2] = v2;
+    if (c0 + 3 < N) o[3] = v3;
+  }
+}
+
+__device__ __forceinline__ double tr_rcp(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+
+// One (node, row chunk) unit of level m.  All global reads are asynchronous copies into
+// shared memory (cp.async), so the latency of L2/HBM is paid once per stage, not per load.
+__device__ void tr_unit(const TrArgs& a, double* sm, int inst, int m, int j, int chunk) {
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31, gid = lane >> 2, tig = lane & 3;
+  const int xm = a.xc[m], k = a.xc[m + 1] - xm, ncol1 = a.xc[m + 1];   // child Q: (ncol1-1) x ncol1
+  const int lds = a.lds, ldk = a.ldk;
+  double* Bs = sm + a.off_B;      // k x k   (ld ldk)
+  double* Cs = sm + a.off_C;
+  double* Ms = sm + a.off_M;      // Sc, then Sc^{-1} (Gauss-Jordan ping-pong with M2)
+  double* M2 = sm + a.off_M2;
+  double* Ss = sm + a.off_S;      // rows 0..k-1: S_top; rows k..2k-1: T, then S_bot (ld lds)
+  double* Ts = sm + a.off_T;      // k x xm scratch (S_bot before it moves into Ss)
+  double* Z1 = sm + a.off_Z;      // level-m rows of Q_c1 / Q_c2 (k x ncol1 each)
+  double* Z2 = Z1 + k * ncol1;
+  double* Ub = sm + a.off_U;      // 2 buffers x [Q_c1 rows | Q_c2 rows] (TR_SUB x ncol1 each)
+  const long long qs1 = (long long)(ncol1 - 1) * ncol1;
+  const double* Q1 = a.Q + (long long)inst * a.qinst + a.qlev[m + 1] + (long long)(2 * j) * qs1;
+  const double* Q2 = Q1 + qs1;
+  const int r0 = xm - 1;          // first level-m row of the child Q
+  // row chunk of Q_mu handled by this unit
+  const int nrow = xm - 1;
+  const int rch = m > 0 ? round_up((nrow + a.rc[m] - 1) / a.rc[m], 8) : 0;
+  const int ra = chunk * rch, rb = m > 0 ? min(nrow, ra + rch) : 0;
+  const int nsub = rb > ra ? (rb - ra + TR_SUB - 1) / TR_SUB : 0;
+  auto issue_sub = [&](int sc) {
+    const int rs = ra + sc * TR_SUB, nr = min(TR_SUB, rb - rs);
+    double* U1 = Ub + (sc & 1) * 2 * TR_SUB * ncol1;
+    double* U2 = U1 + TR_SUB * ncol1;
+    const double* g1 = Q1 + (long long)rs * ncol1;
+    const double* g2 = Q2 + (long long)rs * ncol1;
+    for (int e = t; e < nr * ncol1; e += TR_THREADS) { cp_async8(U1 + e, g1 + e); cp_async8(U2 + e, g2 + e); }
+    cp_async_commit();
+  };
+  const bool tdbg = a.trace && blockIdx.x == 0 && t == 0;
+  long long tcl = clock64();
+#define TPH(i) do { if (tdbg) { const long long t_ = clock64(); a.trace[1100 + (i)] += t_ - tcl; tcl = t_; } } while (0)
+  // 1. stage the level-m rows of both children (+ the first Q sub-chunk, in flight meanwhile)
+  for (int e = t; e < k * ncol1; e += TR_THREADS) {
+    cp_async8(Z1 + e, Q1 + (long long)r0 * ncol1 + e);
+    cp_async8(Z2 + e, Q2 + (long long)r0 * ncol1 + e);
+  }
+  cp_async_commit();
+  if (nsub > 0) { issue_sub(0); cp_async_wait_group1(); } else cp_async_wait_all();
+  __syncthreads();
+  TPH(0);
+  // 2. Sc = I - C B ; T = R_bot - C R_top   (B = Z2[:, m-cols], C = Z1[:, m-cols])
+  for (int e = t; e < k * k; e += TR_THREADS) {
+    const int q = e / k, c = e % k;
+    Bs[q * ldk + c] = Z2[q * ncol1 + xm + c];
+    Cs[q * ldk + c] = Z1[q * ncol1 + xm + c];
+    Ms[q * ldk + c] = (q == c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  tr_mm(Ms, ldk, Ms, ldk, Cs, ldk, Bs, ldk, k, k, k, -1.0);
+  tr_mm(Ts, lds, Z1, ncol1, Cs, ldk, Z2, ncol1, k, xm, k, -1.0);
+  __syncthreads();
+  TPH(1);
+  // 3. Sc^{-1}: unpivoted Gauss-Jordan (reading R17), ping-pong Ms <-> M2, one barrier per pivot
+  for (int p = 0; p < k; ++p) {
+    const double* src = (p & 1) ? M2 : Ms;
+    double* dst = (p & 1) ? Ms : M2;
+    const double piv = src[p * ldk + p];
+    if (t == 0 && !(isfinite(piv) && fabs(piv) > 0.0))
+      latch_status(a.st, FDE_ESINGULAR, inst * 65536 + 32768 + node_index(m, j));
+    const double rp = tr_rcp(piv);
+    for (int e = t; e < k * k; e += TR_THREADS) {
+      const int q = e / k, cc = e % k;
+      const double mqp = src[q * ldk + p], mpc = src[p * ldk + cc], mqc = src[q * ldk + cc];
+      double v;
+      if (q == p) v = (cc == p) ? rp : mpc * rp;
+      else v = (cc == p) ? -mqp * rp : fma(-mqp * rp, mpc, mqc);
+      dst[q * ldk + cc] = v;
+    }
+    __syncthreads();
+  }
+  TPH(2);
+  const double* Mi = (k & 1) ? M2 : Ms;            // where the inverse ended up
+  // 4. S_bot = Sc^{-1} T -> Ss rows k..2k-1 ; S_top = R_top - B S_bot -> Ss rows 0..k-1
+  tr_mm(Ss + k * lds, lds, nullptr, 0, Mi, ldk, Ts, lds, k, xm, k, 1.0);
+  __syncthreads();
+  tr_mm(Ss, lds, Z2, ncol1, Bs, ldk, Ss + k * lds, lds, k, xm, k, -1.0);
+  // zero the K padding rows 2k .. round4(2k) and the column padding of S
+  const int K4 = round_up(2 * k, 4), xmp = round_up(xm, 16);
+  if (xmp > xm)
+    for (int e = t; e < K4 * (xmp - xm); e += TR_THREADS) Ss[(e / (xmp - xm)) * lds + xm + e % (xmp - xm)] = 0.0;
+  for (int e = t; e < (K4 - 2 * k) * xmp; e += TR_THREADS) Ss[(2 * k + e / xmp) * lds + e % xmp] = 0.0;
+  __syncthreads();
+  if (chunk == 0) {                       // keep S for the per-leaf v recursion
+    double* So = a.Sst + (long long)inst * a.sinst + a.slev[m] + (long long)j * 2 * k * xm;
+    for (int e = t; e < 2 * k * xm; e += TR_THREADS) So[e] = Ss[(e / xm) * lds + e % xm];
+  }
+  TPH(3);
+  if (nsub == 0) { __syncthreads(); return; }
+  // 5. Q_mu rows [ra, rb) = Q1 + Q2 - [Q1 m-cols | Q2 m-cols] [S_top; S_bot], streamed in
+  //    sub-chunks of TR_SUB rows (the next sub-chunk's copies overlap this one's DMMA)
+  double* Qo = a.Q + (long long)inst * a.qinst + a.qlev[m] + (long long)j * (long long)nrow * xm;
+  for (int sc = 0; sc < nsub; ++sc) {
+    if (sc + 1 < nsub) { issue_sub(sc + 1); cp_async_wait_group1(); } else cp_async_wait_all();
+    __syncthreads();
+    const int rs = ra + sc * TR_SUB, nr = min(TR_SUB, rb - rs);
+    const double* U1 = Ub + (sc & 1) * 2 * TR_SUB * ncol1;
+    const double* U2 = U1 + TR_SUB * ncol1;
+    // warp -> m-tile (warp & 1) x n-tiles (warp >> 1) + 4 i: A fragment reused TR_NT times
+    const int mt = warp & 1, nt0 = warp >> 1, NT8 = xmp >> 3;
+    const int r = 8 * mt + gid;
+    const bool rok = r < nr;
+    if (8 * mt < nr) {
+      double d[TR_NT][2];
+#pragma unroll
+      for (int i = 0; i < TR_NT; ++i) {
+        const int c = 8 * (nt0 + 4 * i) + 2 * tig;
+        d[i][0] = (rok && c < xm) ? U1[r * ncol1 + c] + U2[r * ncol1 + c] : 0.0;
+        d[i][1] = (rok && c + 1 < xm) ? U1[r * ncol1 + c + 1] + U2[r * ncol1 + c + 1] : 0.0;
+      }
+      const double* bp = Ss + tig * lds + 8 * nt0 + gid;
+      for (int k0 = 0; k0 < K4; k0 += 4) {
+        const int q = k0 + tig;                    // A = -[U1 m-cols | U2 m-cols] (zero padded)
+        const double av = (rok && q < 2 * k) ? -(q < k ? U1[r * ncol1 + xm + q] : U2[r * ncol1 + xm + q - k]) : 0.0;
+#pragma unroll
+        for (int i = 0; i < TR_NT; ++i)
+          if (nt0 + 4 * i < NT8) dmma884(d[i][0], d[i][1], av, bp[k0 * lds + 32 * i]);
+      }
+      if (rok) {
+        double* qr = Qo + (long long)(rs + r) * xm;
+#pragma unroll
+        for (int i = 0; i < TR_NT; ++i) {
+          const int c = 8 * (nt0 + 4 * i) + 2 * tig;
+          if (c < xm) qr[c] = d[i][0];
+          if (c + 1 < xm) qr[c + 1] = d[i][1];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  TPH(4);
+#undef TPH
+}
+
+__global__ void __launch_bounds__(TR_THREADS, 1)
+k_tree(const TrArgs a) {
+  extern __shared__ double sm[];
+  const int G = gridDim.x, b = blockIdx.x;
+  unsigned nbar = 0;
+  auto stamp = [&](int i) {
+    if (a.trace && b == 0 && threadIdx.x == 0) {
+      unsigned long long tm;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm));
+      a.trace[1024 + i] = tm;
+    }
+  };
+  stamp(0);
+  for (int m = a.L - 1; m >= 0; --m) {
+    const int per_inst = (1 << m) * a.rc[m];
+    for (int u = b; u < a.batch * per_inst; u += G) {
+      const int inst = u / per_inst, w = u % per_inst;
+      tr_unit(a, sm, inst, m, w / a.rc[m], w % a.rc[m]);
+    }
+    stamp(2 * (a.L - m) - 1);
+    tr_grid_barrier(a.bar, (++nbar) * G);
+    stamp(2 * (a.L - m));
+  }
+  // per-leaf v recursion (one warp per leaf, S blocks double-buffered through shared memory),
+  // then u = X v with the leaf's panel block copied to shared memory
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int NL = 4;                                  // leaves in flight per CTA (v phase)
+  const int total = a.batch * a.nleaf;
+  const int vstride = round_up(a.NC, 8), sbuf = a.kmaxc * a.NC;
+  double* vs = sm;                                   // [NL][vstride]
+  double* Sb = sm + NL * vstride;                    // v phase: [NL warps][2][kmax x NC]
+  double* Xs = sm + NL * vstride;                    // u phase: [NC cols][128 rows] (aliases Sb)
+  double* part = Xs + (long long)a.NC * 128;         // [2][128]
+  long long fcl = clock64();
+  for (int base = b; base < total; base += NL * G) {
+    if (warp < NL && base + warp * G < total) {
+      const int lu = base + warp * G, inst = lu / a.nleaf, leaf = lu % a.nleaf;
+      double* v = vs + warp * vstride;
+      double* buf = Sb + warp * 2 * sbuf;
+      auto S_of = [&](int m) {
+        const int xm = a.xc[m], k = a.xc[m + 1] - xm;
+        const int jn = leaf >> (a.L - m), side = (leaf >> (a.L - m - 1)) & 1;
+        return a.Sst + (long long)inst * a.sinst + a.slev[m] + (long long)jn * 2 * k * xm + (long long)side * k * xm;
+      };
+      auto issue = [&](int m) {
+        const int xm = a.xc[m], k = a.xc[m + 1] - xm;
+        const double* g = S_of(m);
+        double* d = buf + (m & 1) * sbuf;
+        for (int e = lane; e < k * xm; e += 32) cp_async8(d + e, g + e);
+        cp_async_commit();
+      };
+      for (int c = lane; c < a.NC; c += 32) v[c] = (c == 0) ? 1.0 : 0.0;
+      issue(0);
+      for (int m = 0; m < a.L; ++m) {
+        if (m + 1 < a.L) { issue(m + 1); cp_async_wait_group1(); } else cp_async_wait_all();
+        __syncwarp();
+        const int xm = a.xc[m], k = a.xc[m + 1] - xm;
+        const double* S = buf + (m & 1) * sbuf;
+        for (int q = 0; q < k; ++q) {
+          double acc = 0.0;
+          for (int c = lane; c < xm; c += 32) acc = fma(S[q * xm + c], v[c], acc);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+          if (lane == 0) v[xm + q] = -acc;
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    if (a.trace && b == 0 && t == 0) { const long long t_ = clock64(); a.trace[1110] += t_ - fcl; fcl = t_; }
+    for (int w = 0; w < NL && base + w * G < total; ++w) {
+      const int lu = base + w * G, inst = lu / a.nleaf, leaf = lu % a.nleaf;
+      const int r0 = a.leaf_r0[leaf], s = a.leaf_n[leaf];
+      const double* Xi = a.X + (long long)inst * a.xstride + r0;
+      for (int e = t; e < a.NC * 128; e += TR_THREADS) {
+        const int c = e >> 7, i = e & 127;
+        if (i < s) cp_async8(Xs + e, Xi + (long long)c * a.n + i);
+      }
+      cp_async_commit();
+      cp_async_wait_all();
+      __syncthreads();
+      if (a.trace && b == 0 && t == 0) { const long long t_ = clock64(); a.trace[1111] += t_ - fcl; fcl = t_; }
+      const double* v = vs + w * vstride;
+      {
+        const int i = t & 127, h = t >> 7;           // two column halves, fixed-order sums
+        double acc = 0.0;
+        if (i < s)
+          for (int c = h; c < a.NC; c += 2) acc = fma(Xs[c * 128 + i], v[c], acc);
+        part[h * 128 + i] = acc;
+      }
+      __syncthreads();
+      for (int i = t; i < s; i += TR_THREADS) a.u[(long long)inst * a.n + r0 + i] = part[i] + part[128 + i];
+      __syncthreads();
+      if (a.trace && b == 0 && t == 0) { const long long t_ = clock64(); a.trace[1112] += t_ - fcl; fcl = t_; }
+    }
+  }
+  stamp(2 * a.L + 1);
+}

@@ -58,14 +58,18 @@ CASES = [  # n, alpha, leaf, tol, kind
 ]
 
 
+NO_KEEP = 8   # FDE_NO_KEEP: fused factor + solve through the projected tree (k_leaf Q + k_tree)
+
+
 @gpu
+@pytest.mark.parametrize("flags", [0, NO_KEEP], ids=["keep", "nokeep"])
 @pytest.mark.parametrize("n,alpha,leaf,tol,kind", CASES)
-def test_one_step_shared_input(n, alpha, leaf, tol, kind):
+def test_one_step_shared_input(n, alpha, leaf, tol, kind, flags):
     wl = W.make_1d(n, alpha, leaf, tol, K=3, kind=kind)
     st = _stepper(wl)
     u = wl.u0
     for m in (1, 2, 3):
-        ug = _gpu_step(st, wl, m, u)
+        ug = _gpu_step(st, wl, m, u, flags=flags)
         uo = _oracle_step(wl, m, u)
         assert _rel(ug[0], uo) <= 1e-8, (m, _rel(ug[0], uo))
         u = uo[None]                         # shared input for the next step
@@ -102,13 +106,14 @@ def test_cfg1_trajectory():
 
 
 @gpu
-def test_cfg2_steps():
+@pytest.mark.parametrize("flags", [0, NO_KEEP], ids=["keep", "nokeep"])
+def test_cfg2_steps(flags):
     """cfg2 (n = 4096, time-dependent d+-, refactor every step): first 4 steps of the trajectory."""
     wl = W.cfg2(K=4)
     st = _stepper(wl)
     ug, uo = wl.u0, wl.u0
     for m in range(1, 5):
-        ug = _gpu_step(st, wl, m, ug)
+        ug = _gpu_step(st, wl, m, ug, flags=flags)
         uo = _oracle_step(wl, m, uo)[None]
         assert _rel(ug[0], uo[0]) <= 1e-8, (m, _rel(ug[0], uo[0]))
     st.close()
@@ -127,11 +132,24 @@ def test_lu_reuse_matches_refactor():
 
 
 @gpu
-def test_deterministic():
+@pytest.mark.parametrize("flags", [0, NO_KEEP], ids=["keep", "nokeep"])
+def test_deterministic(flags):
     wl = W.make_1d(3000, 1.4, 128, 1e-12, K=1)
-    r1 = _gpu_step(_stepper(wl), wl, 1, wl.u0)
-    r2 = _gpu_step(_stepper(wl), wl, 1, wl.u0)
+    r1 = _gpu_step(_stepper(wl), wl, 1, wl.u0, flags=flags)
+    r2 = _gpu_step(_stepper(wl), wl, 1, wl.u0, flags=flags)
     assert np.array_equal(r1, r2)
+
+
+@gpu
+def test_tree_path_matches_level_passes():
+    """The projected-tree S5/S6 (FDE_NO_KEEP) and the level-pass S5/S6 compute the same
+    SMW solve of the same compressed matrix: equal up to rounding."""
+    wl = W.make_1d(5000, 1.7, 100, 1e-12, K=2)
+    a, b = _stepper(wl), _stepper(wl)
+    ua = _gpu_step(a, wl, 1, wl.u0, flags=0)
+    ub = _gpu_step(b, wl, 1, wl.u0, flags=NO_KEEP)
+    assert _rel(ub[0], ua[0]) <= 1e-11
+    a.close(); b.close()
 
 
 @gpu
@@ -224,13 +242,15 @@ def test_hodlr_solve_and_matvec_multi_rhs():
 
 
 @gpu
-def test_cfg3_full_size_backward_error():
-    """cfg3 at full size (n = 65536, tol 1e-10, leaf 128): eta <= 1e-10 for two steps."""
+@pytest.mark.parametrize("flags", [0, NO_KEEP], ids=["keep", "nokeep"])
+def test_cfg3_full_size_backward_error(flags):
+    """cfg3 at full size (n = 65536, tol 1e-10, leaf 128): eta <= 1e-10 for two steps
+    (NO_KEEP is the launch configuration bench.py times)."""
     wl = W.cfg3(K=2)
     st = _stepper(wl)
     u = wl.u0
     for m in (1, 2):
-        un = _gpu_step(st, wl, m, u)
+        un = _gpu_step(st, wl, m, u, flags=flags)
         dp, dm = wl.coeffs(m)
         b = u[0] + wl.dt * wl.source(m)[0]
         be = backward_error(float(wl.alpha[0]), wl.h, wl.dt, dp[0], dm[0], un[0], b)
