@@ -100,22 +100,34 @@ class ClockSampler:
 
 # ---------------------------------------------------------------------------------------
 def algorithmic_work(ranks, n, leaf_sizes, nf=1):
-    """Per-step algorithmic FP64 flops and compulsory HBM bytes per kernel.
+    """Per-step algorithmic FP64 flops and compulsory bytes per kernel.
 
-    k = r + 1 columns per level (r low-rank + the exact -g_0 column), W_l = sum_{l'<l} k_l'.
-      k_leaf  : LU (2/3 s^3) + triangular solves 2 s^2 (nf + W) per leaf;
-                bytes: write X (n x (nf+W)), read the L_l rows, d+-, u, f.
-      k_levels: per level, reduce V^T X over the nf + W_l + k_l columns and update
-                X[:, :nf+W_l] -= W S (2 n k (nf + W_l + k) + 2 n k (nf + W_l) flops);
-                bytes: read X[:, :nf+W_l+k] + write X[:, :nf+W_l] per level.
+    k = r + 1 columns per level (r low-rank + the exact -g_0 column), NC = nf + sum k (panel
+    width), xc[l] = nf + sum_{l'<l} k_l' (first panel column of level l).
+      k_leaf : per leaf of s rows: LU (2/3) s^3, panel solve 2 s^2 NC, projection of the panel
+               on every ancestor's V factor 2 s (NC - nf) NC (Q = V^T X);
+               bytes: write X (n x NC) and Q (per leaf (NC-1) x NC), read d+-, u, f, L_l rows.
+      k_tree : per node of level m (2^m nodes): the K solve (2/3)(k^3) + 3 k^2 xc[m] flops and
+               the projected update 2 (xc[m]-1) xc[m] 2k; final u = X v: 2 n NC;
+               bytes: read the children's Q, write Q_node, read X once.
+      k_levels (level-pass variant): 2 n k (nf + W_l + k) + 2 n k (nf + W_l) flops per level.
     """
     ks = [r + 1 for r in ranks]
-    Wl = [sum(ks[:l]) for l in range(len(ks))]
-    W = sum(ks)
+    L = len(ks)
+    xc = [nf + sum(ks[:l]) for l in range(L + 1)]
+    NC = xc[L]
+    nleaf = len(leaf_sizes)
     work = {}
-    fl = sum(2.0 / 3.0 * s ** 3 + 2.0 * s * s * (nf + W) for s in leaf_sizes)
-    by = 8.0 * n * (nf + W) + 8.0 * n * sum(ranks) + 8.0 * 4 * n
+    fl = sum(2.0 / 3.0 * s ** 3 + 2.0 * s * s * NC + 2.0 * s * (NC - nf) * NC for s in leaf_sizes)
+    by = 8.0 * n * NC + 8.0 * nleaf * (NC - 1) * NC + 8.0 * n * sum(ranks) + 8.0 * 4 * n
     work["k_leaf"] = (fl, by)
+    ft, bt = 2.0 * n * NC, 8.0 * n * NC
+    for m in range(L):
+        k, x = ks[m], xc[m]
+        ft += 2 ** m * (2.0 / 3.0 * k ** 3 + 3.0 * k * k * x + 2.0 * (x - 1) * x * 2 * k)
+        bt += 2 ** m * 8.0 * (2 * (xc[m + 1] - 1) * xc[m + 1] + (x - 1) * x + 2 * k * x)
+    work["k_tree"] = (ft, bt)
+    Wl = [sum(ks[:l]) for l in range(L)]
     fl_l = sum(2.0 * n * k * (nf + w + k) + 2.0 * n * k * (nf + w) for k, w in zip(ks, Wl))
     by_l = sum(8.0 * n * (nf + w + k) + 8.0 * n * (nf + w) for k, w in zip(ks, Wl))
     work["k_levels"] = (fl_l, by_l)
@@ -319,7 +331,7 @@ def run_ours(args, world, rank, local):
         t_s = kern[dom]["ms_per_step"] / 1e3
         launches_dom = kern[dom]["launches_per_step"]
         fl, by = work.get(dom, (0.0, 0.0))
-        if dom in ("k_leaf", "k_levels"):
+        if dom in ("k_leaf", "k_levels", "k_tree"):
             # FP64 contractions on the DMMA (FP64 tensor) path; MEASURED_PEAKS has no FP64
             # entry: peak = tools/fp64_peak.cu measurement (profiles/fp64_peak_r01.json),
             # equal to the derived 148 SMs x 64 FMA/clk x 2 x 1.965 GHz = 37.2 TFLOP/s

@@ -70,28 +70,28 @@ __device__ __forceinline__ void tr_grid_barrier(unsigned* bar, unsigned target) 
 #define TR_NT 6                  // n-tiles per warp in the Q update (4 warp columns x 6 = 24 n-tiles)
 
 // O[q][c] = Cin[q][c] + sgn * sum_p A[q][p] B[p][c]  (q < M, c < N; Cin may be null = 0).
-// Row-major shared-memory operands; each thread owns 4 consecutive columns of one row (four
-// independent FMA chains).  Reads up to round4(N) - 1 columns of B / Cin (callers pad).
+// Row-major shared-memory operands.  A warp item = 4 rows x 32 consecutive columns (lane =
+// column: conflict-free B / Cin / O accesses, broadcast A loads), four independent FMA chains.
 __device__ __forceinline__ void tr_mm(double* O, int ldo, const double* Cin, int ldci, const double* A,
                                       int lda, const double* B, int ldb, int M, int N, int K, double sgn) {
-  const int NQ = (N + 3) >> 2;
-  for (int e = threadIdx.x; e < M * NQ; e += TR_THREADS) {
-    const int q = e / NQ, c0 = (e - q * NQ) * 4;
-    double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
-    if (Cin) { const double* ci = Cin + q * ldci + c0; v0 = ci[0]; v1 = ci[1]; v2 = ci[2]; v3 = ci[3]; }
-    const double* ar = A + q * lda;
-    const double* bc = B + c0;
-#pragma unroll 4
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int MQ = (M + 3) >> 2, NG = (N + 31) >> 5;
+  for (int it = warp; it < MQ * NG; it += TR_WARPS) {
+    const int q0 = (it / NG) * 4, c = (it % NG) * 32 + lane;
+    const bool cok = c < N;
+    double v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = (Cin && cok && q0 + i < M) ? Cin[(q0 + i) * ldci + c] : 0.0;
+#pragma unroll 2
     for (int p = 0; p < K; ++p) {
-      const double av = sgn * ar[p];
-      const double* br = bc + p * ldb;
-      v0 = fma(av, br[0], v0); v1 = fma(av, br[1], v1); v2 = fma(av, br[2], v2); v3 = fma(av, br[3], v3);
+      const double bv = cok ? B[p * ldb + c] : 0.0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) v[i] = fma(sgn * A[min(q0 + i, M - 1) * lda + p], bv, v[i]);
     }
-    double* o = O + q * ldo + c0;
-    o[0] = v0;
-    if (c0 + 1 < N) o[1] = v1;
-    if (c0 + 2 < N) o[2] = v2;
-    if (c0 + 3 < N) o[3] = v3;
+    if (cok)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (q0 + i < M) O[(q0 + i) * ldo + c] = v[i];
   }
 }
 
@@ -300,12 +300,21 @@ k_tree(const TrArgs a) {
         __syncwarp();
         const int xm = a.xc[m], k = a.xc[m + 1] - xm;
         const double* S = buf + (m & 1) * sbuf;
-        for (int q = 0; q < k; ++q) {
+        if (lane < k) {                            // lane = row q of S_side, 4 FMA chains
+          const double* sr = S + lane * xm;
+          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+          int c = 0;
+          for (; c + 3 < xm; c += 4) {
+            a0 = fma(sr[c], v[c], a0); a1 = fma(sr[c + 1], v[c + 1], a1);
+            a2 = fma(sr[c + 2], v[c + 2], a2); a3 = fma(sr[c + 3], v[c + 3], a3);
+          }
+          for (; c < xm; ++c) a0 = fma(sr[c], v[c], a0);
+          v[xm + lane] = -((a0 + a1) + (a2 + a3));
+        }
+        for (int q = 32 + lane; q < k; q += 32) {  // (k > 32: remaining rows, one per lane)
           double acc = 0.0;
-          for (int c = lane; c < xm; c += 32) acc = fma(S[q * xm + c], v[c], acc);
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-          if (lane == 0) v[xm + q] = -acc;
+          for (int c = 0; c < xm; ++c) acc = fma(S[q * xm + c], v[c], acc);
+          v[xm + q] = -acc;
         }
         __syncwarp();
       }

@@ -142,3 +142,54 @@ class Fde1dStepper:
 
 def launch_count():
     return _lib.load().fde_launch_count()
+
+
+class Fde2dStepper:
+    """One implicit-Euler step of the 2D FDE as the Sylvester equation of Eq. (4.3)
+    over fde2d_step, with the two HODLR operator handles cached across steps.
+
+    step(Fu, Fv, Uu, Uv) solves  A1 X + X A2^T = Uu Uv^T + dt Fu Fv^T  and returns
+    (Xu, Xv, resid, iters) with X = Xu Xv^T (CUDA float64, column blocks (r, n) row-major =
+    column-major (n, r))."""
+
+    def __init__(self, nx, ny, alpha1, alpha2, hx, hy, dt, d1p, d1m, d2p, d2m, tol, ek_tol=1e-11,
+                 ek_maxit=30, leaf=128, rmax=256):
+        self.nx, self.ny = nx, ny
+        self.alpha1, self.alpha2, self.hx, self.hy, self.dt = alpha1, alpha2, hx, hy, dt
+        self.coef = [_dev(d1p, "d1p", nx), _dev(d1m, "d1m", nx), _dev(d2p, "d2p", ny), _dev(d2m, "d2m", ny)]
+        self._keep = (d1p, d1m, d2p, d2m)
+        self.tol, self.ek_tol, self.ek_maxit, self.leaf, self.rmax = tol, ek_tol, ek_maxit, leaf, rmax
+        self._cache = (ctypes.c_void_p * 2)()
+
+    def step(self, Fu, Fv, Uu=None, Uv=None, stream=None):
+        """Fu (rf, nx), Fv (rf, ny), Uu (ru, nx), Uv (ru, ny): CUDA float64, one factor column per row."""
+        dev = Fu.device
+        rf = Fu.shape[0]
+        ru = 0 if Uu is None else Uu.shape[0]
+        Xu = torch.zeros(self.rmax, self.nx, dtype=torch.float64, device=dev)
+        Xv = torch.zeros(self.rmax, self.ny, dtype=torch.float64, device=dev)
+        rx = ctypes.c_int()
+        res = ctypes.c_double()
+        its = ctypes.c_int()
+        nul = ctypes.c_void_p()
+        check(_lib.load().fde2d_step(
+            self.nx, self.ny, self.alpha1, self.alpha2, self.hx, self.hy, self.dt,
+            *self.coef, _dev(Fu, "Fu", rf * self.nx), _dev(Fv, "Fv", rf * self.ny), rf,
+            _dev(Uu, "Uu", ru * self.nx) if ru else nul, _dev(Uv, "Uv", ru * self.ny) if ru else nul, ru,
+            _dev(Xu, "Xu"), _dev(Xv, "Xv"), self.rmax, ctypes.byref(rx), self.tol, self.ek_tol,
+            self.ek_maxit, self.leaf, ctypes.cast(self._cache, ctypes.POINTER(ctypes.c_void_p)),
+            ctypes.byref(res), ctypes.byref(its), 0, _stream(stream)))
+        r = rx.value
+        return Xu[:r].contiguous(), Xv[:r].contiguous(), res.value, its.value
+
+    def close(self):
+        for i in range(2):
+            if self._cache[i]:
+                _lib.load().hodlr_destroy(self._cache[i])
+                self._cache[i] = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,111 @@
+"""GPU <-> oracle parity for the 2D Sylvester step (S8-S10, Eq. 4.3) through the
+C-ABI fde2d_step.  The oracle is the dense Bartels-Stewart solve of oracle/sylvester2d.py
+(reading R11: the right-hand side carries dt).  Bar: relative Frobenius error <= 1e-8 per
+step with ek_tol 1e-11 and HODLR tol 1e-12 (reading R13)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle.sylvester2d import operators_2d, BartelsStewart
+from paper_1804_05522_b200 import workloads as W
+
+gpu = pytest.mark.gpu
+
+
+def _t(a):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device="cuda")
+
+
+def _stepper(wl, ek_tol=1e-11):
+    from paper_1804_05522_b200.hodlr import Fde2dStepper
+    return Fde2dStepper(wl.nx, wl.ny, wl.alpha1, wl.alpha2, wl.hx, wl.hy, wl.dt,
+                        _t(wl.d1p), _t(wl.d1m), _t(wl.d2p), _t(wl.d2m), wl.tol, ek_tol=ek_tol,
+                        leaf=wl.leaf)
+
+
+def _oracle(wl):
+    A1, A2 = operators_2d(wl.alpha1, wl.alpha2, wl.nx, wl.ny, wl.hx, wl.hy, wl.dt,
+                          wl.d1p, wl.d1m, wl.d2p, wl.d2m)
+    return BartelsStewart(A1, A2)
+
+
+def _rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def _run(wl, K, check_every=True):
+    st = _stepper(wl)
+    bs = _oracle(wl)
+    Uo = np.zeros((wl.nx, wl.ny))
+    Xu = Xv = None
+    errs = []
+    for m in range(1, K + 1):
+        Fa, Fb = wl.source_factors(m)
+        Fu, Fv = _t(Fa.T), _t(Fb.T)
+        if Xu is None:
+            Xu, Xv, res, its = st.step(Fu, Fv)
+        else:
+            Xu, Xv, res, its = st.step(Fu, Fv, Xu, Xv)
+        Xg = (Xu.cpu().numpy().T @ Xv.cpu().numpy())
+        Uo = bs.solve(Uo + wl.dt * Fa @ Fb.T)
+        errs.append(_rel(Xg, Uo))
+        assert res <= 10 * wl.ek_tol, (m, res, its)    # ek_tol or its rounding floor (R19)
+    st.close()
+    return errs
+
+
+@gpu
+@pytest.mark.parametrize("n", [64, 200, 512])
+def test_cfg5_shape_trajectory(n):
+    """cfg5 parameters at reduced size: 3 steps, each side propagating its own state."""
+    wl = W.cfg5(n=n)                       # dt = 1/16 as in cfg5
+    errs = _run(wl, 3)
+    assert max(errs) <= 1e-8, errs
+
+
+@gpu
+def test_cfg5_full_size_first_steps():
+    """cfg5 at full size (nx = ny = 2048): two steps against dense Bartels-Stewart."""
+    wl = W.cfg5()
+    errs = _run(wl, 2)
+    assert max(errs) <= 1e-8, errs
+
+
+@gpu
+def test_zero_rhs_gives_zero():
+    wl = W.cfg5(n=128, K=1)
+    st = _stepper(wl)
+    Fu = torch.zeros(2, wl.nx, dtype=torch.float64, device="cuda")
+    Fv = torch.zeros(2, wl.ny, dtype=torch.float64, device="cuda")
+    Xu, Xv, res, its = st.step(Fu, Fv)
+    assert Xu.shape[0] == 0
+    st.close()
+
+
+@gpu
+def test_dt_zero_gives_half_identity_solution():
+    """dt = 0: A1 = A2 = I/2, so A1 X + X A2^T = C gives X = C (C = U U^T, no source)."""
+    wl = W.cfg5(n=150, K=1)
+    wl.dt = 0.0
+    st = _stepper(wl)
+    rng = np.random.default_rng(11)
+    Ua, Ub = rng.standard_normal((3, 150)), rng.standard_normal((3, 150))
+    Fu = torch.zeros(1, 150, dtype=torch.float64, device="cuda")
+    Xu, Xv, res, its = st.step(Fu, Fu.clone(), _t(Ua), _t(Ub))
+    Xg = Xu.cpu().numpy().T @ Xv.cpu().numpy()
+    assert _rel(Xg, Ua.T @ Ub) <= 1e-12
+    st.close()
+
+
+@gpu
+def test_symmetric_data_gives_symmetric_solution():
+    """alpha1 = alpha2, same coefficients, symmetric source  =>  X = X^T."""
+    wl = W.cfg5(n=256, K=1)
+    wl.alpha2 = wl.alpha1
+    wl.d2p, wl.d2m = wl.d1p.copy(), wl.d1m.copy()
+    st = _stepper(wl)
+    Fa, _ = wl.source_factors(1)
+    Xu, Xv, res, its = st.step(_t(Fa.T), _t(Fa.T))
+    Xg = Xu.cpu().numpy().T @ Xv.cpu().numpy()
+    assert _rel(Xg, Xg.T) <= 1e-10
+    st.close()
