@@ -41,6 +41,8 @@ def parse():
                    help="recompute S1 (GL weights) + S2 (compression of T) inside every timed step")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-extra", action="store_true",
+                   help="skip the informational cfg4 (sharded batch) and cfg5 (2D) measurements")
     return p.parse_args()
 
 
@@ -198,6 +200,81 @@ def run_reference(args, world, rank):
 
 
 # ---------------------------------------------------------------------------------------
+def measure_cfg4(dev, world, rank, steps=16):
+    """BASELINE configs[3]: 512 independent n = 8192 problems, time-invariant d+- (factor
+    once), 16 steps; instances sharded over the ranks (shard.py), no collective in the
+    timed region.  Returns instance-steps/s over all ranks (max-over-ranks time)."""
+    import torch
+    from paper_1804_05522_b200 import workloads as W
+    from paper_1804_05522_b200.hodlr import Fde1dStepper
+    from paper_1804_05522_b200.shard import ShardedRun
+    wl = W.cfg4()
+    run = ShardedRun(wl.batch, world, rank)
+    sl = slice(run.start, run.start + run.count)
+    t = lambda a: torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device=dev)
+    dp, dm = wl.coeffs(1)
+    DP, DM, F = t(dp[sl]), t(dm[sl]), t(wl.source(1)[sl])
+    u = [t(wl.u0[sl]), torch.empty_like(t(wl.u0[sl]))]
+    st = Fde1dStepper(wl.n, wl.alpha[sl], wl.h, wl.tol, wl.leaf, batch=run.count)
+    st.step(wl.dt, DP, DM, F, u[0], u_next=u[1], coeffs_changed=True)     # build + factor
+    torch.cuda.synchronize()
+
+    def go(refactor):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        a.record()
+        for k in range(steps):
+            st.step(wl.dt, DP, DM, F, u[k % 2], u_next=u[(k + 1) % 2], coeffs_changed=refactor)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b)
+        if world > 1:
+            x = torch.tensor([ms], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(x, op=torch.distributed.ReduceOp.MAX)
+            ms = float(x.item())
+        return wl.batch * steps / (ms / 1e3), ms
+    go(False)
+    v_reuse, ms_reuse = go(False)
+    v_ref, ms_ref = go(True)
+    st.close()
+    return {"workload": "cfg4: 512 x n=8192, alpha_i~U(1.1,1.9), 16 steps, leaf 128, tol 1e-13 (R18)",
+            "metric": "instance-steps/s", "value_factor_once": v_reuse, "ms_16_steps_factor_once": ms_reuse,
+            "value_refactor_every_step": v_ref, "ms_16_steps_refactor": ms_ref,
+            "sharding": "%d instances per rank (shard.py), no data-path collective" % run.count}
+
+
+def measure_cfg5(dev, steps=4):
+    """BASELINE configs[4]: 2D Sylvester step (fde2d_step), nx = ny = 2048, first `steps`
+    steps of the trajectory (coefficients time-invariant: operators factored once)."""
+    import torch
+    from paper_1804_05522_b200 import workloads as W
+    from paper_1804_05522_b200.hodlr import Fde2dStepper
+    wl = W.cfg5()
+    t = lambda a: torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device=dev)
+    st = Fde2dStepper(wl.nx, wl.ny, wl.alpha1, wl.alpha2, wl.hx, wl.hy, wl.dt, t(wl.d1p), t(wl.d1m),
+                      t(wl.d2p), t(wl.d2m), wl.tol, ek_tol=wl.ek_tol, leaf=wl.leaf)
+    Fs = [tuple(t(f.T) for f in wl.source_factors(m)) for m in range(1, steps + 1)]
+    Xu, Xv, _, _ = st.step(*Fs[0])                     # builds + factors the two operators
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    Xu = Xv = None
+    its = []
+    for m in range(steps):
+        if Xu is None:
+            Xu, Xv, res, it = st.step(*Fs[m])
+        else:
+            Xu, Xv, res, it = st.step(*Fs[m], Xu, Xv)
+        its.append(it)
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    st.close()
+    return {"workload": "cfg5: 2D nx=ny=2048, alpha=(1.3,1.7), rank-4 source, ek_tol 1e-11, tol 1e-12",
+            "metric": "time-steps/s", "value": steps / el, "steps": steps, "ek_iterations": its,
+            "final_rank": int(Xu.shape[0]), "timing": "host wall clock around synchronous fde2d_step calls"}
+
+
 def run_ours(args, world, rank, local):
     import torch
     from paper_1804_05522_b200 import build as B
@@ -363,6 +440,18 @@ def run_ours(args, world, rank, local):
             "gpu_launches": launches,
             "clocks": clk, "e2e": e2e, "roofline": roof, "kernels": kern,
             "other_variant": other}
+    if not args.no_extra:
+        extra = {}
+        try:
+            extra["cfg4"] = measure_cfg4(dev, world, rank)
+        except Exception as e:                              # reported, not fatal for the headline
+            extra["cfg4"] = {"error": str(e)[:200]}
+        if world == 1:
+            try:
+                extra["cfg5"] = measure_cfg5(dev)
+            except Exception as e:
+                extra["cfg5"] = {"error": str(e)[:200]}
+        line["other_configs"] = extra
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_oracle_baseline(wl)
     if rank == 0:
