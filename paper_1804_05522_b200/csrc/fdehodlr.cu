@@ -17,6 +17,7 @@
 #include "k_levels.cuh"
 #include "k_matvec.cuh"
 #include "k_tree.cuh"
+#include "k_solve.cuh"
 
 // ---------------------------------------------------------------------------------------
 // errors, launch accounting
@@ -498,9 +499,10 @@ static int tree_layout(fde_hodlr* H) {
   g.off_M2 = (int)o; o += (long long)kp * g.ldk;
   o = round_up((int)o, 2);
   g.off_S = (int)o; o += (long long)K4 * g.lds;
-  g.off_T = (int)o; o += (long long)kp * g.lds;
-  g.off_Z = (int)o; o += 2LL * H->kmax * NC;
-  g.off_U = (int)o; o += 2LL * 2 * TR_SUB * NC;
+  g.off_T = (int)o;                                   // union { T + Z (S phase), U (Q update) }
+  g.off_Z = (int)(o + (long long)kp * g.lds);
+  g.off_U = (int)o;
+  o += std::max((long long)kp * g.lds + 2LL * H->kmax * NC, 2LL * 2 * TR_SUB * NC);
   // final pass: 4 v vectors + max(4 warps x 2 S buffers, X block + partials)
   const long long fin = 4LL * round_up(NC, 8) + std::max(8LL * H->kmax * NC, (long long)NC * 128 + 256);
   const size_t bytes = (size_t)std::max(o, fin) * sizeof(double);
@@ -814,18 +816,24 @@ static int factor_impl(fde_hodlr* H, const double* dp, const double* dm, int nf,
 }
 
 // solve with the kept factor: y = A^{-1}(b + dt f) (f may be NULL), nrhs columns, ld
+// (k_solve.cuh: explicit leaf inverses, then one streaming pass per level)
 static int solve_impl(fde_hodlr* H, const double* b, const double* f, double* y, int nrhs, int ld,
                       cudaStream_t s) {
   const int L = H->L, B = H->batch;
-  LeafArgs la{};
-  la.tree = H->tree; la.mode = 1; la.LU = H->d_LU; la.lustride = H->lustride;
-  la.b = b; la.y = y; la.nrhs = nrhs; la.ld = ld; la.f = f; la.dt = H->dt; la.st = H->d_status;
-  TRY(trace_reset(s));
-  la.trace = g_trace;
-  { PROF("k_leaf"); k_leaf<<<dim3(H->nleaf, B), LEAF_THREADS, LEAF_SMEM, s>>>(la); }
+  SaArgs sa{};
+  sa.tree = H->tree; sa.Ainv = H->d_LU; sa.lustride = H->lustride; sa.b = b; sa.f = f; sa.dt = H->dt;
+  sa.y = y; sa.nrhs = nrhs; sa.ld = ld;
+  { PROF("k_leaf_apply"); k_leaf_apply<<<dim3(H->nleaf, B), SA_THREADS, 0, s>>>(sa); }
   LAUNCHED();
-  (void)L;
-  TRY(launch_levels(H, 1, 0, y, ld, nrhs, s));
+  SlArgs sl{};
+  sl.tree = H->tree; sl.Lf = H->d_Lf; sl.lf_stride = H->lf_stride; sl.rank = H->d_rank;
+  sl.X = H->d_X; sl.xstride = H->xstride; sl.Kst = H->d_Kst; sl.kstride_inst = H->kstride_inst;
+  sl.Y = y; sl.nrhs = nrhs; sl.ld = ld;
+  for (int l = L - 1; l >= 0; --l) {
+    sl.level = l; sl.k = H->kl[l]; sl.xcol = H->xcol[l]; sl.kofs = H->kofs[l];
+    { PROF("k_solve_level"); k_solve_level<<<dim3(1 << l, B), SL_THREADS, 0, s>>>(sl); }
+    LAUNCHED();
+  }
   return FDE_OK;
 }
 

@@ -495,9 +495,6 @@ k_leaf(const LeafArgs a) {
     // ---- S4: block LU (inverse-diagonal form, off-diagonal blocks negated)
     leaf_block_lu(A, sp, S, a.st, where, a.trace);
     stamp(2);
-    if (a.keep)
-      for (int j = warp; j < sp; j += LEAF_WARPS)
-        for (int i = lane; i < sp; i += 32) LUg[i + j * sp] = A[i + j * LDA_LEAF];
     // ---- panel X = A_leaf^{-1} [b | U_0 .. U_{L-1}] by warp stripes of 8 columns
     const int c_begin = 1 - a.nf, c_end = a.xcol[tr.L];
     const int nstripe = (c_end - c_begin + 7) >> 3;
@@ -575,6 +572,26 @@ k_leaf(const LeafArgs a) {
       PTR(3);
     }
 #undef PTR
+    if (a.keep) {
+      // kept factor = the explicit leaf inverse (stripe solves of the identity): a later solve
+      // is one streaming pass over it (k_solve.cuh), not a sequential block sweep
+      for (int st = warp; st < sp / 8; st += LEAF_WARPS) {
+#pragma unroll
+        for (int tt = 0; tt < 16; ++tt) {
+          const int i = 8 * tt + gid;
+          acc[tt][0] = (i == 8 * st + 2 * tig) ? 1.0 : 0.0;
+          acc[tt][1] = (i == 8 * st + 2 * tig + 1) ? 1.0 : 0.0;
+        }
+        stripe_solve(acc, A, nb, Ys);
+#pragma unroll
+        for (int tt = 0; tt < 16; ++tt)
+          if (tt < 4 * nb) {
+            const int i = 8 * tt + gid;
+            LUg[i + (8 * st + 2 * tig) * sp] = acc[tt][0];
+            LUg[i + (8 * st + 2 * tig + 1) * sp] = acc[tt][1];
+          }
+      }
+    }
     if (a.Q) leaf_project(a, A, pcd, c_begin, c_end, s, sp, Xi, a.Q + (long long)inst * a.qinst + (long long)leaf * a.qstride);
     if (a.trace) {                      // (no barrier inside a stamp after divergent loops)
       __syncthreads();

@@ -1,0 +1,142 @@
+// k_solve.cuh -- S6 with a kept factor (LU reuse; hodlr_solve and fde1d_step with
+// coeffs_changed == 0): the tree-ordered solve as streaming passes.
+//
+//  k_leaf_apply : y[leaf rows] = A_leaf^{-1} (b + dt f)  with the kept explicit leaf inverse
+//                 (k_leaf keep mode stores A_leaf^{-1}, computed by stripe solves of the
+//                 identity): one pass over the 128 x 128 inverse, no sequential sweep.
+//  k_solve_level: one launch per level l = L-1 .. 0, one CTA per (node, instance):
+//                 a = V12^T y2, b = V21^T y1 (fixed-order warp reductions),
+//                 y_v = Sc^{-1}(b - C a), top = a - B y_v   (kept B, C, Sc^{-1}, k_levels.cuh),
+//                 y1 -= W1 top, y2 -= W2 y_v   (W = the level's panel columns kept in X).
+// Per step the factor data are streamed once: HBM-bound by design.
+#pragma once
+#include "fde_common.cuh"
+
+#define SA_THREADS 256
+#define SL_THREADS 256
+#define SA_COLS 4                      // right-hand sides per pass of k_leaf_apply
+
+struct SaArgs {
+  TreeDev tree;
+  const double* Ainv; long long lustride;    // [inst][leaf][sp x sp] column-major
+  const double* b; const double* f; double dt;
+  double* y; int nrhs; int ld;
+};
+
+__global__ void __launch_bounds__(SA_THREADS)
+k_leaf_apply(const SaArgs a) {
+  __shared__ double xs[LEAF_MAX * SA_COLS];
+  __shared__ double part[SA_THREADS * SA_COLS];
+  const int leaf = blockIdx.x, inst = blockIdx.y, t = threadIdx.x;
+  const int r0 = a.tree.leaf_r0[leaf], s = a.tree.leaf_n[leaf], sp = round_up(s, 32);
+  const double* Ai = a.Ainv + (long long)inst * a.lustride + (long long)leaf * LEAF_MAX * LEAF_MAX;
+  const long long ib = (long long)inst * a.ld * a.nrhs + r0;
+  const int i = t % 128, h = t / 128;            // row, half of the j range
+  for (int c0 = 0; c0 < a.nrhs; c0 += SA_COLS) {
+    const int nc = min(SA_COLS, a.nrhs - c0);
+    for (int e = t; e < s * nc; e += SA_THREADS) {
+      const int j = e % s, cc = e / s;
+      const long long o = ib + (long long)(c0 + cc) * a.ld + j;
+      xs[cc * LEAF_MAX + j] = a.b[o] + (a.f ? a.dt * a.f[o] : 0.0);
+    }
+    __syncthreads();
+    double acc[SA_COLS] = {0.0, 0.0, 0.0, 0.0};
+    if (i < s) {
+      const int j0 = h * (s / 2), j1 = h ? s : s / 2;
+      for (int j = j0; j < j1; ++j) {
+        const double av = Ai[(long long)j * sp + i];
+#pragma unroll
+        for (int cc = 0; cc < SA_COLS; ++cc) acc[cc] = fma(av, xs[cc * LEAF_MAX + j], acc[cc]);
+      }
+    }
+#pragma unroll
+    for (int cc = 0; cc < SA_COLS; ++cc) part[cc * SA_THREADS + t] = acc[cc];
+    __syncthreads();
+    for (int e = t; e < s * nc; e += SA_THREADS) {
+      const int r = e % s, cc = e / s;
+      a.y[ib + (long long)(c0 + cc) * a.ld + r] = part[cc * SA_THREADS + r] + part[cc * SA_THREADS + 128 + r];
+    }
+    __syncthreads();
+  }
+}
+
+struct SlArgs {
+  TreeDev tree;
+  int level, k, xcol;                  // level, columns per level (max rank + 1), first X column
+  const double* Lf; long long lf_stride;
+  const int* rank;
+  const double* X; long long xstride;
+  const double* Kst; long long kstride_inst, kofs;
+  double* Y; int nrhs, ld;
+};
+
+__global__ void __launch_bounds__(SL_THREADS)
+k_solve_level(const SlArgs a) {
+  __shared__ double z[2 * KCAP];                 // [a (k) | b (k)]
+  __shared__ double sv[2 * KCAP];                // [top (k) | y_v (k)]
+  const TreeDev& tr = a.tree;
+  const int j = blockIdx.x, inst = blockIdx.y, t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int l = a.level, n = tr.n, L = tr.L, k = a.k;
+  const int nd = node_index(l, j);
+  const int r0 = tr.node_r0[nd], n1 = tr.node_n1[nd], n2 = tr.node_n2[nd];
+  const int m = tr.lev_m[l], r = a.rank[inst * L + l];
+  const double* Ll = a.Lf + (long long)inst * a.lf_stride + tr.lev_lofs[l];
+  const double* Kn = a.Kst + (long long)inst * a.kstride_inst + a.kofs + (long long)j * 3 * k * k;
+  const double* W = a.X + (long long)inst * a.xstride + (long long)a.xcol * n;
+  for (int c = 0; c < a.nrhs; ++c) {
+    double* y = a.Y + (long long)inst * a.ld * a.nrhs + (long long)c * a.ld;
+    // a_q = V12[:, q]^T y2 (child 2 rows), b_q = V21[:, q]^T y1 (child 1 rows)
+    for (int w = warp; w < 2 * k; w += SL_THREADS / 32) {
+      const int q = w % k, side = w / k;       // side 0: a (child 2), 1: b (child 1)
+      double acc = 0.0;
+      if (q == k - 1) {                        // exact column: single row
+        if (lane == 0) acc = side == 0 ? y[r0 + n1] : y[r0 + n1 - 1];
+      } else if (q < r) {
+        const double* Lq = Ll + (long long)q * m;
+        if (side == 0)
+          for (int i2 = lane; i2 < n2; i2 += 32) acc = fma(Lq[i2], y[r0 + n1 + i2], acc);
+        else
+          for (int j1 = lane; j1 < n1; j1 += 32) acc = fma(Lq[n1 - 1 - j1], y[r0 + j1], acc);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) z[side * k + q] = acc;
+    }
+    __syncthreads();
+    if (warp == 0) {                           // y_v = Sc^{-1}(b - C a) ; top = a - B y_v
+      const double* Bk = Kn;
+      const double* Ck = Kn + k * k;
+      const double* Si = Kn + 2 * k * k;
+      for (int q = lane; q < k; q += 32) {
+        double acc = z[k + q];
+        for (int p = 0; p < k; ++p) acc = fma(-Ck[q * k + p], z[p], acc);
+        sv[k + q] = acc;                       // (temporarily b - C a)
+      }
+      __syncwarp();
+      double yv0 = 0.0, yv1 = 0.0;
+      {
+        const int q0 = lane, q1 = lane + 32;
+        if (q0 < k) for (int p = 0; p < k; ++p) yv0 = fma(Si[q0 * k + p], sv[k + p], yv0);
+        if (q1 < k) for (int p = 0; p < k; ++p) yv1 = fma(Si[q1 * k + p], sv[k + p], yv1);
+        __syncwarp();
+        if (q0 < k) sv[k + q0] = yv0;
+        if (q1 < k) sv[k + q1] = yv1;
+      }
+      __syncwarp();
+      for (int q = lane; q < k; q += 32) {
+        double acc = z[q];
+        for (int p = 0; p < k; ++p) acc = fma(-Bk[q * k + p], sv[k + p], acc);
+        sv[q] = acc;
+      }
+    }
+    __syncthreads();
+    // y1 -= W1 top (child 1 rows), y2 -= W2 y_v (child 2 rows)
+    for (int R = r0 + t; R < r0 + n1 + n2; R += SL_THREADS) {
+      const double* s = R < r0 + n1 ? sv : sv + k;
+      double acc = 0.0;
+      for (int q = 0; q < k; ++q) acc = fma(W[(long long)q * n + R], s[q], acc);
+      y[R] -= acc;
+    }
+    __syncthreads();
+  }
+}

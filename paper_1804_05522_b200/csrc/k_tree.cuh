@@ -66,14 +66,15 @@ __device__ __forceinline__ void tr_grid_barrier(unsigned* bar, unsigned target) 
   __syncthreads();
 }
 
-#define TR_SUB 16                // Q_mu rows per streamed sub-chunk (double buffered)
-#define TR_NT 6                  // n-tiles per warp in the Q update (4 warp columns x 6 = 24 n-tiles)
+#define TR_SUB 32                // Q_mu rows per streamed sub-chunk (double buffered)
+#define TR_NT 12                 // n-tiles per warp in the Q update (2 warp columns x 12 = 24 n-tiles)
 
 // O[q][c] = Cin[q][c] + sgn * sum_p A[q][p] B[p][c]  (q < M, c < N; Cin may be null = 0).
 // Row-major shared-memory operands.  A warp item = 4 rows x 32 consecutive columns (lane =
 // column: conflict-free B / Cin / O accesses, broadcast A loads), four independent FMA chains.
 __device__ __forceinline__ void tr_mm(double* O, int ldo, const double* Cin, int ldci, const double* A,
-                                      int lda, const double* B, int ldb, int M, int N, int K, double sgn) {
+                                      int lda, const double* B, int ldb, int M, int N, int K, double sgn,
+                                      double diag_add = 0.0) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int MQ = (M + 3) >> 2, NG = (N + 31) >> 5;
   for (int it = warp; it < MQ * NG; it += TR_WARPS) {
@@ -81,7 +82,8 @@ __device__ __forceinline__ void tr_mm(double* O, int ldo, const double* Cin, int
     const bool cok = c < N;
     double v[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) v[i] = (Cin && cok && q0 + i < M) ? Cin[(q0 + i) * ldci + c] : 0.0;
+    for (int i = 0; i < 4; ++i)
+      v[i] = ((Cin && cok && q0 + i < M) ? Cin[(q0 + i) * ldci + c] : 0.0) + (q0 + i == c ? diag_add : 0.0);
 #pragma unroll 2
     for (int p = 0; p < K; ++p) {
       const double bv = cok ? B[p * ldb + c] : 0.0;
@@ -118,7 +120,8 @@ __device__ void tr_unit(const TrArgs& a, double* sm, int inst, int m, int j, int
   double* Ts = sm + a.off_T;      // k x xm scratch (S_bot before it moves into Ss)
   double* Z1 = sm + a.off_Z;      // level-m rows of Q_c1 / Q_c2 (k x ncol1 each)
   double* Z2 = Z1 + k * ncol1;
-  double* Ub = sm + a.off_U;      // 2 buffers x [Q_c1 rows | Q_c2 rows] (TR_SUB x ncol1 each)
+  double* Ub = sm + a.off_U;      // 2 buffers x [Q_c1 rows | Q_c2 rows] (TR_SUB x ncol1 each);
+                                  // aliases Ts and Z: streamed only after the S phase
   const long long qs1 = (long long)(ncol1 - 1) * ncol1;
   const double* Q1 = a.Q + (long long)inst * a.qinst + a.qlev[m + 1] + (long long)(2 * j) * qs1;
   const double* Q2 = Q1 + qs1;
@@ -146,45 +149,60 @@ __device__ void tr_unit(const TrArgs& a, double* sm, int inst, int m, int j, int
     cp_async8(Z2 + e, Q2 + (long long)r0 * ncol1 + e);
   }
   cp_async_commit();
-  if (nsub > 0) { issue_sub(0); cp_async_wait_group1(); } else cp_async_wait_all();
+  cp_async_wait_all();
   __syncthreads();
   TPH(0);
-  // 2. Sc = I - C B ; T = R_bot - C R_top   (B = Z2[:, m-cols], C = Z1[:, m-cols])
-  for (int e = t; e < k * k; e += TR_THREADS) {
-    const int q = e / k, c = e % k;
-    Bs[q * ldk + c] = Z2[q * ncol1 + xm + c];
-    Cs[q * ldk + c] = Z1[q * ncol1 + xm + c];
-    Ms[q * ldk + c] = (q == c) ? 1.0 : 0.0;
+  // 2. Sc = I - C B ; T = R_bot - C R_top   (B = Z2[:, m-cols], C = Z1[:, m-cols], read in place)
+  const double* Bz = Z2 + xm;
+  const double* Cz = Z1 + xm;
+  tr_mm(Ms, ldk, nullptr, 0, Cz, ncol1, Bz, ncol1, k, k, k, -1.0, 1.0);
+  tr_mm(Ts, lds, Z1, ncol1, Cz, ncol1, Z2, ncol1, k, xm, k, -1.0);
+  __shared__ double rcp_buf[2];
+  if (t == 0) rcp_buf[0] = 0.0;
+  __syncthreads();
+  if (t == 0) {
+    const double p0 = Ms[0];
+    if (!(isfinite(p0) && fabs(p0) > 0.0)) latch_status(a.st, FDE_ESINGULAR, inst * 65536 + 32768 + node_index(m, j));
+    rcp_buf[0] = tr_rcp(p0);
   }
   __syncthreads();
-  tr_mm(Ms, ldk, Ms, ldk, Cs, ldk, Bs, ldk, k, k, k, -1.0);
-  tr_mm(Ts, lds, Z1, ncol1, Cs, ldk, Z2, ncol1, k, xm, k, -1.0);
-  __syncthreads();
   TPH(1);
-  // 3. Sc^{-1}: unpivoted Gauss-Jordan (reading R17), ping-pong Ms <-> M2, one barrier per pivot
-  for (int p = 0; p < k; ++p) {
-    const double* src = (p & 1) ? M2 : Ms;
-    double* dst = (p & 1) ? Ms : M2;
-    const double piv = src[p * ldk + p];
-    if (t == 0 && !(isfinite(piv) && fabs(piv) > 0.0))
-      latch_status(a.st, FDE_ESINGULAR, inst * 65536 + 32768 + node_index(m, j));
-    const double rp = tr_rcp(piv);
-    for (int e = t; e < k * k; e += TR_THREADS) {
-      const int q = e / k, cc = e % k;
-      const double mqp = src[q * ldk + p], mpc = src[p * ldk + cc], mqc = src[q * ldk + cc];
-      double v;
-      if (q == p) v = (cc == p) ? rp : mpc * rp;
-      else v = (cc == p) ? -mqp * rp : fma(-mqp * rp, mpc, mqc);
-      dst[q * ldk + cc] = v;
+  // 3. Sc^{-1}: unpivoted Gauss-Jordan (reading R17), ping-pong Ms <-> M2, one barrier per
+  //    pivot; the thread that updates the next pivot also forms its reciprocal (off the
+  //    critical path of the following step)
+  {
+    const int kk = k * k;
+    const int q0 = t / k, c0 = t % k, e1 = t + TR_THREADS, q1 = e1 / k, c1 = e1 % k;
+    for (int p = 0; p < k; ++p) {
+      const double* src = (p & 1) ? M2 : Ms;
+      double* dst = (p & 1) ? Ms : M2;
+      const double rp = rcp_buf[p & 1];
+      for (int h = 0; h * TR_THREADS < kk; ++h) {      // (q, cc) precomputed for 2 elements
+        const int e = t + h * TR_THREADS;
+        if (e >= kk) break;
+        const int q = h == 0 ? q0 : (h == 1 ? q1 : e / k), cc = h == 0 ? c0 : (h == 1 ? c1 : e % k);
+        const double mqp = src[q * ldk + p], mpc = src[p * ldk + cc], mqc = src[q * ldk + cc];
+        double v;
+        if (q == p) v = (cc == p) ? rp : mpc * rp;
+        else v = (cc == p) ? -mqp * rp : fma(-mqp * rp, mpc, mqc);
+        dst[q * ldk + cc] = v;
+        if (q == p + 1 && cc == p + 1) {
+          if (!(isfinite(v) && fabs(v) > 0.0))
+            latch_status(a.st, FDE_ESINGULAR, inst * 65536 + 32768 + node_index(m, j));
+          rcp_buf[(p + 1) & 1] = tr_rcp(v);
+        }
+      }
+      __syncthreads();
     }
-    __syncthreads();
   }
   TPH(2);
   const double* Mi = (k & 1) ? M2 : Ms;            // where the inverse ended up
-  // 4. S_bot = Sc^{-1} T -> Ss rows k..2k-1 ; S_top = R_top - B S_bot -> Ss rows 0..k-1
-  tr_mm(Ss + k * lds, lds, nullptr, 0, Mi, ldk, Ts, lds, k, xm, k, 1.0);
+  double* Gs = (k & 1) ? Ms : M2;                  // free k x k scratch
+  tr_mm(Gs, ldk, nullptr, 0, Bz, ncol1, Mi, ldk, k, k, k, 1.0);            // G = B Sc^{-1}
   __syncthreads();
-  tr_mm(Ss, lds, Z2, ncol1, Bs, ldk, Ss + k * lds, lds, k, xm, k, -1.0);
+  // 4. S_bot = Sc^{-1} T -> Ss rows k..2k-1 ; S_top = R_top - G T -> Ss rows 0..k-1
+  tr_mm(Ss + k * lds, lds, nullptr, 0, Mi, ldk, Ts, lds, k, xm, k, 1.0);
+  tr_mm(Ss, lds, Z2, ncol1, Gs, ldk, Ts, lds, k, xm, k, -1.0);
   // zero the K padding rows 2k .. round4(2k) and the column padding of S
   const int K4 = round_up(2 * k, 4), xmp = round_up(xm, 16);
   if (xmp > xm)
@@ -200,21 +218,22 @@ __device__ void tr_unit(const TrArgs& a, double* sm, int inst, int m, int j, int
   // 5. Q_mu rows [ra, rb) = Q1 + Q2 - [Q1 m-cols | Q2 m-cols] [S_top; S_bot], streamed in
   //    sub-chunks of TR_SUB rows (the next sub-chunk's copies overlap this one's DMMA)
   double* Qo = a.Q + (long long)inst * a.qinst + a.qlev[m] + (long long)j * (long long)nrow * xm;
+  issue_sub(0);
   for (int sc = 0; sc < nsub; ++sc) {
     if (sc + 1 < nsub) { issue_sub(sc + 1); cp_async_wait_group1(); } else cp_async_wait_all();
     __syncthreads();
     const int rs = ra + sc * TR_SUB, nr = min(TR_SUB, rb - rs);
     const double* U1 = Ub + (sc & 1) * 2 * TR_SUB * ncol1;
     const double* U2 = U1 + TR_SUB * ncol1;
-    // warp -> m-tile (warp & 1) x n-tiles (warp >> 1) + 4 i: A fragment reused TR_NT times
-    const int mt = warp & 1, nt0 = warp >> 1, NT8 = xmp >> 3;
+    // warp -> m-tile (warp & 3) x n-tiles (warp >> 2) + 2 i: A fragment reused TR_NT times
+    const int mt = warp & 3, nt0 = warp >> 2, NT8 = xmp >> 3;
     const int r = 8 * mt + gid;
     const bool rok = r < nr;
     if (8 * mt < nr) {
       double d[TR_NT][2];
 #pragma unroll
       for (int i = 0; i < TR_NT; ++i) {
-        const int c = 8 * (nt0 + 4 * i) + 2 * tig;
+        const int c = 8 * (nt0 + 2 * i) + 2 * tig;
         d[i][0] = (rok && c < xm) ? U1[r * ncol1 + c] + U2[r * ncol1 + c] : 0.0;
         d[i][1] = (rok && c + 1 < xm) ? U1[r * ncol1 + c + 1] + U2[r * ncol1 + c + 1] : 0.0;
       }
@@ -224,13 +243,13 @@ __device__ void tr_unit(const TrArgs& a, double* sm, int inst, int m, int j, int
         const double av = (rok && q < 2 * k) ? -(q < k ? U1[r * ncol1 + xm + q] : U2[r * ncol1 + xm + q - k]) : 0.0;
 #pragma unroll
         for (int i = 0; i < TR_NT; ++i)
-          if (nt0 + 4 * i < NT8) dmma884(d[i][0], d[i][1], av, bp[k0 * lds + 32 * i]);
+          if (nt0 + 2 * i < NT8) dmma884(d[i][0], d[i][1], av, bp[k0 * lds + 16 * i]);
       }
       if (rok) {
         double* qr = Qo + (long long)(rs + r) * xm;
 #pragma unroll
         for (int i = 0; i < TR_NT; ++i) {
-          const int c = 8 * (nt0 + 4 * i) + 2 * tig;
+          const int c = 8 * (nt0 + 2 * i) + 2 * tig;
           if (c < xm) qr[c] = d[i][0];
           if (c + 1 < xm) qr[c + 1] = d[i][1];
         }
