@@ -36,9 +36,28 @@ static int dn_check(const char* what) {
 }
 
 // C (m x n) = alpha A^T B + beta C  (A: K x m, B: K x n; K tall)
+static double* g_dn_part = nullptr;     // split-K partials (device, grown on demand)
+static size_t g_dn_part_cap = 0;
+
 static int ts_tn(cudaStream_t s, int m, int n, int K, double alpha, const double* A, int lda,
                  const double* B, int ldb, double beta, double* C, int ldc) {
   if (m <= 0 || n <= 0) return FDE_OK;
+  const int nz = std::min(32, std::max(1, K / 128));
+  if (nz > 1) {
+    const size_t need = (size_t)nz * m * n;
+    if (need > g_dn_part_cap) {
+      if (g_dn_part) { cudaStreamSynchronize(s); cudaFree(g_dn_part); }
+      CU(cudaMalloc(&g_dn_part, need * sizeof(double)));
+      g_dn_part_cap = need;
+    }
+    const int kchunk = round_up((K + nz - 1) / nz, 64);
+    const int nzz = (K + kchunk - 1) / kchunk;
+    { PROF("k_ts_gemm_tn"); k_ts_gemm_tn_split<<<dim3((m + TS_TILE - 1) / TS_TILE, (n + TS_TILE - 1) / TS_TILE, nzz), DN_THREADS, 0, s>>>(
+        m, n, K, kchunk, A, lda, B, ldb, g_dn_part); }
+    TRY(dn_check("k_ts_gemm_tn_split"));
+    { PROF("k_reduce_partials"); k_reduce_partials<<<(m * n + 255) / 256, 256, 0, s>>>(m, n, nzz, g_dn_part, alpha, beta, C, ldc); }
+    return dn_check("k_reduce_partials");
+  }
   { PROF("k_ts_gemm_tn"); k_ts_gemm_tn<<<dim3((m + TS_TILE - 1) / TS_TILE, (n + TS_TILE - 1) / TS_TILE), DN_THREADS, 0, s>>>(
       m, n, K, alpha, A, lda, B, ldb, beta, C, ldc); }
   return dn_check("k_ts_gemm_tn");
@@ -51,6 +70,26 @@ static int ts_nn(cudaStream_t s, int M, int n, int K, double alpha, const double
   { PROF("k_ts_gemm_nn"); k_ts_gemm_nn<<<dim3((M + DN_THREADS - 1) / DN_THREADS, n), DN_THREADS, 0, s>>>(
       M, n, K, alpha, A, lda, B, ldb, beta, C, ldc); }
   return dn_check("k_ts_gemm_nn");
+}
+
+static int transpose(cudaStream_t s, int m, int n, const double* X, int ldx, double* Y, int ldy) {
+  if (m <= 0 || n <= 0) return FDE_OK;
+  { PROF("k_transpose"); k_transpose<<<dim3((m + 31) / 32, (n + 31) / 32), dim3(32, 8), 0, s>>>(m, n, X, ldx, Y, ldy); }
+  return dn_check("k_transpose");
+}
+
+static bool g_dn_attr = false;
+static int dn_attrs() {
+  if (g_dn_attr) return FDE_OK;
+  CU(cudaFuncSetAttribute(k_sym_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, DN_SMEM_MAX + 8192));
+  CU(cudaFuncSetAttribute(k_osj_svd, cudaFuncAttributeMaxDynamicSharedMemorySize, DN_SMEM_MAX + 8192));
+  CU(cudaFuncSetAttribute(k_gj_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, DN_SMEM_MAX + 8192));
+  g_dn_attr = true;
+  return FDE_OK;
+}
+static size_t dn_smem(long long resident_doubles, int ints) {
+  const long long b = resident_doubles * 8 + ints * 4;
+  return (size_t)(b <= DN_SMEM_MAX ? b + 16 : ints * 4 + 16);
 }
 
 static int scale_copy(cudaStream_t s, int m, int n, double alpha, const double* X, int ldx, double* Y, int ldy) {
@@ -162,7 +201,7 @@ static int orth_append(cudaStream_t s, const DenseWs& w, int n, double* W, int b
       TRY(ts_nn(s, n, cur, sb, -1.0, Ub, n, w.M1, sb, 1.0, src, n));      // W -= U H
     }
     TRY(ts_tn(s, cur, cur, n, 1.0, src, n, src, n, 0.0, w.G, cur));
-    { PROF("k_sym_jacobi"); k_sym_jacobi<<<1, DN_BIG, (cur + 2) * sizeof(int), s>>>(cur, w.G, cur, w.V, w.lam, 60); }
+    { PROF("k_sym_jacobi"); k_sym_jacobi<<<1, DN_BIG, dn_smem(2LL * cur * cur, cur + 2), s>>>(cur, w.G, cur, w.V, w.lam, 60); }
     TRY(dn_check("k_sym_jacobi"));
     CU(cudaMemcpyAsync(h.data(), w.lam, cur * sizeof(double), cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
@@ -204,7 +243,7 @@ static int proj_sylvester(cudaStream_t s, const DenseWs& w, int sa, int sb, doub
   for (; it < 60; ++it) {
     CU(cudaMemcpyAsync(Ai, A, (size_t)sa * sa * sizeof(double), cudaMemcpyDeviceToDevice, s));
     CU(cudaMemcpyAsync(Bi, B, (size_t)sb * sb * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    { PROF("k_gj_inverse"); k_gj_inverse<<<2, DN_BIG, std::max(sa, sb) * sizeof(int), s>>>(w.jobs, st); }
+    { PROF("k_gj_inverse"); k_gj_inverse<<<2, DN_BIG, std::max(dn_smem((long long)sa * sa, sa), dn_smem((long long)sb * sb, sb)), s>>>(w.jobs, st); }
     TRY(dn_check("k_gj_inverse"));
     // T2 = Ai C Bi
     TRY(ts_nn(s, sa, sb, sa, 1.0, Ai, sa, C, sa, 0.0, T, sa));
@@ -301,6 +340,7 @@ extern "C" int fde2d_step(int nx, int ny, double alpha1, double alpha2, double h
   if (!(ek_tol > 0.0 && ek_tol < 1.0) || ek_maxit < 1) return set_err(FDE_EDOMAIN, "ek_tol / ek_maxit out of range");
   if (rf + ru > NRHS_MAX) return set_err(FDE_EDIM, "rf + ru = %d exceeds %d", rf + ru, NRHS_MAX);
   cudaStream_t s = (cudaStream_t)stream;
+  TRY(dn_attrs());
   // operators (built and factorised once, reused while the arguments match)
   fde_hodlr* tmp[2] = {nullptr, nullptr};
   fde_hodlr** ops = cache ? reinterpret_cast<fde_hodlr**>(cache) : tmp;
@@ -380,16 +420,11 @@ extern "C" int fde2d_step(int nx, int ny, double alpha1, double alpha2, double h
     double* LcT = w.M3;
     double* RcT = w.M4;
     // transpose via k_scale_copy row/col swap: write element (q, i) of LcT = Lc(i, q)
-    for (int q = 0; q < r0; ++q) {
-      // column q of Lc (bl entries, contiguous) becomes row q of LcT (stride r0)
-      CU(cudaMemcpy2DAsync(LcT + q, r0 * sizeof(double), Lc + (size_t)q * EK_SMAX, sizeof(double),
-                           sizeof(double), bl, cudaMemcpyDeviceToDevice, s));
-      CU(cudaMemcpy2DAsync(RcT + q, r0 * sizeof(double), Rc + (size_t)q * EK_SMAX, sizeof(double),
-                           sizeof(double), br, cudaMemcpyDeviceToDevice, s));
-    }
+    if ((rc = transpose(s, bl, r0, Lc, EK_SMAX, LcT, r0)) != FDE_OK) return fail(rc);
+    if ((rc = transpose(s, br, r0, Rc, EK_SMAX, RcT, r0)) != FDE_OK) return fail(rc);
     if ((rc = ts_tn(s, bl, br, r0, 1.0, LcT, r0, RcT, r0, 0.0, Ym, bl)) != FDE_OK) return fail(rc);
   }
-  { PROF("k_osj_svd"); k_osj_svd<<<1, DN_BIG, (br + 2) * sizeof(int), s>>>(bl, br, Ym, bl, Zm, sig, 60); }
+  { PROF("k_osj_svd"); k_osj_svd<<<1, DN_BIG, dn_smem((long long)bl * br, br + 2), s>>>(bl, br, Ym, bl, Zm, sig, 60); }
   if ((rc = dn_check("k_osj_svd")) != FDE_OK) return fail(rc);
   CU(cudaMemcpyAsync(hs.data(), sig, br * sizeof(double), cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
@@ -463,9 +498,7 @@ extern "C" int fde2d_step(int nx, int ny, double alpha1, double alpha2, double h
     CU(cudaMemcpyAsync(Wt, AVy, (size_t)ny * sbb * 8, cudaMemcpyDeviceToDevice, s));
     if ((rc = ts_nn(s, ny, sbb, sbb, -1.0, Vy, ny, Rc, sbb, 1.0, Wt, ny)) != FDE_OK) return fail(rc);
     // Y^T (sbb x sa) for Rb Y^T: transpose Y into Zm
-    for (int q = 0; q < sbb; ++q)
-      CU(cudaMemcpy2DAsync(Zm + q, sbb * sizeof(double), Ym + (size_t)q * sa, sizeof(double), sizeof(double), sa,
-                           cudaMemcpyDeviceToDevice, s));
+    if ((rc = transpose(s, sa, sbb, Ym, sa, Zm, sbb)) != FDE_OK) return fail(rc);
     if ((rc = ts_nn(s, ny, sa, sbb, 1.0, Wt, ny, Zm, sbb, 0.0, w.M2, ny)) != FDE_OK) return fail(rc);
     if ((rc = sumsq(s, ny, sa, w.M2, ny, w.dv + 8, &rb2)) != FDE_OK) return fail(rc);
     rel = std::sqrt((ra2 + rb2) / cnorm2);
@@ -487,7 +520,7 @@ extern "C" int fde2d_step(int nx, int ny, double alpha1, double alpha2, double h
   if (iters_out) *iters_out = std::min(it, ek_maxit);
   // ---- truncation: Y Z = W Sigma (one-sided Jacobi), X = (U W Sigma)(V Z)^T, keep sigma > tol sigma_1
   const int sa = sx.s, sbb = sy.s;
-  { PROF("k_osj_svd"); k_osj_svd<<<1, DN_BIG, (sbb + 2) * sizeof(int), s>>>(sa, sbb, Ym, sa, Zm, sig, 60); }
+  { PROF("k_osj_svd"); k_osj_svd<<<1, DN_BIG, dn_smem((long long)sa * sbb, sbb + 2), s>>>(sa, sbb, Ym, sa, Zm, sig, 60); }
   if ((rc = dn_check("k_osj_svd")) != FDE_OK) return fail(rc);
   CU(cudaMemcpyAsync(hs.data(), sig, sbb * sizeof(double), cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));

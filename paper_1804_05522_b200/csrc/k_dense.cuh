@@ -11,6 +11,7 @@
 #define DN_THREADS 256
 #define DN_BIG 1024                    // threads of the single-CTA kernels
 #define TS_TILE 16
+#define DN_SMEM_MAX (200 * 1024)       // dynamic shared memory of the single-CTA kernels
 
 // C (m x n) = alpha * A^T B + beta * C;  A: K x m (lda), B: K x n (ldb); K is the tall dim.
 // One CTA per 16 x 16 tile of C; the K loop is staged through shared memory.
@@ -35,6 +36,56 @@ k_ts_gemm_tn(int m, int n, int K, double alpha, const double* __restrict__ A, in
   if (i0 + ti < m && j0 + tj < n) {
     double* c = C + (long long)(j0 + tj) * ldc + i0 + ti;
     *c = alpha * acc + (beta == 0.0 ? 0.0 : beta * *c);
+  }
+}
+
+// Split-K variant: partial tile sums of the K chunk blockIdx.z go to P[z][n][m] (column-major
+// m x n per chunk); k_reduce_partials adds the chunks in a fixed order.
+__global__ void __launch_bounds__(DN_THREADS)
+k_ts_gemm_tn_split(int m, int n, int K, int kchunk, const double* __restrict__ A, int lda,
+                   const double* __restrict__ B, int ldb, double* __restrict__ P) {
+  __shared__ double As[64][TS_TILE + 1], Bs[64][TS_TILE + 1];
+  const int i0 = blockIdx.x * TS_TILE, j0 = blockIdx.y * TS_TILE;
+  const int kb = blockIdx.z * kchunk, ke = min(K, kb + kchunk);
+  const int t = threadIdx.x, ti = t % TS_TILE, tj = t / TS_TILE;
+  double acc = 0.0;
+  for (int k0 = kb; k0 < ke; k0 += 64) {
+    for (int e = t; e < 64 * TS_TILE; e += DN_THREADS) {
+      const int kk = e % 64, c = e / 64;
+      As[kk][c] = (k0 + kk < ke && i0 + c < m) ? A[(long long)(i0 + c) * lda + k0 + kk] : 0.0;
+      Bs[kk][c] = (k0 + kk < ke && j0 + c < n) ? B[(long long)(j0 + c) * ldb + k0 + kk] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < 64; ++kk) acc = fma(As[kk][ti], Bs[kk][tj], acc);
+    __syncthreads();
+  }
+  if (i0 + ti < m && j0 + tj < n) P[(long long)blockIdx.z * m * n + (long long)(j0 + tj) * m + i0 + ti] = acc;
+}
+
+__global__ void k_reduce_partials(int m, int n, int nz, const double* __restrict__ P, double alpha, double beta,
+                                  double* __restrict__ C, int ldc) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (long long)m * n) return;
+  double s = 0.0;
+  for (int z = 0; z < nz; ++z) s += P[(long long)z * m * n + e];
+  const int i = (int)(e % m), j = (int)(e / m);
+  double* c = C + (long long)j * ldc + i;
+  *c = alpha * s + (beta == 0.0 ? 0.0 : beta * *c);
+}
+
+// Y (n x m, ld ldy) = X^T (X: m x n, ld ldx)
+__global__ void k_transpose(int m, int n, const double* __restrict__ X, int ldx, double* __restrict__ Y, int ldy) {
+  __shared__ double tile[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;          // bx over rows of X, by over cols
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int i = bx + threadIdx.x, j = by + r;
+    if (i < m && j < n) tile[r][threadIdx.x] = X[(long long)j * ldx + i];
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int j = by + threadIdx.x, i = bx + r;                 // Y[j][i] column i of Y^T... Y(j, i)
+    if (i < m && j < n) Y[(long long)i * ldy + j] = tile[threadIdx.x][r];
   }
 }
 
@@ -83,9 +134,18 @@ k_sumsq(int m, int n, const double* __restrict__ X, int ldx, double* __restrict_
 // lam[i] = eigenvalues (unsorted), V (b x b, ld b) the eigenvectors.  Round-robin ordering:
 // b/2 disjoint rotations per round run in parallel (one warp each), b-1 rounds per sweep.
 __global__ void __launch_bounds__(DN_BIG)
-k_sym_jacobi(int b, double* __restrict__ G, int ldg, double* __restrict__ V, double* __restrict__ lam,
+k_sym_jacobi(int b, double* __restrict__ Gg, int ldgg, double* __restrict__ Vg, double* __restrict__ lam,
              int max_sweeps) {
-  extern __shared__ int sh_pairs[];                  // [b+1] round-robin tournament
+  extern __shared__ double sh_dn[];                  // [G | V | pairs] when resident, else [pairs]
+  const bool res = 2LL * b * b * 8 + (b + 2) * 4 <= DN_SMEM_MAX;
+  double* G = res ? sh_dn : Gg;
+  double* V = res ? sh_dn + b * b : Vg;
+  const int ldg = res ? b : ldgg;
+  int* sh_pairs = reinterpret_cast<int*>(res ? sh_dn + 2 * b * b : sh_dn);
+  if (res) {
+    for (int e = threadIdx.x; e < b * b; e += DN_BIG) G[e] = Gg[(long long)(e / b) * ldgg + e % b];
+    __syncthreads();
+  }
   __shared__ double cs[512], sn[512];
   __shared__ int done;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31, nw = DN_BIG / 32;
@@ -106,7 +166,7 @@ k_sym_jacobi(int b, double* __restrict__ G, int ldg, double* __restrict__ V, dou
         double c = 1.0, s = 0.0;
         if (q < b) {
           const double apq = G[(long long)q * ldg + p], app = G[(long long)p * ldg + p], aqq = G[(long long)q * ldg + q];
-          if (fabs(apq) > 1e-300 && fabs(apq) > 1e-16 * sqrt(fabs(app * aqq))) {
+          if (fabs(apq) > 1e-300 && fabs(apq) > 4e-15 * sqrt(fabs(app * aqq))) {
             const double tau = (aqq - app) / (2.0 * apq);
             const double tt = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
             c = 1.0 / sqrt(1.0 + tt * tt);
@@ -157,15 +217,27 @@ k_sym_jacobi(int b, double* __restrict__ G, int ldg, double* __restrict__ V, dou
     (void)off0;
   }
   for (int i = t; i < b; i += DN_BIG) lam[i] = G[(long long)i * ldg + i];
+  if (res) {
+    __syncthreads();
+    for (int e = t; e < b * b; e += DN_BIG) { Vg[e] = V[e]; Gg[(long long)(e / b) * ldgg + e % b] = G[e]; }
+  }
 }
 
 // ---------------------------------------------------------------------------------------
 // One-sided Jacobi SVD of Y (m x n, ld ldy; overwritten by W Sigma): on exit the columns of Y
 // are mutually orthogonal (Y_out = Y_in Z), Z (n x n) orthogonal, sig[j] = ||Y_out[:, j]||.
 __global__ void __launch_bounds__(DN_BIG)
-k_osj_svd(int m, int n, double* __restrict__ Y, int ldy, double* __restrict__ Z, double* __restrict__ sig,
+k_osj_svd(int m, int n, double* __restrict__ Yg, int ldyg, double* __restrict__ Z, double* __restrict__ sig,
           int max_sweeps) {
-  extern __shared__ int sh_pairs[];
+  extern __shared__ double sh_dn[];                  // [Y | pairs] when resident, else [pairs]
+  const bool res = (long long)m * n * 8 + (n + 2) * 4 <= DN_SMEM_MAX;
+  double* Y = res ? sh_dn : Yg;
+  const int ldy = res ? m : ldyg;
+  int* sh_pairs = reinterpret_cast<int*>(res ? sh_dn + (long long)m * n : sh_dn);
+  if (res) {
+    for (long long e = threadIdx.x; e < (long long)m * n; e += DN_BIG) Y[e] = Yg[(e / m) * ldyg + e % m];
+    __syncthreads();
+  }
   __shared__ double cs[512], sn[512];
   __shared__ int done;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31, nw = DN_BIG / 32;
@@ -194,7 +266,7 @@ k_osj_svd(int m, int n, double* __restrict__ Y, int ldy, double* __restrict__ Z,
             be += __shfl_xor_sync(0xffffffffu, be, o);
             ga += __shfl_xor_sync(0xffffffffu, ga, o);
           }
-          if (fabs(ga) > 1e-15 * sqrt(al * be) && fabs(ga) > 1e-300) {
+          if (fabs(ga) > 4e-15 * sqrt(al * be) && fabs(ga) > 1e-300) {
             const double zeta = (be - al) / (2.0 * ga);
             const double tt = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
             c = 1.0 / sqrt(1.0 + tt * tt);
@@ -231,6 +303,10 @@ k_osj_svd(int m, int n, double* __restrict__ Y, int ldy, double* __restrict__ Z,
     for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
     if (lane == 0) sig[j] = sqrt(s2);
   }
+  if (res) {
+    __syncthreads();
+    for (long long e = t; e < (long long)m * n; e += DN_BIG) Yg[(e / m) * ldyg + e % m] = Y[e];
+  }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -241,14 +317,21 @@ struct InvJob { double* A; int s; int lda; };
 
 __global__ void __launch_bounds__(DN_BIG)
 k_gj_inverse(const InvJob* __restrict__ jobs, DevStatus* st) {
-  extern __shared__ int sh_piv[];                    // [s] row permutation
+  extern __shared__ double sh_dn[];                  // [A | piv] when resident, else [piv]
   __shared__ double colk[1024], rowk[1024];
   __shared__ double red_v[DN_BIG / 32];
   __shared__ int red_i[DN_BIG / 32];
   __shared__ int prow;
   const InvJob jb = jobs[blockIdx.x];
-  double* A = jb.A;
-  const int s = jb.s, lda = jb.lda, t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int s = jb.s, t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const bool res = (long long)s * s * 8 + s * 4 <= DN_SMEM_MAX;
+  double* A = res ? sh_dn : jb.A;
+  const int lda = res ? s : jb.lda;
+  int* sh_piv = reinterpret_cast<int*>(res ? sh_dn + (long long)s * s : sh_dn);
+  if (res) {
+    for (int e = t; e < s * s; e += DN_BIG) A[e] = jb.A[(long long)(e / s) * jb.lda + e % s];
+    __syncthreads();
+  }
 
   for (int k = 0; k < s; ++k) {
     // pivot search in column k, rows k..s-1 (fixed-order argmax: largest |a|, smallest index)
@@ -265,12 +348,19 @@ k_gj_inverse(const InvJob* __restrict__ jobs, DevStatus* st) {
     }
     if (lane == 0) { red_v[warp] = bv; red_i[warp] = bi; }
     __syncthreads();
-    if (t == 0) {
-      double v = -1.0; int ii = s;
-      for (int w = 0; w < DN_BIG / 32; ++w)
-        if (red_v[w] > v || (red_v[w] == v && red_i[w] < ii)) { v = red_v[w]; ii = red_i[w]; }
-      prow = ii;
-      if (!(v > 0.0) || !isfinite(v)) latch_status(st, FDE_ESINGULAR, k);
+    if (warp == 0) {                                 // fixed-order warp reduction of the partials
+      double v = red_v[lane];
+      int ii = red_i[lane];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, ii, o);
+        if (ov > v || (ov == v && oi < ii)) { v = ov; ii = oi; }
+      }
+      if (lane == 0) {
+        prow = ii;
+        if (!(v > 0.0) || !isfinite(v)) latch_status(st, FDE_ESINGULAR, k);
+      }
     }
     __syncthreads();
     const int p = prow;
@@ -311,4 +401,6 @@ k_gj_inverse(const InvJob* __restrict__ jobs, DevStatus* st) {
       }
     __syncthreads();
   }
+  if (res)
+    for (int e = t; e < s * s; e += DN_BIG) jb.A[(long long)(e / s) * jb.lda + e % s] = A[e];
 }
