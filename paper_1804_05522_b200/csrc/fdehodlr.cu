@@ -18,6 +18,7 @@
 #include "k_matvec.cuh"
 #include "k_tree.cuh"
 #include "k_solve.cuh"
+#include "k_step.cuh"
 
 // ---------------------------------------------------------------------------------------
 // errors, launch accounting
@@ -133,6 +134,10 @@ struct fde_hodlr {
   int tr_grid = 0;
   TrArgs tr_geo{};
   size_t tr_smem = 0;
+  int* d_done = nullptr;            // k_step task counter + completion counters
+  long long dofs[LMAX + 1] = {}, ndone = 0;
+  int step_grid = 0;
+  size_t step_smem = 0;
   int npost = 0;
   // compression scratch
   PcTask* d_tasks = nullptr;
@@ -515,6 +520,17 @@ static int tree_layout(fde_hodlr* H) {
   H->tr_smem = bytes;
   TRY(dalloc(H, &H->d_Q, (size_t)B * H->qinst));
   TRY(dalloc(H, &H->d_S, (size_t)B * H->sinst));
+  // persistent dataflow kernel (k_step.cuh): counters and launch geometry
+  long long dn = 1;                                   // [0] = task counter
+  for (int m = 0; m < L; ++m) { H->dofs[m] = dn; dn += (long long)B << m; }
+  H->dofs[L] = dn; dn += (long long)B << (L - 1);
+  H->ndone = dn;
+  TRY(dalloc(H, &H->d_done, (size_t)dn));
+  H->step_smem = std::max((size_t)LEAF_SMEM, bytes);
+  CU(cudaFuncSetAttribute(k_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)H->step_smem));
+  int per_sm2 = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_step, TR_THREADS, H->step_smem));
+  H->step_grid = nsm * std::max(1, per_sm2);
   H->tree_ok = true;
   return FDE_OK;
 }
@@ -802,6 +818,30 @@ static int factor_impl(fde_hodlr* H, const double* dp, const double* dm, int nf,
   if (tree) {
     la.Q = H->d_Q + H->qlev[L]; la.qinst = H->qinst;
     la.qstride = (long long)(H->xcol[L] - 1) * H->xcol[L];
+  }
+  if (tree && !getenv("FDE_SPLIT_KERNELS")) {
+    // one persistent dataflow launch: leaves -> tree levels -> u = X v (k_step.cuh)
+    StepArgs sa{};
+    sa.la = la;
+    TrArgs& a = sa.ta;
+    a = H->tr_geo;
+    a.L = L; a.NC = H->xcol[L]; a.nleaf = H->nleaf; a.batch = H->batch; a.kmaxc = H->kmax;
+    for (int l = 0; l <= L; ++l) a.xc[l] = H->xcol[l];
+    for (int m = 0; m < L; ++m) { a.rc[m] = H->trc[m]; a.slev[m] = H->slev[m]; }
+    for (int m = 1; m <= L; ++m) a.qlev[m] = H->qlev[m];
+    a.qinst = H->qinst; a.sinst = H->sinst;
+    a.Qleaf = H->d_Q + H->qlev[L]; a.Q = H->d_Q; a.Sst = H->d_S;
+    a.X = H->d_X; a.xstride = H->xstride; a.n = H->n;
+    a.leaf_r0 = H->tree.leaf_r0; a.leaf_n = H->tree.leaf_n;
+    a.u = u_next; a.bar = H->d_bar; a.st = H->d_status; a.trace = nullptr;
+    sa.ctr = reinterpret_cast<unsigned*>(H->d_done);
+    sa.done = H->d_done;
+    for (int l = 0; l <= L; ++l) sa.dofs[l] = H->dofs[l];
+    CU(cudaMemsetAsync(H->d_done, 0, H->ndone * sizeof(int), s));
+    void* args[] = {&sa};
+    { PROF("k_step"); CU(cudaLaunchCooperativeKernel((void*)k_step, dim3(H->step_grid), dim3(TR_THREADS), args, H->step_smem, s)); }
+    LAUNCHED();
+    return FDE_OK;
   }
   { PROF("k_leaf"); k_leaf<<<dim3(H->nleaf, B), LEAF_THREADS, LEAF_SMEM, s>>>(la); }
   LAUNCHED();

@@ -427,9 +427,7 @@ __device__ void leaf_project(const LeafArgs& a, double* big, const PanelCol* pcd
   }
 }
 
-__global__ void __launch_bounds__(LEAF_THREADS, 1)
-k_leaf(const LeafArgs a) {
-  extern __shared__ double smem[];
+__device__ __forceinline__ void leaf_task(const LeafArgs& a, double* smem, int leaf, int inst) {
   double* S = smem;                               // 32 x 33 scratch (g staging, Gauss-Jordan)
   double* dps = S + 32 * 33;                      // d+ / d- of the leaf rows
   double* dms = dps + LEAF_MAX;
@@ -437,7 +435,7 @@ k_leaf(const LeafArgs a) {
   PanelCol* pcd = reinterpret_cast<PanelCol*>(bs + LEAF_MAX);   // panel column descriptors
   double* A = smem + LEAF_FRONT;                  // [LEAF_MAX cols][LDA_LEAF]
   const TreeDev& tr = a.tree;
-  const int leaf = blockIdx.x, inst = blockIdx.y, t = threadIdx.x, warp = t >> 5;
+  const int t = threadIdx.x, warp = t >> 5;
   const int lane = t & 31, gid = lane >> 2, tig = lane & 3;
   double* Ys = A + LEAF_MAX * LDA_LEAF + warp * 8 * YLD;   // warp-private 128 x 8 stripe buffer
   const int n = tr.n;
@@ -636,4 +634,10 @@ k_leaf(const LeafArgs a) {
       }
     }
   }
+}
+
+__global__ void __launch_bounds__(LEAF_THREADS, 1)
+k_leaf(const LeafArgs a) {
+  extern __shared__ double smem[];
+  leaf_task(a, smem, blockIdx.x, blockIdx.y);
 }

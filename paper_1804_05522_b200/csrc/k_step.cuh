@@ -1,0 +1,92 @@
+// k_step.cuh -- the whole fused factor + solve step (S3-S6, tree path) as ONE persistent
+// dataflow kernel: leaf tasks (k_leaf.cuh leaf_task), then the SMW tree units of every level
+// (k_tree.cuh tr_unit), then the final u = X v groups (tr_final), claimed in that
+// topological order from a single atomic counter.  A unit waits only for its own inputs
+// (completion counters of its two children, release/acquire at gpu scope) instead of a grid
+// barrier per level, so the tree's bottom levels fill the SMs left idle by the last wave of
+// leaves, and no level waits for unrelated nodes.  Every claimed task only depends on tasks
+// with smaller indices, all claimed by co-resident CTAs (cooperative launch): progress is
+// guaranteed.  The arithmetic is exactly that of k_leaf + k_tree (same functions).
+#pragma once
+#include "k_leaf.cuh"
+#include "k_tree.cuh"
+
+struct StepArgs {
+  LeafArgs la;
+  TrArgs ta;
+  unsigned* ctr;                 // task counter (zeroed before the launch)
+  int* done;                     // completion counters (zeroed before the launch)
+  long long dofs[LMAX + 1];      // per level m (0..L-1): offset of [inst][node] counters;
+                                 // dofs[L]: [inst][level L-1 node] count of finished leaves
+};
+
+__device__ __forceinline__ int st_ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_wait(const int* p, int target) {
+  if (threadIdx.x == 0)
+    while (st_ld_acquire(p) < target) __nanosleep(64);
+  __syncthreads();
+}
+
+__device__ __forceinline__ void st_signal(int* p) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(p, 1);
+  }
+}
+
+__global__ void __launch_bounds__(TR_THREADS, 1)
+k_step(const StepArgs sa) {
+  extern __shared__ double smem[];
+  __shared__ int task;
+  const TrArgs& a = sa.ta;
+  const int B = a.batch, L = a.L, nleaf = a.nleaf;
+  const long long n_leaf = (long long)B * nleaf;
+  long long n_lvl[LMAX];
+  long long total = n_leaf;
+  for (int m = L - 1; m >= 0; --m) { n_lvl[m] = (long long)B * (1LL << m) * a.rc[m]; total += n_lvl[m]; }
+  const long long n_fin = (n_leaf + TR_NL - 1) / TR_NL;
+  total += n_fin;
+  while (true) {
+    __syncthreads();                               // (task of the previous iteration consumed)
+    if (threadIdx.x == 0) task = (int)atomicAdd(sa.ctr, 1u);
+    __syncthreads();
+    long long tk = task;
+    if (tk >= total) break;
+    if (tk < n_leaf) {                             // ---- leaf: LU, panel, projection
+      const int inst = (int)(tk / nleaf), leaf = (int)(tk % nleaf);
+      leaf_task(sa.la, smem, leaf, inst);
+      st_signal(sa.done + sa.dofs[L] + (long long)inst * (1 << (L - 1)) + (leaf >> 1));
+      continue;
+    }
+    tk -= n_leaf;
+    int m = L - 1;
+    while (m >= 0 && tk >= n_lvl[m]) { tk -= n_lvl[m]; --m; }
+    if (m >= 0) {                                  // ---- SMW unit of level m
+      const long long per_inst = (1LL << m) * a.rc[m];
+      const int inst = (int)(tk / per_inst), w = (int)(tk % per_inst);
+      const int j = w / a.rc[m], chunk = w % a.rc[m];
+      if (m == L - 1) {
+        st_wait(sa.done + sa.dofs[L] + (long long)inst * (1 << (L - 1)) + j, 2);
+      } else {
+        const int* c = sa.done + sa.dofs[m + 1] + (long long)inst * (1 << (m + 1)) + 2 * j;
+        st_wait(c, a.rc[m + 1]);
+        st_wait(c + 1, a.rc[m + 1]);
+      }
+      tr_unit(a, smem, inst, m, j, chunk);
+      st_signal(sa.done + sa.dofs[m] + (long long)inst * (1 << m) + j);
+      continue;
+    }
+    // ---- final group: u = X v for TR_NL leaves (needs every ancestor's S: the root's done)
+    const long long lu0 = tk * TR_NL;
+    const int nl = (int)min((long long)TR_NL, n_leaf - lu0);
+    const int i0 = (int)(lu0 / nleaf), i1 = (int)((lu0 + nl - 1) / nleaf);
+    for (int inst = i0; inst <= i1; ++inst) st_wait(sa.done + sa.dofs[0] + inst, a.rc[0]);
+    tr_final(a, smem, (int)lu0, nl);
+  }
+}

@@ -97,6 +97,50 @@ __device__ __forceinline__ void tr_mm(double* O, int ldo, const double* Cin, int
   }
 }
 
+
+// O[q][c] = Cin[q][c] (+ diag_add on q == c) + sgn * sum_p A[q][p] B[p][c] on the FP64 tensor
+// cores (DMMA m8n8k4): row-major shared-memory operands, out-of-range rows / columns / K
+// entries read as zero (bounds-checked fragments).  Warp item = one m-tile x up to 4 n-tiles
+// (A fragment reused); items over all warps of the CTA.  No barrier inside.
+__device__ __forceinline__ void tr_dmma(double* O, int ldo, const double* Cin, int ldci, const double* A,
+                                        int lda, const double* B, int ldb, int M, int N, int K, double sgn,
+                                        double diag_add = 0.0) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gid = lane >> 2, tig = lane & 3;
+  const int MT = (M + 7) >> 3, NT = (N + 7) >> 3, NG = (NT + 3) >> 2;
+  for (int it = warp; it < MT * NG; it += TR_WARPS) {
+    const int mt = it % MT, ng = it / MT;
+    const int q = 8 * mt + gid;
+    double d[4][2];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = 8 * (4 * ng + u) + 2 * tig;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const bool in = q < M && c + h < N;
+        d[u][h] = in ? ((Cin ? Cin[q * ldci + c + h] : 0.0) + (q == c + h ? diag_add : 0.0)) : 0.0;
+      }
+    }
+    for (int k0 = 0; k0 < K; k0 += 4) {
+      const int p = k0 + tig;
+      const double av = (q < M && p < K) ? sgn * A[q * lda + p] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int n = 8 * (4 * ng + u) + gid;
+        const double bv = (p < K && n < N) ? B[p * ldb + n] : 0.0;
+        dmma884(d[u][0], d[u][1], av, bv);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = 8 * (4 * ng + u) + 2 * tig;
+      if (q < M) {
+        if (c < N) O[q * ldo + c] = d[u][0];
+        if (c + 1 < N) O[q * ldo + c + 1] = d[u][1];
+      }
+    }
+  }
+}
+
 __device__ __forceinline__ double tr_rcp(double x) {
   double y;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
@@ -155,8 +199,8 @@ __device__ void tr_unit(const TrArgs& a, double* sm, int inst, int m, int j, int
   // 2. Sc = I - C B ; T = R_bot - C R_top   (B = Z2[:, m-cols], C = Z1[:, m-cols], read in place)
   const double* Bz = Z2 + xm;
   const double* Cz = Z1 + xm;
-  tr_mm(Ms, ldk, nullptr, 0, Cz, ncol1, Bz, ncol1, k, k, k, -1.0, 1.0);
-  tr_mm(Ts, lds, Z1, ncol1, Cz, ncol1, Z2, ncol1, k, xm, k, -1.0);
+  tr_dmma(Ms, ldk, nullptr, 0, Cz, ncol1, Bz, ncol1, k, k, k, -1.0, 1.0);
+  tr_dmma(Ts, lds, Z1, ncol1, Cz, ncol1, Z2, ncol1, k, xm, k, -1.0);
   __shared__ double rcp_buf[2];
   if (t == 0) rcp_buf[0] = 0.0;
   __syncthreads();
@@ -171,25 +215,52 @@ __device__ void tr_unit(const TrArgs& a, double* sm, int inst, int m, int j, int
   //    pivot; the thread that updates the next pivot also forms its reciprocal (off the
   //    critical path of the following step)
   {
+    // fast path (k*k <= 2 * TR_THREADS): each thread owns at most two fixed elements, all
+    // addresses hoisted out of the pivot loop; per pivot: 3 loads, 2 flops, 1 store, 1 barrier
     const int kk = k * k;
-    const int q0 = t / k, c0 = t % k, e1 = t + TR_THREADS, q1 = e1 / k, c1 = e1 % k;
+    const bool fast = kk <= 2 * TR_THREADS;
+    const int e0 = t, e1 = t + TR_THREADS;
+    const int q0 = e0 / k, c0 = e0 - q0 * k, q1 = e1 / k, c1 = e1 - q1 * k;
+    const bool h0 = e0 < kk, h1 = e1 < kk;
+    const int oq0 = q0 * ldk, oq1 = q1 * ldk;
     for (int p = 0; p < k; ++p) {
       const double* src = (p & 1) ? M2 : Ms;
       double* dst = (p & 1) ? Ms : M2;
       const double rp = rcp_buf[p & 1];
-      for (int h = 0; h * TR_THREADS < kk; ++h) {      // (q, cc) precomputed for 2 elements
-        const int e = t + h * TR_THREADS;
-        if (e >= kk) break;
-        const int q = h == 0 ? q0 : (h == 1 ? q1 : e / k), cc = h == 0 ? c0 : (h == 1 ? c1 : e % k);
-        const double mqp = src[q * ldk + p], mpc = src[p * ldk + cc], mqc = src[q * ldk + cc];
-        double v;
-        if (q == p) v = (cc == p) ? rp : mpc * rp;
-        else v = (cc == p) ? -mqp * rp : fma(-mqp * rp, mpc, mqc);
-        dst[q * ldk + cc] = v;
-        if (q == p + 1 && cc == p + 1) {
-          if (!(isfinite(v) && fabs(v) > 0.0))
-            latch_status(a.st, FDE_ESINGULAR, inst * 65536 + 32768 + node_index(m, j));
-          rcp_buf[(p + 1) & 1] = tr_rcp(v);
+      const int op = p * ldk;
+      if (fast) {
+        double v0 = 0.0, v1 = 0.0;
+        if (h0) {
+          const double mqp = src[oq0 + p], mpc = src[op + c0], mqc = src[oq0 + c0];
+          const double fq = -mqp * rp;
+          v0 = (q0 == p) ? ((c0 == p) ? rp : mpc * rp) : ((c0 == p) ? fq : fma(fq, mpc, mqc));
+        }
+        if (h1) {
+          const double mqp = src[oq1 + p], mpc = src[op + c1], mqc = src[oq1 + c1];
+          const double fq = -mqp * rp;
+          v1 = (q1 == p) ? ((c1 == p) ? rp : mpc * rp) : ((c1 == p) ? fq : fma(fq, mpc, mqc));
+        }
+        if (h0) dst[oq0 + c0] = v0;
+        if (h1) dst[oq1 + c1] = v1;
+        if (h0 && q0 == p + 1 && c0 == p + 1) {
+          if (!(isfinite(v0) && fabs(v0) > 0.0)) latch_status(a.st, FDE_ESINGULAR, inst * 65536 + 32768 + node_index(m, j));
+          rcp_buf[(p + 1) & 1] = tr_rcp(v0);
+        }
+        if (h1 && q1 == p + 1 && c1 == p + 1) {
+          if (!(isfinite(v1) && fabs(v1) > 0.0)) latch_status(a.st, FDE_ESINGULAR, inst * 65536 + 32768 + node_index(m, j));
+          rcp_buf[(p + 1) & 1] = tr_rcp(v1);
+        }
+      } else {
+        for (int e = t; e < kk; e += TR_THREADS) {
+          const int q = e / k, cc = e - q * k;
+          const double mqp = src[q * ldk + p], mpc = src[op + cc], mqc = src[q * ldk + cc];
+          const double fq = -mqp * rp;
+          const double v = (q == p) ? ((cc == p) ? rp : mpc * rp) : ((cc == p) ? fq : fma(fq, mpc, mqc));
+          dst[q * ldk + cc] = v;
+          if (q == p + 1 && cc == p + 1) {
+            if (!(isfinite(v) && fabs(v) > 0.0)) latch_status(a.st, FDE_ESINGULAR, inst * 65536 + 32768 + node_index(m, j));
+            rcp_buf[(p + 1) & 1] = tr_rcp(v);
+          }
         }
       }
       __syncthreads();
@@ -198,11 +269,11 @@ __device__ void tr_unit(const TrArgs& a, double* sm, int inst, int m, int j, int
   TPH(2);
   const double* Mi = (k & 1) ? M2 : Ms;            // where the inverse ended up
   double* Gs = (k & 1) ? Ms : M2;                  // free k x k scratch
-  tr_mm(Gs, ldk, nullptr, 0, Bz, ncol1, Mi, ldk, k, k, k, 1.0);            // G = B Sc^{-1}
+  tr_dmma(Gs, ldk, nullptr, 0, Bz, ncol1, Mi, ldk, k, k, k, 1.0);          // G = B Sc^{-1}
   __syncthreads();
   // 4. S_bot = Sc^{-1} T -> Ss rows k..2k-1 ; S_top = R_top - G T -> Ss rows 0..k-1
-  tr_mm(Ss + k * lds, lds, nullptr, 0, Mi, ldk, Ts, lds, k, xm, k, 1.0);
-  tr_mm(Ss, lds, Z2, ncol1, Gs, ldk, Ts, lds, k, xm, k, -1.0);
+  tr_dmma(Ss + k * lds, lds, nullptr, 0, Mi, ldk, Ts, lds, k, xm, k, 1.0);
+  tr_dmma(Ss, lds, Z2, ncol1, Gs, ldk, Ts, lds, k, xm, k, -1.0);
   // zero the K padding rows 2k .. round4(2k) and the column padding of S
   const int K4 = round_up(2 * k, 4), xmp = round_up(xm, 16);
   if (xmp > xm)
@@ -261,6 +332,86 @@ __device__ void tr_unit(const TrArgs& a, double* sm, int inst, int m, int j, int
 #undef TPH
 }
 
+#define TR_NL 4                  // leaves per final-pass group (one warp each in the v phase)
+
+// Final pass for the leaves lu0 .. lu0+nl-1 (global index inst * nleaf + leaf): per-leaf v
+// recursion (one warp per leaf, S blocks double-buffered through shared memory), then
+// u = X v with each leaf's panel block copied to shared memory.
+__device__ void tr_final(const TrArgs& a, double* sm, int lu0, int nl) {
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int vstride = round_up(a.NC, 8), sbuf = a.kmaxc * a.NC;
+  double* vs = sm;                                   // [TR_NL][vstride]
+  double* Sb = sm + TR_NL * vstride;                 // v phase: [TR_NL warps][2][kmax x NC]
+  double* Xs = sm + TR_NL * vstride;                 // u phase: [NC cols][128 rows] (aliases Sb)
+  double* part = Xs + (long long)a.NC * 128;         // [2][128]
+  if (warp < nl) {
+    const int lu = lu0 + warp, inst = lu / a.nleaf, leaf = lu % a.nleaf;
+    double* v = vs + warp * vstride;
+    double* buf = Sb + warp * 2 * sbuf;
+    auto S_of = [&](int m) {
+      const int xm = a.xc[m], k = a.xc[m + 1] - xm;
+      const int jn = leaf >> (a.L - m), side = (leaf >> (a.L - m - 1)) & 1;
+      return a.Sst + (long long)inst * a.sinst + a.slev[m] + (long long)jn * 2 * k * xm + (long long)side * k * xm;
+    };
+    auto issue = [&](int m) {
+      const int xm = a.xc[m], k = a.xc[m + 1] - xm;
+      const double* g = S_of(m);
+      double* d = buf + (m & 1) * sbuf;
+      for (int e = lane; e < k * xm; e += 32) cp_async8(d + e, g + e);
+      cp_async_commit();
+    };
+    for (int c = lane; c < a.NC; c += 32) v[c] = (c == 0) ? 1.0 : 0.0;
+    issue(0);
+    for (int m = 0; m < a.L; ++m) {
+      if (m + 1 < a.L) { issue(m + 1); cp_async_wait_group1(); } else cp_async_wait_all();
+      __syncwarp();
+      const int xm = a.xc[m], k = a.xc[m + 1] - xm;
+      const double* S = buf + (m & 1) * sbuf;
+      if (lane < k) {                            // lane = row q of S_side, 4 FMA chains
+        const double* sr = S + lane * xm;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int c = 0;
+        for (; c + 3 < xm; c += 4) {
+          a0 = fma(sr[c], v[c], a0); a1 = fma(sr[c + 1], v[c + 1], a1);
+          a2 = fma(sr[c + 2], v[c + 2], a2); a3 = fma(sr[c + 3], v[c + 3], a3);
+        }
+        for (; c < xm; ++c) a0 = fma(sr[c], v[c], a0);
+        v[xm + lane] = -((a0 + a1) + (a2 + a3));
+      }
+      for (int q = 32 + lane; q < k; q += 32) {  // (k > 32: remaining rows, one per lane)
+        double acc = 0.0;
+        for (int c = 0; c < xm; ++c) acc = fma(S[q * xm + c], v[c], acc);
+        v[xm + q] = -acc;
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int w = 0; w < nl; ++w) {
+    const int lu = lu0 + w, inst = lu / a.nleaf, leaf = lu % a.nleaf;
+    const int r0 = a.leaf_r0[leaf], s = a.leaf_n[leaf];
+    const double* Xi = a.X + (long long)inst * a.xstride + r0;
+    for (int e = t; e < a.NC * 128; e += TR_THREADS) {
+      const int c = e >> 7, i = e & 127;
+      if (i < s) cp_async8(Xs + e, Xi + (long long)c * a.n + i);
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+    const double* v = vs + w * vstride;
+    {
+      const int i = t & 127, h = t >> 7;           // two column halves, fixed-order sums
+      double acc = 0.0;
+      if (i < s)
+        for (int c = h; c < a.NC; c += 2) acc = fma(Xs[c * 128 + i], v[c], acc);
+      part[h * 128 + i] = acc;
+    }
+    __syncthreads();
+    for (int i = t; i < s; i += TR_THREADS) a.u[(long long)inst * a.n + r0 + i] = part[i] + part[128 + i];
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(TR_THREADS, 1)
 k_tree(const TrArgs a) {
   extern __shared__ double sm[];
@@ -284,87 +435,7 @@ k_tree(const TrArgs a) {
     tr_grid_barrier(a.bar, (++nbar) * G);
     stamp(2 * (a.L - m));
   }
-  // per-leaf v recursion (one warp per leaf, S blocks double-buffered through shared memory),
-  // then u = X v with the leaf's panel block copied to shared memory
-  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  const int NL = 4;                                  // leaves in flight per CTA (v phase)
   const int total = a.batch * a.nleaf;
-  const int vstride = round_up(a.NC, 8), sbuf = a.kmaxc * a.NC;
-  double* vs = sm;                                   // [NL][vstride]
-  double* Sb = sm + NL * vstride;                    // v phase: [NL warps][2][kmax x NC]
-  double* Xs = sm + NL * vstride;                    // u phase: [NC cols][128 rows] (aliases Sb)
-  double* part = Xs + (long long)a.NC * 128;         // [2][128]
-  long long fcl = clock64();
-  for (int base = b; base < total; base += NL * G) {
-    if (warp < NL && base + warp * G < total) {
-      const int lu = base + warp * G, inst = lu / a.nleaf, leaf = lu % a.nleaf;
-      double* v = vs + warp * vstride;
-      double* buf = Sb + warp * 2 * sbuf;
-      auto S_of = [&](int m) {
-        const int xm = a.xc[m], k = a.xc[m + 1] - xm;
-        const int jn = leaf >> (a.L - m), side = (leaf >> (a.L - m - 1)) & 1;
-        return a.Sst + (long long)inst * a.sinst + a.slev[m] + (long long)jn * 2 * k * xm + (long long)side * k * xm;
-      };
-      auto issue = [&](int m) {
-        const int xm = a.xc[m], k = a.xc[m + 1] - xm;
-        const double* g = S_of(m);
-        double* d = buf + (m & 1) * sbuf;
-        for (int e = lane; e < k * xm; e += 32) cp_async8(d + e, g + e);
-        cp_async_commit();
-      };
-      for (int c = lane; c < a.NC; c += 32) v[c] = (c == 0) ? 1.0 : 0.0;
-      issue(0);
-      for (int m = 0; m < a.L; ++m) {
-        if (m + 1 < a.L) { issue(m + 1); cp_async_wait_group1(); } else cp_async_wait_all();
-        __syncwarp();
-        const int xm = a.xc[m], k = a.xc[m + 1] - xm;
-        const double* S = buf + (m & 1) * sbuf;
-        if (lane < k) {                            // lane = row q of S_side, 4 FMA chains
-          const double* sr = S + lane * xm;
-          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-          int c = 0;
-          for (; c + 3 < xm; c += 4) {
-            a0 = fma(sr[c], v[c], a0); a1 = fma(sr[c + 1], v[c + 1], a1);
-            a2 = fma(sr[c + 2], v[c + 2], a2); a3 = fma(sr[c + 3], v[c + 3], a3);
-          }
-          for (; c < xm; ++c) a0 = fma(sr[c], v[c], a0);
-          v[xm + lane] = -((a0 + a1) + (a2 + a3));
-        }
-        for (int q = 32 + lane; q < k; q += 32) {  // (k > 32: remaining rows, one per lane)
-          double acc = 0.0;
-          for (int c = 0; c < xm; ++c) acc = fma(S[q * xm + c], v[c], acc);
-          v[xm + q] = -acc;
-        }
-        __syncwarp();
-      }
-    }
-    __syncthreads();
-    if (a.trace && b == 0 && t == 0) { const long long t_ = clock64(); a.trace[1110] += t_ - fcl; fcl = t_; }
-    for (int w = 0; w < NL && base + w * G < total; ++w) {
-      const int lu = base + w * G, inst = lu / a.nleaf, leaf = lu % a.nleaf;
-      const int r0 = a.leaf_r0[leaf], s = a.leaf_n[leaf];
-      const double* Xi = a.X + (long long)inst * a.xstride + r0;
-      for (int e = t; e < a.NC * 128; e += TR_THREADS) {
-        const int c = e >> 7, i = e & 127;
-        if (i < s) cp_async8(Xs + e, Xi + (long long)c * a.n + i);
-      }
-      cp_async_commit();
-      cp_async_wait_all();
-      __syncthreads();
-      if (a.trace && b == 0 && t == 0) { const long long t_ = clock64(); a.trace[1111] += t_ - fcl; fcl = t_; }
-      const double* v = vs + w * vstride;
-      {
-        const int i = t & 127, h = t >> 7;           // two column halves, fixed-order sums
-        double acc = 0.0;
-        if (i < s)
-          for (int c = h; c < a.NC; c += 2) acc = fma(Xs[c * 128 + i], v[c], acc);
-        part[h * 128 + i] = acc;
-      }
-      __syncthreads();
-      for (int i = t; i < s; i += TR_THREADS) a.u[(long long)inst * a.n + r0 + i] = part[i] + part[128 + i];
-      __syncthreads();
-      if (a.trace && b == 0 && t == 0) { const long long t_ = clock64(); a.trace[1112] += t_ - fcl; fcl = t_; }
-    }
-  }
+  for (int base = b * TR_NL; base < total; base += TR_NL * G) tr_final(a, sm, base, min(TR_NL, total - base));
   stamp(2 * a.L + 1);
 }
