@@ -129,6 +129,8 @@ def algorithmic_work(ranks, n, leaf_sizes, nf=1):
         ft += 2 ** m * (2.0 / 3.0 * k ** 3 + 3.0 * k * k * x + 2.0 * (x - 1) * x * 2 * k)
         bt += 2 ** m * 8.0 * (2 * (xc[m + 1] - 1) * xc[m + 1] + (x - 1) * x + 2 * k * x)
     work["k_tree"] = (ft, bt)
+    # k_step = k_leaf + k_tree fused in one persistent dataflow launch (the default path)
+    work["k_step"] = (fl + ft, by + bt)
     Wl = [sum(ks[:l]) for l in range(L)]
     fl_l = sum(2.0 * n * k * (nf + w + k) + 2.0 * n * k * (nf + w) for k, w in zip(ks, Wl))
     by_l = sum(8.0 * n * (nf + w + k) + 8.0 * n * (nf + w) for k, w in zip(ks, Wl))
@@ -408,7 +410,7 @@ def run_ours(args, world, rank, local):
         t_s = kern[dom]["ms_per_step"] / 1e3
         launches_dom = kern[dom]["launches_per_step"]
         fl, by = work.get(dom, (0.0, 0.0))
-        if dom in ("k_leaf", "k_levels", "k_tree"):
+        if dom in ("k_leaf", "k_levels", "k_tree", "k_step"):
             # FP64 contractions on the DMMA (FP64 tensor) path; MEASURED_PEAKS has no FP64
             # entry: peak = tools/fp64_peak.cu measurement (profiles/fp64_peak_r01.json),
             # equal to the derived 148 SMs x 64 FMA/clk x 2 x 1.965 GHz = 37.2 TFLOP/s
