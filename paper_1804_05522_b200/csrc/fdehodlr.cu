@@ -463,6 +463,26 @@ static int lv_config(const fde_hodlr* H, int mode, int nrhs, LvCfg* cfg) {
                  H->kmax, NCPX);
 }
 
+static void print_leaf_trace(unsigned long long* d_trace) {
+  std::vector<unsigned long long> lt(4096), h(1024);
+  cudaDeviceSynchronize();
+  cudaMemcpy(lt.data(), d_trace + 2048, 4096 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  cudaMemcpy(h.data(), d_trace, 1024 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  double ph[4] = {0, 0, 0, 0};
+  unsigned long long t0 = ~0ULL, t1 = 0;
+  int cnt = 0;
+  for (int l = 0; l < 512 && lt[l * 8 + 4]; ++l, ++cnt) {
+    for (int q = 0; q < 4; ++q) ph[q] += (double)(lt[l * 8 + q + 1] - lt[l * 8 + q]);
+    t0 = std::min(t0, lt[l * 8]);
+    t1 = std::max(t1, lt[l * 8 + 4]);
+  }
+  fprintf(stderr, "k_leaf LU cycles CTA0: gj0 %llu ovw %llu diagupd %llu gj||trail %llu\n", h[960], h[961], h[962], h[963]);
+  fprintf(stderr, "k_leaf panel cycles CTA0 warp0: gen %llu ld %llu solve %llu store %llu\n", h[970], h[971], h[972], h[973]);
+  if (cnt)
+    fprintf(stderr, "k_leaf per-CTA avg us: build %.2f lu %.2f panel %.2f proj %.2f (%d CTAs, span %.1f us)\n",
+            ph[0] / cnt * 1e-3, ph[1] / cnt * 1e-3, ph[2] / cnt * 1e-3, ph[3] / cnt * 1e-3, cnt, (t1 - t0) * 1e-3);
+}
+
 // Layout of the projected-tree path (k_tree.cuh): Q stores of levels 1..L (leaves: L), S
 // stores of levels 0..L-1, work split and shared-memory geometry.  Leaves tree_ok = false
 // (the level-pass path is used) when the panel is too wide for the leaf Q phase.
@@ -553,6 +573,7 @@ static int launch_tree(fde_hodlr* H, double* u_next, cudaStream_t s) {
   { PROF("k_tree"); CU(cudaLaunchCooperativeKernel((void*)k_tree, dim3(H->tr_grid), dim3(TR_THREADS), args, H->tr_smem, s)); }
   LAUNCHED();
   if (g_trace) {
+    print_leaf_trace(g_trace);
     std::vector<unsigned long long> h(64);
     CU(cudaStreamSynchronize(s));
     CU(cudaMemcpy(h.data(), g_trace + 1024, 64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
@@ -692,25 +713,7 @@ static int launch_levels(fde_hodlr* H, int mode, int nf, double* Y, int ld, int 
             h[800], h[801], h[802], h[803], h[804]);
     fprintf(stderr, "k_levels node cycles CTA 0: prep %llu GJ %llu Si %llu store %llu solves %llu\n",
             h[810], h[811], h[812], h[813], h[814]);
-    {
-      std::vector<unsigned long long> lt(4096);
-      CU(cudaMemcpy(lt.data(), d_trace + 2048, 4096 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-      double ph[3] = {0, 0, 0};
-      unsigned long long t0 = ~0ULL, t1 = 0;
-      int cnt = 0;
-      for (int l = 0; l < 1024 && lt[l * 4 + 3]; ++l, ++cnt) {
-        for (int q = 0; q < 3; ++q) ph[q] += (double)(lt[l * 4 + q + 1] - lt[l * 4 + q]);
-        t0 = std::min(t0, lt[l * 4]);
-        t1 = std::max(t1, lt[l * 4 + 3]);
-      }
-      fprintf(stderr, "k_leaf LU cycles CTA0: gj0 %llu ovw %llu diagupd %llu gj||trail %llu\n",
-              h[960], h[961], h[962], h[963]);
-      fprintf(stderr, "k_leaf panel cycles CTA0 warp0: gen %llu ld %llu solve %llu store %llu\n",
-              h[970], h[971], h[972], h[973]);
-      if (cnt)
-        fprintf(stderr, "k_leaf per-CTA avg us: build %.2f lu %.2f panel %.2f (%d CTAs, span %.1f us)\n",
-                ph[0] / cnt * 1e-3, ph[1] / cnt * 1e-3, ph[2] / cnt * 1e-3, cnt, (t1 - t0) * 1e-3);
-    }
+    print_leaf_trace(d_trace);
   }
   return FDE_OK;
 }

@@ -390,8 +390,14 @@ __device__ void leaf_project(const LeafArgs& a, double* big, const PanelCol* pcd
     }
   }
   cp_async_commit();
-  for (int c0 = 0; c0 < NC; c0 += XCH) {
-    const int ncp = min(XCH, round_up(NC - c0, 16));
+  // balanced column chunks of whole n-tile pairs (16 columns), at most XCH wide
+  const int NPT = round_up(NC, 16) >> 4, maxp = XCH >> 4;
+  const int nchunk = (NPT + maxp - 1) / maxp;
+  const int MP = (MT + 1) >> 1;                       // m-tile pairs
+  int c0 = 0;
+  for (int ch = 0; ch < nchunk; ++ch) {
+    const int npc = (NPT * (ch + 1)) / nchunk - (NPT * ch) / nchunk;   // n-pairs in this chunk
+    const int ncp = 16 * npc;
     for (int cc = warp; cc < ncp; cc += LEAF_WARPS)
       for (int q = 0; q < LEAF_MAX / 32; ++q) {
         const int i = lane + 32 * q;
@@ -401,29 +407,39 @@ __device__ void leaf_project(const LeafArgs& a, double* big, const PanelCol* pcd
     cp_async_commit();
     cp_async_wait_all();
     __syncthreads();
-    const int NP = ncp >> 4;
-    for (int u = warp; u < MT * NP; u += LEAF_WARPS) {
-      const int mt = u % MT, n0 = (u / MT) * 16;
-      double d0[2] = {0.0, 0.0}, d1[2] = {0.0, 0.0};
-      const double* ap = Vs + (8 * mt + gid) * LDA_LEAF + tig;
+    // warp unit = (m-tile pair) x (n-tile pair): 2 A + 2 B fragments feed 4 DMMAs per k-step
+    for (int u = warp; u < MP * npc; u += LEAF_WARPS) {
+      const int mp = u % MP, n0 = (u / MP) * 16;
+      const bool m2 = 2 * mp + 1 < MT;
+      double d[2][2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};
+      const double* ap0 = Vs + (16 * mp + gid) * LDA_LEAF + tig;
+      const double* ap1 = ap0 + 8 * LDA_LEAF;
       const double* bp0 = Xs + (n0 + gid) * LDA_LEAF + tig;
       const double* bp1 = bp0 + 8 * LDA_LEAF;
-#pragma unroll 8
+#pragma unroll 4
       for (int k0 = 0; k0 < sp; k0 += 4) {
-        const double av = ap[k0];
-        dmma884(d0[0], d0[1], av, bp0[k0]);
-        dmma884(d1[0], d1[1], av, bp1[k0]);
+        const double a0 = ap0[k0], a1 = m2 ? ap1[k0] : 0.0, b0 = bp0[k0], b1 = bp1[k0];
+        dmma884(d[0][0][0], d[0][0][1], a0, b0);
+        dmma884(d[0][1][0], d[0][1][1], a0, b1);
+        dmma884(d[1][0][0], d[1][0][1], a1, b0);
+        dmma884(d[1][1][0], d[1][1][1], a1, b1);
       }
-      const int j = 8 * mt + gid, c = c0 + n0 + 2 * tig;
-      if (j < NV) {
-        double* qr = Qo + (long long)j * NC;
-        if (c < NC) qr[c] = d0[0];
-        if (c + 1 < NC) qr[c + 1] = d0[1];
-        if (c + 8 < NC) qr[c + 8] = d1[0];
-        if (c + 9 < NC) qr[c + 9] = d1[1];
+#pragma unroll
+      for (int hm = 0; hm < 2; ++hm) {
+        const int j = 16 * mp + 8 * hm + gid;
+        if (j < NV) {
+          double* qr = Qo + (long long)j * NC;
+#pragma unroll
+          for (int hn = 0; hn < 2; ++hn) {
+            const int c = c0 + n0 + 8 * hn + 2 * tig;
+            if (c < NC) qr[c] = d[hm][hn][0];
+            if (c + 1 < NC) qr[c + 1] = d[hm][hn][1];
+          }
+        }
       }
     }
     __syncthreads();
+    c0 += ncp;
   }
 }
 
@@ -452,7 +468,7 @@ __device__ __forceinline__ void leaf_task(const LeafArgs& a, double* smem, int l
       if (trc) {
         unsigned long long tm;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm));
-        a.trace[2048 + leaf * 4 + ph] = tm;
+        a.trace[2048 + leaf * 8 + ph] = tm;
       }
     }
   };
@@ -475,19 +491,34 @@ __device__ __forceinline__ void leaf_task(const LeafArgs& a, double* smem, int l
       for (int cc = t; cc < ce - cb; cc += LEAF_THREADS) pcd[cc] = panel_col(a, inst, leaf, r0, cb + cc, ce);
     }
     __syncthreads();
-    for (int j = warp; j < sp; j += LEAF_WARPS)
-      for (int i = lane; i < sp; i += 32) {
-        double v;
-        if (i < s && j < s) {
-          const int k1 = i - j + 1, k2 = j - i + 1;     // T[i,j] = -g_{i-j+1}, T^T[i,j] = T[j,i]
-          const double tij = (k1 >= 0) ? -gs[k1] : 0.0;
-          const double tji = (k2 >= 0) ? -gs[k2] : 0.0;
-          v = (i == j ? a.shift : 0.0) + c * (dps[i] * tij + dms[i] * tji);
-        } else {
-          v = (i == j) ? 1.0 : 0.0;
-        }
-        A[i + j * LDA_LEAF] = v;
+    {
+      // lane owns rows lane + 32u (their d+- in registers); 4 independent elements per column
+      double dpr[LEAF_MAX / 32], dmr[LEAF_MAX / 32];
+#pragma unroll
+      for (int u = 0; u < LEAF_MAX / 32; ++u) {
+        const int i = lane + 32 * u;
+        dpr[u] = i < s ? dps[i] : 0.0;
+        dmr[u] = i < s ? dms[i] : 0.0;
       }
+      for (int j = warp; j < sp; j += LEAF_WARPS) {
+#pragma unroll
+        for (int u = 0; u < LEAF_MAX / 32; ++u) {
+          const int i = lane + 32 * u;
+          if (i < sp) {
+            double v;
+            if (i < s && j < s) {
+              const int k1 = i - j + 1, k2 = j - i + 1;   // T[i,j] = -g_{i-j+1}, T^T[i,j] = T[j,i]
+              const double tij = (k1 >= 0) ? -gs[k1] : 0.0;
+              const double tji = (k2 >= 0) ? -gs[k2] : 0.0;
+              v = (i == j ? a.shift : 0.0) + c * (dpr[u] * tij + dmr[u] * tji);
+            } else {
+              v = (i == j) ? 1.0 : 0.0;
+            }
+            A[i + j * LDA_LEAF] = v;
+          }
+        }
+      }
+    }
     __syncthreads();
     stamp(1);
     // ---- S4: block LU (inverse-diagonal form, off-diagonal blocks negated)
@@ -590,15 +621,9 @@ __device__ __forceinline__ void leaf_task(const LeafArgs& a, double* smem, int l
           }
       }
     }
+    stamp(3);
     if (a.Q) leaf_project(a, A, pcd, c_begin, c_end, s, sp, Xi, a.Q + (long long)inst * a.qinst + (long long)leaf * a.qstride);
-    if (a.trace) {                      // (no barrier inside a stamp after divergent loops)
-      __syncthreads();
-      if (trc) {
-        unsigned long long tm;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm));
-        a.trace[2048 + leaf * 4 + 3] = tm;
-      }
-    }
+    stamp(4);
   } else {
     // ---- solve mode: factor from HBM, right-hand sides b (+ dt f) -> y (y may alias b)
     for (int j = warp; j < sp; j += LEAF_WARPS)

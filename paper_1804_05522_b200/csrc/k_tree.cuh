@@ -150,6 +150,40 @@ __device__ __forceinline__ double tr_rcp(double x) {
   return fma(y, e, y);
 }
 
+
+// Sc^{-1} for k <= KG by ONE warp, no CTA barrier: unpivoted Gauss-Jordan (reading R17) with
+// lane r owning row r of the KG x KG matrix (identity padding beyond k), the pivot row
+// broadcast by shuffles, and the columns rotated left by one per pivot so that the pivot
+// column is always register 0 (compile-time register indices; after KG pivots the rotation
+// is the identity).  In: M (k x k, ld ldm); out: Mi (k x k, ld ldm).
+template <int KG>
+__device__ __noinline__ void tr_warp_gj(const double* M, double* Mi, int ldm, int k, DevStatus* st, int where) {
+  const int r = threadIdx.x & 31;
+  double row[KG];
+#pragma unroll
+  for (int c = 0; c < KG; ++c) row[c] = (r < k && c < k) ? M[r * ldm + c] : (r == c ? 1.0 : 0.0);
+  bool bad = false;
+#pragma unroll 1
+  for (int p = 0; p < KG; ++p) {
+    double pr[KG];
+#pragma unroll
+    for (int c = 0; c < KG; ++c) pr[c] = __shfl_sync(0xffffffffu, row[c], p);
+    const double piv = pr[0];
+    bad |= !(isfinite(piv) && piv != 0.0);
+    const double rp = tr_rcp(piv);
+    const bool me = r == p;
+    const double f = row[0] * rp;
+#pragma unroll
+    for (int c = 1; c < KG; ++c) row[c - 1] = me ? pr[c] * rp : fma(-f, pr[c], row[c]);
+    row[KG - 1] = me ? rp : -f;
+  }
+  if (bad && r == 0) latch_status(st, FDE_ESINGULAR, where);
+  if (r < k)
+#pragma unroll
+    for (int c = 0; c < KG; ++c)
+      if (c < k) Mi[r * ldm + c] = row[c];
+}
+
 // One (node, row chunk) unit of level m.  All global reads are asynchronous copies into
 // shared memory (cp.async), so the latency of L2/HBM is paid once per stage, not per load.
 __device__ void tr_unit(const TrArgs& a, double* sm, int inst, int m, int j, int chunk) {
@@ -211,64 +245,44 @@ __device__ void tr_unit(const TrArgs& a, double* sm, int inst, int m, int j, int
   }
   __syncthreads();
   TPH(1);
-  // 3. Sc^{-1}: unpivoted Gauss-Jordan (reading R17), ping-pong Ms <-> M2, one barrier per
-  //    pivot; the thread that updates the next pivot also forms its reciprocal (off the
-  //    critical path of the following step)
-  {
-    // fast path (k*k <= 2 * TR_THREADS): each thread owns at most two fixed elements, all
-    // addresses hoisted out of the pivot loop; per pivot: 3 loads, 2 flops, 1 store, 1 barrier
+  // 3. Sc^{-1}: warp-level Gauss-Jordan in registers (tr_warp_gj) for k <= 32, else the
+  //    CTA-wide ping-pong version with one barrier per pivot
+  const double* Mi;
+  double* Gs;
+  if (k <= 32) {
+    if (warp == 0) {
+      const int where = inst * 65536 + 32768 + node_index(m, j);
+      if (k <= 16) tr_warp_gj<16>(Ms, M2, ldk, k, a.st, where);
+      else if (k <= 24) tr_warp_gj<24>(Ms, M2, ldk, k, a.st, where);
+      else tr_warp_gj<32>(Ms, M2, ldk, k, a.st, where);
+    }
+    __syncthreads();
+    Mi = M2;
+    Gs = Ms;
+  } else {
     const int kk = k * k;
-    const bool fast = kk <= 2 * TR_THREADS;
-    const int e0 = t, e1 = t + TR_THREADS;
-    const int q0 = e0 / k, c0 = e0 - q0 * k, q1 = e1 / k, c1 = e1 - q1 * k;
-    const bool h0 = e0 < kk, h1 = e1 < kk;
-    const int oq0 = q0 * ldk, oq1 = q1 * ldk;
     for (int p = 0; p < k; ++p) {
       const double* src = (p & 1) ? M2 : Ms;
       double* dst = (p & 1) ? Ms : M2;
       const double rp = rcp_buf[p & 1];
       const int op = p * ldk;
-      if (fast) {
-        double v0 = 0.0, v1 = 0.0;
-        if (h0) {
-          const double mqp = src[oq0 + p], mpc = src[op + c0], mqc = src[oq0 + c0];
-          const double fq = -mqp * rp;
-          v0 = (q0 == p) ? ((c0 == p) ? rp : mpc * rp) : ((c0 == p) ? fq : fma(fq, mpc, mqc));
-        }
-        if (h1) {
-          const double mqp = src[oq1 + p], mpc = src[op + c1], mqc = src[oq1 + c1];
-          const double fq = -mqp * rp;
-          v1 = (q1 == p) ? ((c1 == p) ? rp : mpc * rp) : ((c1 == p) ? fq : fma(fq, mpc, mqc));
-        }
-        if (h0) dst[oq0 + c0] = v0;
-        if (h1) dst[oq1 + c1] = v1;
-        if (h0 && q0 == p + 1 && c0 == p + 1) {
-          if (!(isfinite(v0) && fabs(v0) > 0.0)) latch_status(a.st, FDE_ESINGULAR, inst * 65536 + 32768 + node_index(m, j));
-          rcp_buf[(p + 1) & 1] = tr_rcp(v0);
-        }
-        if (h1 && q1 == p + 1 && c1 == p + 1) {
-          if (!(isfinite(v1) && fabs(v1) > 0.0)) latch_status(a.st, FDE_ESINGULAR, inst * 65536 + 32768 + node_index(m, j));
-          rcp_buf[(p + 1) & 1] = tr_rcp(v1);
-        }
-      } else {
-        for (int e = t; e < kk; e += TR_THREADS) {
-          const int q = e / k, cc = e - q * k;
-          const double mqp = src[q * ldk + p], mpc = src[op + cc], mqc = src[q * ldk + cc];
-          const double fq = -mqp * rp;
-          const double v = (q == p) ? ((cc == p) ? rp : mpc * rp) : ((cc == p) ? fq : fma(fq, mpc, mqc));
-          dst[q * ldk + cc] = v;
-          if (q == p + 1 && cc == p + 1) {
-            if (!(isfinite(v) && fabs(v) > 0.0)) latch_status(a.st, FDE_ESINGULAR, inst * 65536 + 32768 + node_index(m, j));
-            rcp_buf[(p + 1) & 1] = tr_rcp(v);
-          }
+      for (int e = t; e < kk; e += TR_THREADS) {
+        const int q = e / k, cc = e - q * k;
+        const double mqp = src[q * ldk + p], mpc = src[op + cc], mqc = src[q * ldk + cc];
+        const double fq = -mqp * rp;
+        const double v = (q == p) ? ((cc == p) ? rp : mpc * rp) : ((cc == p) ? fq : fma(fq, mpc, mqc));
+        dst[q * ldk + cc] = v;
+        if (q == p + 1 && cc == p + 1) {
+          if (!(isfinite(v) && fabs(v) > 0.0)) latch_status(a.st, FDE_ESINGULAR, inst * 65536 + 32768 + node_index(m, j));
+          rcp_buf[(p + 1) & 1] = tr_rcp(v);
         }
       }
       __syncthreads();
     }
+    Mi = (k & 1) ? M2 : Ms;
+    Gs = (k & 1) ? Ms : M2;
   }
   TPH(2);
-  const double* Mi = (k & 1) ? M2 : Ms;            // where the inverse ended up
-  double* Gs = (k & 1) ? Ms : M2;                  // free k x k scratch
   tr_dmma(Gs, ldk, nullptr, 0, Bz, ncol1, Mi, ldk, k, k, k, 1.0);          // G = B Sc^{-1}
   __syncthreads();
   // 4. S_bot = Sc^{-1} T -> Ss rows k..2k-1 ; S_top = R_top - G T -> Ss rows 0..k-1
