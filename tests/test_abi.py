@@ -86,3 +86,22 @@ def test_product_path_never_touches_the_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(from|import)\s+oracle", txt, flags=re.M), f
+
+
+def test_fde2d_rejects_bad_arguments_on_host(lib):
+    """fde2d_step validates alpha / sizes / tolerances before any device work (no GPU needed)."""
+    import ctypes
+    from paper_1804_05522_b200 import _lib
+    nul = ctypes.c_void_p()
+    rx, res, its = ctypes.c_int(), ctypes.c_double(), ctypes.c_int()
+    cache = (ctypes.c_void_p * 2)()
+    def call(nx=64, a1=1.3, a2=1.7, tol=1e-12, ek_tol=1e-11, rmax=8):
+        return lib.fde2d_step(nx, 64, a1, a2, 1.0 / 65, 1.0 / 65, 0.1, nul, nul, nul, nul, nul, nul, 0,
+                              nul, nul, 0, nul, nul, rmax, ctypes.byref(rx), tol, ek_tol, 10, 32,
+                              ctypes.cast(cache, ctypes.POINTER(ctypes.c_void_p)), ctypes.byref(res),
+                              ctypes.byref(its), 0, nul)
+    assert call(a1=2.5) == _lib.FDE_EDOMAIN
+    assert call(nx=0) == _lib.FDE_EDOMAIN
+    assert call(tol=0.0) == _lib.FDE_EDOMAIN
+    assert call() == _lib.FDE_EDOMAIN            # NULL coefficient arrays
+    assert "NULL" in lib.fde_last_error().decode() or "coefficient" in lib.fde_last_error().decode()

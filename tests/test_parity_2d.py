@@ -109,3 +109,24 @@ def test_symmetric_data_gives_symmetric_solution():
     Xg = Xu.cpu().numpy().T @ Xv.cpu().numpy()
     assert _rel(Xg, Xg.T) <= 1e-10
     st.close()
+
+
+@gpu
+def test_rank_cap_and_nonconvergence_are_reported():
+    """rmax below the solution rank -> FDE_EDIM; ek_maxit = 1 -> FDE_ENOCONV (best iterate kept)."""
+    from paper_1804_05522_b200._lib import FdeError, FDE_EDIM, FDE_ENOCONV
+    from paper_1804_05522_b200.hodlr import Fde2dStepper
+    wl = W.cfg5(n=256)
+    Fa, Fb = wl.source_factors(1)
+    st = Fde2dStepper(wl.nx, wl.ny, wl.alpha1, wl.alpha2, wl.hx, wl.hy, wl.dt, _t(wl.d1p), _t(wl.d1m),
+                      _t(wl.d2p), _t(wl.d2m), wl.tol, ek_tol=wl.ek_tol, leaf=wl.leaf, rmax=3)
+    with pytest.raises(FdeError) as e:
+        st.step(_t(Fa.T), _t(Fb.T))
+    assert e.value.code == FDE_EDIM
+    st.close()
+    st = Fde2dStepper(wl.nx, wl.ny, wl.alpha1, wl.alpha2, wl.hx, wl.hy, wl.dt, _t(wl.d1p), _t(wl.d1m),
+                      _t(wl.d2p), _t(wl.d2m), wl.tol, ek_tol=wl.ek_tol, ek_maxit=1, leaf=wl.leaf)
+    with pytest.raises(FdeError) as e:
+        st.step(_t(Fa.T), _t(Fb.T))
+    assert e.value.code == FDE_ENOCONV
+    st.close()
