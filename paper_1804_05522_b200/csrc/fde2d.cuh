@@ -81,9 +81,9 @@ static int transpose(cudaStream_t s, int m, int n, const double* X, int ldx, dou
 static bool g_dn_attr = false;
 static int dn_attrs() {
   if (g_dn_attr) return FDE_OK;
-  CU(cudaFuncSetAttribute(k_sym_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, DN_SMEM_MAX + 8192));
-  CU(cudaFuncSetAttribute(k_osj_svd, cudaFuncAttributeMaxDynamicSharedMemorySize, DN_SMEM_MAX + 8192));
-  CU(cudaFuncSetAttribute(k_gj_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, DN_SMEM_MAX + 8192));
+  CU(cudaFuncSetAttribute(k_sym_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, DN_SMEM_MAX + 4096));
+  CU(cudaFuncSetAttribute(k_osj_svd, cudaFuncAttributeMaxDynamicSharedMemorySize, DN_SMEM_MAX + 4096));
+  CU(cudaFuncSetAttribute(k_gj_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, DN_SMEM_MAX + 4096));
   g_dn_attr = true;
   return FDE_OK;
 }
@@ -467,53 +467,72 @@ extern "C" int fde2d_step(int nx, int ny, double alpha1, double alpha2, double h
   int it = 0, sit = 0;
   double rel = 1.0, prev_rel = 1e300;
   bool conv = false;
-  for (it = 1; it <= ek_maxit; ++it) {
+  int solved_x = -1, solved_y = -1;
+  // one projected solve on the current bases + the true residual (returns rc; sets rel)
+  auto solve_and_check = [&]() -> int {
     const int sa = sx.s, sbb = sy.s;
     // A~ = U^T A1 U ; Bh = V^T A2 V ; B~ = Bh^T ; C~ = (U^T Cu) diag(sig) (V^T Cv)^T
-    if ((rc = ts_tn(s, sa, sa, nx, 1.0, Ux, nx, AUx, nx, 0.0, Am, sa)) != FDE_OK) return fail(rc);
-    if ((rc = ts_tn(s, sbb, sbb, ny, 1.0, AVy, ny, Vy, ny, 0.0, Bm, sbb)) != FDE_OK) return fail(rc);  // (A2 V)^T V = B~
-    if ((rc = ts_tn(s, sa, rcr, nx, 1.0, Ux, nx, Cu, nx, 0.0, w.M1, sa)) != FDE_OK) return fail(rc);
-    if ((rc = ts_tn(s, rcr, sbb, ny, 1.0, Cv, ny, Vy, ny, 0.0, w.S, rcr)) != FDE_OK) return fail(rc);   // (V^T Cv)^T
+    if ((rc = ts_tn(s, sa, sa, nx, 1.0, Ux, nx, AUx, nx, 0.0, Am, sa)) != FDE_OK) return rc;
+    if ((rc = ts_tn(s, sbb, sbb, ny, 1.0, AVy, ny, Vy, ny, 0.0, Bm, sbb)) != FDE_OK) return rc;  // (A2 V)^T V = B~
+    if ((rc = ts_tn(s, sa, rcr, nx, 1.0, Ux, nx, Cu, nx, 0.0, w.M1, sa)) != FDE_OK) return rc;
+    if ((rc = ts_tn(s, rcr, sbb, ny, 1.0, Cv, ny, Vy, ny, 0.0, w.S, rcr)) != FDE_OK) return rc;   // (V^T Cv)^T
     CU(cudaMemcpyAsync(w.lam, sigc.data(), rcr * 8, cudaMemcpyHostToDevice, s));
     {
       // scale the rows of (V^T Cv)^T by sigma: use a diagonal via k_ts_gemm_nn with a diag matrix
       std::vector<double> dg((size_t)rcr * rcr, 0.0);
       for (int i = 0; i < rcr; ++i) dg[(size_t)i * rcr + i] = sigc[i];
       CU(cudaMemcpyAsync(w.G, dg.data(), dg.size() * 8, cudaMemcpyHostToDevice, s));
-      if ((rc = ts_nn(s, sa, rcr, rcr, 1.0, w.M1, sa, w.G, rcr, 0.0, w.M2, sa)) != FDE_OK) return fail(rc);
-      if ((rc = ts_nn(s, sa, sbb, rcr, 1.0, w.M2, sa, w.S, rcr, 0.0, Cm, sa)) != FDE_OK) return fail(rc);
+      if ((rc = ts_nn(s, sa, rcr, rcr, 1.0, w.M1, sa, w.G, rcr, 0.0, w.M2, sa)) != FDE_OK) return rc;
+      if ((rc = ts_nn(s, sa, sbb, rcr, 1.0, w.M2, sa, w.S, rcr, 0.0, Cm, sa)) != FDE_OK) return rc;
       CU(cudaStreamSynchronize(s));
     }
     CU(cudaMemcpyAsync(Ym, Cm, (size_t)sa * sbb * 8, cudaMemcpyDeviceToDevice, s));
     // keep copies of A~ and B~ (the sign iteration destroys them): Lc <- A~, Rc <- Bh = B~^T
     CU(cudaMemcpyAsync(Lc, Am, (size_t)sa * sa * 8, cudaMemcpyDeviceToDevice, s));
-    if ((rc = ts_tn(s, sbb, sbb, ny, 1.0, Vy, ny, AVy, ny, 0.0, Rc, sbb)) != FDE_OK) return fail(rc);
-    if ((rc = proj_sylvester(s, w, sa, sbb, Am, Bm, Ym, st, &sit)) != FDE_OK) return fail(rc);
+    if ((rc = ts_tn(s, sbb, sbb, ny, 1.0, Vy, ny, AVy, ny, 0.0, Rc, sbb)) != FDE_OK) return rc;
+    if ((rc = proj_sylvester(s, w, sa, sbb, Am, Bm, Ym, st, &sit)) != FDE_OK) return rc;
     // residual: Ra = A1 U - U A~ (nx x sa) ; ||Ra Y|| ; Rb = A2 V - V Bh ; ||Rb Y^T||
     CU(cudaMemcpyAsync(Wt, AUx, (size_t)nx * sa * 8, cudaMemcpyDeviceToDevice, s));
-    if ((rc = ts_nn(s, nx, sa, sa, -1.0, Ux, nx, Lc, sa, 1.0, Wt, nx)) != FDE_OK) return fail(rc);
-    if ((rc = ts_nn(s, nx, sbb, sa, 1.0, Wt, nx, Ym, sa, 0.0, w.M2, nx)) != FDE_OK) return fail(rc);
+    if ((rc = ts_nn(s, nx, sa, sa, -1.0, Ux, nx, Lc, sa, 1.0, Wt, nx)) != FDE_OK) return rc;
+    if ((rc = ts_nn(s, nx, sbb, sa, 1.0, Wt, nx, Ym, sa, 0.0, w.M2, nx)) != FDE_OK) return rc;
     double ra2 = 0.0, rb2 = 0.0;
-    if ((rc = sumsq(s, nx, sbb, w.M2, nx, w.dv + 8, &ra2)) != FDE_OK) return fail(rc);
+    if ((rc = sumsq(s, nx, sbb, w.M2, nx, w.dv + 8, &ra2)) != FDE_OK) return rc;
     CU(cudaMemcpyAsync(Wt, AVy, (size_t)ny * sbb * 8, cudaMemcpyDeviceToDevice, s));
-    if ((rc = ts_nn(s, ny, sbb, sbb, -1.0, Vy, ny, Rc, sbb, 1.0, Wt, ny)) != FDE_OK) return fail(rc);
+    if ((rc = ts_nn(s, ny, sbb, sbb, -1.0, Vy, ny, Rc, sbb, 1.0, Wt, ny)) != FDE_OK) return rc;
     // Y^T (sbb x sa) for Rb Y^T: transpose Y into Zm
-    if ((rc = transpose(s, sa, sbb, Ym, sa, Zm, sbb)) != FDE_OK) return fail(rc);
-    if ((rc = ts_nn(s, ny, sa, sbb, 1.0, Wt, ny, Zm, sbb, 0.0, w.M2, ny)) != FDE_OK) return fail(rc);
-    if ((rc = sumsq(s, ny, sa, w.M2, ny, w.dv + 8, &rb2)) != FDE_OK) return fail(rc);
+    if ((rc = transpose(s, sa, sbb, Ym, sa, Zm, sbb)) != FDE_OK) return rc;
+    if ((rc = ts_nn(s, ny, sa, sbb, 1.0, Wt, ny, Zm, sbb, 0.0, w.M2, ny)) != FDE_OK) return rc;
+    if ((rc = sumsq(s, ny, sa, w.M2, ny, w.dv + 8, &rb2)) != FDE_OK) return rc;
     rel = std::sqrt((ra2 + rb2) / cnorm2);
     if (getenv("FDE_DEBUG2D"))
       fprintf(stderr, "fde2d it %d: sa %d sb %d rc %d sign-its %d rel %.3e (ra2 %.3e rb2 %.3e c2 %.3e)\n", it, sa,
               sbb, rcr, sit, rel, ra2, rb2, cnorm2);
-    // converged: below ek_tol, or stagnated at the rounding floor of the residual evaluation
-    // (reading R19: ||Rb|| carries eps ||A2 V||; cfg5's floor is ~1.2e-11 relative) within 10x
-    if (rel <= ek_tol || (rel <= 10.0 * ek_tol && rel >= 0.9 * prev_rel)) { conv = true; break; }
-    prev_rel = rel;
+    solved_x = sx.s; solved_y = sy.s;
+    return FDE_OK;
+  };
+  bool solve_now = true;
+  for (it = 1; it <= ek_maxit; ++it) {
+    if (solve_now || it == ek_maxit) {
+      if ((rc = solve_and_check()) != FDE_OK) return fail(rc);
+      // converged: below ek_tol, or stagnated at the rounding floor of the residual evaluation
+      // (reading R19: ||Rb|| carries eps ||A2 V||; cfg5's floor is ~1.2e-11 relative) within 10x
+      if (rel <= ek_tol || (rel <= 10.0 * ek_tol && rel >= 0.9 * prev_rel)) { conv = true; break; }
+      prev_rel = rel;
+      // far from converged: grow twice before the next projected solve (the residual of the
+      // extended Krylov method falls by well under 1e3 per iteration)
+      solve_now = rel <= 1e3 * ek_tol;
+    } else {
+      solve_now = true;
+    }
     if (it == ek_maxit) break;
     const int s0x = sx.s, s0y = sy.s;
     if ((rc = ek_grow(s, w, sx, Wt, dtol)) != FDE_OK) return fail(rc);
     if ((rc = ek_grow(s, w, sy, Wt, dtol)) != FDE_OK) return fail(rc);
     if (sx.s == s0x && sy.s == s0y) break;         // no new directions (EK_SMAX or exhausted)
+  }
+  if (!conv && (solved_x != sx.s || solved_y != sy.s)) {   // Y must belong to the final bases
+    if ((rc = solve_and_check()) != FDE_OK) return fail(rc);
+    conv = rel <= 10.0 * ek_tol;
   }
   (void)hsum;
   if (resid_out) *resid_out = rel;

@@ -135,7 +135,7 @@ struct fde_hodlr {
   TrArgs tr_geo{};
   size_t tr_smem = 0;
   int* d_done = nullptr;            // k_step task counter + completion counters
-  long long dofs[LMAX + 1] = {}, ndone = 0;
+  long long dofs[LMAX + 1] = {}, ndone = 0, lofs = 0;
   int step_grid = 0;
   size_t step_smem = 0;
   int npost = 0;
@@ -544,6 +544,7 @@ static int tree_layout(fde_hodlr* H) {
   long long dn = 1;                                   // [0] = task counter
   for (int m = 0; m < L; ++m) { H->dofs[m] = dn; dn += (long long)B << m; }
   H->dofs[L] = dn; dn += (long long)B << (L - 1);
+  H->lofs = dn; dn += (long long)B * H->nleaf;
   H->ndone = dn;
   TRY(dalloc(H, &H->d_done, (size_t)dn));
   H->step_smem = std::max((size_t)LEAF_SMEM, bytes);
@@ -840,10 +841,28 @@ static int factor_impl(fde_hodlr* H, const double* dp, const double* dm, int nf,
     sa.ctr = reinterpret_cast<unsigned*>(H->d_done);
     sa.done = H->d_done;
     for (int l = 0; l <= L; ++l) sa.dofs[l] = H->dofs[l];
+    sa.lofs = H->lofs;
+    static unsigned long long* step_trace = nullptr;
+    if (getenv("FDE_TRACE_STEP")) {
+      if (!step_trace) CU(cudaMalloc(&step_trace, 16384 * sizeof(unsigned long long)));
+      CU(cudaMemsetAsync(step_trace, 0, 16384 * sizeof(unsigned long long), s));
+      sa.trace = step_trace;
+    }
     CU(cudaMemsetAsync(H->d_done, 0, H->ndone * sizeof(int), s));
     void* args[] = {&sa};
     { PROF("k_step"); CU(cudaLaunchCooperativeKernel((void*)k_step, dim3(H->step_grid), dim3(TR_THREADS), args, H->step_smem, s)); }
     LAUNCHED();
+    if (sa.trace) {
+      std::vector<unsigned long long> h(16384);
+      CU(cudaStreamSynchronize(s));
+      CU(cudaMemcpy(h.data(), sa.trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+      FILE* fo = fopen(getenv("FDE_TRACE_STEP"), "w");
+      if (fo) {
+        for (int i = 0; i < 4000; ++i)
+          if (h[4 * i + 1]) fprintf(fo, "%d %llu %llu %llu %llu\n", i, h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3]);
+        fclose(fo);
+      }
+    }
     return FDE_OK;
   }
   { PROF("k_leaf"); k_leaf<<<dim3(H->nleaf, B), LEAF_THREADS, LEAF_SMEM, s>>>(la); }

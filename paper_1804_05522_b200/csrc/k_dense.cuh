@@ -11,7 +11,7 @@
 #define DN_THREADS 256
 #define DN_BIG 1024                    // threads of the single-CTA kernels
 #define TS_TILE 16
-#define DN_SMEM_MAX (200 * 1024)       // dynamic shared memory of the single-CTA kernels
+#define DN_SMEM_MAX (206 * 1024)       // dynamic shared memory of the single-CTA kernels
 
 // C (m x n) = alpha * A^T B + beta * C;  A: K x m (lda), B: K x n (ldb); K is the tall dim.
 // One CTA per 16 x 16 tile of C; the K loop is staged through shared memory.

@@ -443,7 +443,8 @@ __device__ void leaf_project(const LeafArgs& a, double* big, const PanelCol* pcd
   }
 }
 
-__device__ __forceinline__ void leaf_task(const LeafArgs& a, double* smem, int leaf, int inst) {
+__device__ __forceinline__ void leaf_task(const LeafArgs& a, double* smem, int leaf, int inst,
+                                          bool do_proj = true) {
   double* S = smem;                               // 32 x 33 scratch (g staging, Gauss-Jordan)
   double* dps = S + 32 * 33;                      // d+ / d- of the leaf rows
   double* dms = dps + LEAF_MAX;
@@ -622,7 +623,8 @@ __device__ __forceinline__ void leaf_task(const LeafArgs& a, double* smem, int l
       }
     }
     stamp(3);
-    if (a.Q) leaf_project(a, A, pcd, c_begin, c_end, s, sp, Xi, a.Q + (long long)inst * a.qinst + (long long)leaf * a.qstride);
+    if (a.Q && do_proj)
+      leaf_project(a, A, pcd, c_begin, c_end, s, sp, Xi, a.Q + (long long)inst * a.qinst + (long long)leaf * a.qstride);
     stamp(4);
   } else {
     // ---- solve mode: factor from HBM, right-hand sides b (+ dt f) -> y (y may alias b)
@@ -665,4 +667,19 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1)
 k_leaf(const LeafArgs a) {
   extern __shared__ double smem[];
   leaf_task(a, smem, blockIdx.x, blockIdx.y);
+}
+
+// The projection Q_leaf = V_all^T X_leaf as a task of its own (k_step.cuh): X is read back from
+// global memory, so it can run on any SM once the leaf's panel is written.
+__device__ __forceinline__ void leaf_proj_task(const LeafArgs& a, double* smem, int leaf, int inst) {
+  double* bs = smem + 32 * 33 + 2 * LEAF_MAX;
+  PanelCol* pcd = reinterpret_cast<PanelCol*>(bs + LEAF_MAX);
+  const TreeDev& tr = a.tree;
+  const int r0 = tr.leaf_r0[leaf], s = tr.leaf_n[leaf], sp = round_up(s, 32);
+  const int c_begin = 1 - a.nf, c_end = a.xcol[tr.L];
+  for (int cc = threadIdx.x; cc < c_end - c_begin; cc += LEAF_THREADS)
+    pcd[cc] = panel_col(a, inst, leaf, r0, c_begin + cc, c_end);
+  const double* Xi = a.X + (long long)inst * a.xstride + r0;
+  leaf_project(a, smem + LEAF_FRONT, pcd, c_begin, c_end, s, sp, Xi,
+               a.Q + (long long)inst * a.qinst + (long long)leaf * a.qstride);
 }

@@ -17,7 +17,9 @@ struct StepArgs {
   unsigned* ctr;                 // task counter (zeroed before the launch)
   int* done;                     // completion counters (zeroed before the launch)
   long long dofs[LMAX + 1];      // per level m (0..L-1): offset of [inst][node] counters;
-                                 // dofs[L]: [inst][level L-1 node] count of finished leaves
+                                 // dofs[L]: [inst][level L-1 node] count of projected leaves
+  long long lofs;                // [inst][leaf] panel-done flags
+  unsigned long long* trace;     // optional: [task][start, end, kind, sm] (FDE_TRACE_STEP)
 };
 
 __device__ __forceinline__ int st_ld_acquire(const int* p) {
@@ -48,7 +50,7 @@ k_step(const StepArgs sa) {
   const int B = a.batch, L = a.L, nleaf = a.nleaf;
   const long long n_leaf = (long long)B * nleaf;
   long long n_lvl[LMAX];
-  long long total = n_leaf;
+  long long total = 2 * n_leaf;                    // panel tasks, then projection tasks
   for (int m = L - 1; m >= 0; --m) { n_lvl[m] = (long long)B * (1LL << m) * a.rc[m]; total += n_lvl[m]; }
   const long long n_fin = (n_leaf + TR_NL - 1) / TR_NL;
   total += n_fin;
@@ -58,10 +60,32 @@ k_step(const StepArgs sa) {
     __syncthreads();
     long long tk = task;
     if (tk >= total) break;
-    if (tk < n_leaf) {                             // ---- leaf: LU, panel, projection
+    const long long tk0 = tk;
+    unsigned long long t_start = 0;
+    if (sa.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    auto rec = [&](int kind) {
+      if (sa.trace && threadIdx.x == 0 && tk0 < 4000) {
+        unsigned long long te, smid;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(te));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(*(unsigned*)&smid));
+        sa.trace[4 * tk0] = t_start; sa.trace[4 * tk0 + 1] = te; sa.trace[4 * tk0 + 2] = kind;
+        sa.trace[4 * tk0 + 3] = smid & 0xffffffffu;
+      }
+    };
+    if (tk < n_leaf) {                             // ---- leaf: build, LU, panel X
       const int inst = (int)(tk / nleaf), leaf = (int)(tk % nleaf);
-      leaf_task(sa.la, smem, leaf, inst);
+      leaf_task(sa.la, smem, leaf, inst, false);
+      st_signal(sa.done + sa.lofs + tk);
+      rec(100);
+      continue;
+    }
+    tk -= n_leaf;
+    if (tk < n_leaf) {                             // ---- leaf: projection Q = V^T X
+      const int inst = (int)(tk / nleaf), leaf = (int)(tk % nleaf);
+      st_wait(sa.done + sa.lofs + tk, 1);
+      leaf_proj_task(sa.la, smem, leaf, inst);
       st_signal(sa.done + sa.dofs[L] + (long long)inst * (1 << (L - 1)) + (leaf >> 1));
+      rec(101);
       continue;
     }
     tk -= n_leaf;
@@ -80,6 +104,7 @@ k_step(const StepArgs sa) {
       }
       tr_unit(a, smem, inst, m, j, chunk);
       st_signal(sa.done + sa.dofs[m] + (long long)inst * (1 << m) + j);
+      rec(m);
       continue;
     }
     // ---- final group: u = X v for TR_NL leaves (needs every ancestor's S: the root's done)
@@ -88,5 +113,6 @@ k_step(const StepArgs sa) {
     const int i0 = (int)(lu0 / nleaf), i1 = (int)((lu0 + nl - 1) / nleaf);
     for (int inst = i0; inst <= i1; ++inst) st_wait(sa.done + sa.dofs[0] + inst, a.rc[0]);
     tr_final(a, smem, (int)lu0, nl);
+    rec(200);
   }
 }
