@@ -208,7 +208,7 @@ def measure_cfg4(dev, world, rank, steps=16):
     timed region.  Returns instance-steps/s over all ranks (max-over-ranks time)."""
     import torch
     from paper_1804_05522_b200 import workloads as W
-    from paper_1804_05522_b200.hodlr import Fde1dStepper
+    from paper_1804_05522_b200.hodlr import Fde1dStepper, FDE_NO_KEEP
     from paper_1804_05522_b200.shard import ShardedRun
     wl = W.cfg4()
     run = ShardedRun(wl.batch, world, rank)
@@ -228,7 +228,9 @@ def measure_cfg4(dev, world, rank, steps=16):
         torch.cuda.synchronize()
         a.record()
         for k in range(steps):
-            st.step(wl.dt, DP, DM, F, u[k % 2], u_next=u[(k + 1) % 2], coeffs_changed=refactor)
+            # refactor: the fused factor + solve step (k_step, FDE_NO_KEEP) every step
+            st.step(wl.dt, DP, DM, F, u[k % 2], u_next=u[(k + 1) % 2], coeffs_changed=refactor,
+                    flags=FDE_NO_KEEP if refactor else 0)
         b.record()
         torch.cuda.synchronize()
         ms = a.elapsed_time(b)

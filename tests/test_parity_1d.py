@@ -277,3 +277,19 @@ def test_cfg4_sampled_instances():
         be = backward_error(float(wl.alpha[b]), wl.h, wl.dt, dp[b], dm[b], ug[b], wl.dt * f[b])
         assert be["eta"] <= 1e-12, (b, be)
     st.close()
+
+
+@gpu
+def test_batched_fused_step_matches_oracle():
+    """Batched instances through the fused k_step path (FDE_NO_KEEP): each instance vs dense."""
+    n, batch = 1500, 6
+    wl = W.make_1d(n, np.linspace(1.15, 1.85, batch), 100, 1e-12, K=2, batch=batch)
+    st = _stepper(wl)
+    u = wl.u0
+    for m in (1, 2):
+        ug = _gpu_step(st, wl, m, u, flags=NO_KEEP)
+        for b in range(batch):
+            uo = _oracle_step(wl, m, u, b)
+            assert _rel(ug[b], uo) <= 1e-8, (m, b, _rel(ug[b], uo))
+        u = ug
+    st.close()
