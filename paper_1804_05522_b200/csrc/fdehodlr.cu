@@ -476,6 +476,8 @@ static void print_leaf_trace(unsigned long long* d_trace) {
     t0 = std::min(t0, lt[l * 8]);
     t1 = std::max(t1, lt[l * 8 + 4]);
   }
+  fprintf(stderr, "k_leaf build cycles leaf0: warp0 staging %llu build %llu gj0 %llu | warp4 staging %llu build %llu\n",
+          h[980], h[981], h[982], h[984], h[985]);
   fprintf(stderr, "k_leaf LU cycles CTA0: gj0 %llu ovw %llu diagupd %llu gj||trail %llu\n", h[960], h[961], h[962], h[963]);
   fprintf(stderr, "k_leaf panel cycles CTA0 warp0: gen %llu ld %llu solve %llu store %llu\n", h[970], h[971], h[972], h[973]);
   if (cnt)

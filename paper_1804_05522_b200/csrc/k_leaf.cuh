@@ -236,13 +236,15 @@ __device__ __noinline__ void quad_gj_inv32(double* D, int ld, double* buf, DevSt
 // With lookahead: the next diagonal block is updated first and inverted by warps 0..3 while
 // warps 4..7 finish the trailing update (three CTA barriers per block column).
 __device__ void leaf_block_lu(double* A, int sp, double* prow, DevStatus* st, int where,
-                              unsigned long long* trace = nullptr) {
+                              unsigned long long* trace = nullptr, bool gj0_done = false) {
   const int nb = sp >> 5, warp = threadIdx.x >> 5;
   const bool tr = trace && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0;
   long long tl = clock64();
 #define LUT(i) do { if (tr) { const long long t_ = clock64(); trace[960 + (i)] += t_ - tl; tl = t_; } } while (0)
-  if (warp < GJ_WARPS) quad_gj_inv32(A, LDA_LEAF, prow, st, where);
-  __syncthreads();
+  if (!gj0_done) {
+    if (warp < GJ_WARPS) quad_gj_inv32(A, LDA_LEAF, prow, st, where);
+    __syncthreads();
+  }
   LUT(0);
   for (int kb = 0; kb < nb; ++kb) {
     const int k0 = kb * 32;
@@ -475,14 +477,20 @@ __device__ __forceinline__ void leaf_task(const LeafArgs& a, double* smem, int l
   };
   stamp(0);
 
+  const long long bclk = clock64();
   if (a.mode == 0) {
     // ---- S3: generate the leaf block from g and d+- (column-major), identity padding
     const double c = a.cfac[inst];
     const double* gi = a.g + (long long)inst * a.gstride;
     const double* dpi = a.dp + (long long)inst * n + r0;
     const double* dmi = a.dm + (long long)inst * n + r0;
-    double* gs = S;                                  // g_0 .. g_sp staged (S is free scratch)
-    for (int k = t; k <= sp; k += LEAF_THREADS) gs[k] = (k <= n + 1) ? gi[k] : 0.0;
+    // Toeplitz entries by offset: tt[d + sp] = T[i, j] for d = i - j (-g_{d+1} for d >= -1,
+    // else 0), d in [-sp, sp] (S is free scratch; 2 sp + 1 <= 257 doubles)
+    double* tt = S;
+    for (int e = t; e <= 2 * sp; e += LEAF_THREADS) {
+      const int d = e - sp;
+      tt[e] = (d >= -1 && d + 1 <= n + 1) ? -gi[d + 1] : 0.0;
+    }
     for (int i = t; i < s; i += LEAF_THREADS) {
       dps[i] = dpi[i]; dms[i] = dmi[i];
       if (a.nf) bs[i] = a.u_prev[(long long)inst * n + r0 + i] + a.dt * a.f[(long long)inst * n + r0 + i];
@@ -492,6 +500,9 @@ __device__ __forceinline__ void leaf_task(const LeafArgs& a, double* smem, int l
       for (int cc = t; cc < ce - cb; cc += LEAF_THREADS) pcd[cc] = panel_col(a, inst, leaf, r0, cb + cc, ce);
     }
     __syncthreads();
+    const bool btr = a.trace && leaf == 0 && inst == 0 && (t == 0 || t == 128);
+    long long bt0 = clock64();
+    if (btr) a.trace[980 + (t >> 7) * 4] = bt0 - bclk;
     {
       // lane owns rows lane + 32u (their d+- in registers); 4 independent elements per column
       double dpr[LEAF_MAX / 32], dmr[LEAF_MAX / 32];
@@ -501,29 +512,34 @@ __device__ __forceinline__ void leaf_task(const LeafArgs& a, double* smem, int l
         dpr[u] = i < s ? dps[i] : 0.0;
         dmr[u] = i < s ? dms[i] : 0.0;
       }
-      for (int j = warp; j < sp; j += LEAF_WARPS) {
+      // warps 0..3 build block column 0 first and invert its diagonal block (quad GJ) while
+      // warps 4..7 build the remaining columns (the first pivot chain overlaps the build)
+      const int jlo = warp < GJ_WARPS ? 8 * warp : 32 + (warp - GJ_WARPS);
+      const int jhi = warp < GJ_WARPS ? min(8 * warp + 8, sp) : sp;
+      const int jst = warp < GJ_WARPS ? 1 : LEAF_WARPS - GJ_WARPS;
+      for (int j = jlo; j < jhi; j += jst) {
 #pragma unroll
         for (int u = 0; u < LEAF_MAX / 32; ++u) {
           const int i = lane + 32 * u;
           if (i < sp) {
-            double v;
-            if (i < s && j < s) {
-              const int k1 = i - j + 1, k2 = j - i + 1;   // T[i,j] = -g_{i-j+1}, T^T[i,j] = T[j,i]
-              const double tij = (k1 >= 0) ? -gs[k1] : 0.0;
-              const double tji = (k2 >= 0) ? -gs[k2] : 0.0;
-              v = (i == j ? a.shift : 0.0) + c * (dpr[u] * tij + dmr[u] * tji);
-            } else {
-              v = (i == j) ? 1.0 : 0.0;
-            }
+            const double tij = tt[i - j + sp], tji = tt[j - i + sp];   // T[i,j], T^T[i,j] = T[j,i]
+            const double v = (i < s && j < s) ? fma(c, fma(dpr[u], tij, dmr[u] * tji), i == j ? a.shift : 0.0)
+                                              : (i == j ? 1.0 : 0.0);
             A[i + j * LDA_LEAF] = v;
           }
         }
       }
+      if (btr) { const long long t_ = clock64(); a.trace[981 + (t >> 7) * 4] = t_ - bt0; bt0 = t_; }
+      if (warp < GJ_WARPS) {
+        asm volatile("bar.sync 1, %0;" ::"n"(GJ_WARPS * 32) : "memory");
+        quad_gj_inv32(A, LDA_LEAF, S + 272, a.st, where);    // (S + 272: clear of the staged tt)
+        if (btr) { const long long t_ = clock64(); a.trace[982] = t_ - bt0; }
+      }
     }
     __syncthreads();
     stamp(1);
-    // ---- S4: block LU (inverse-diagonal form, off-diagonal blocks negated)
-    leaf_block_lu(A, sp, S, a.st, where, a.trace);
+    // ---- S4: block LU (inverse-diagonal form, off-diagonal blocks negated); block 0 done
+    leaf_block_lu(A, sp, S + 272, a.st, where, a.trace, true);
     stamp(2);
     // ---- panel X = A_leaf^{-1} [b | U_0 .. U_{L-1}] by warp stripes of 8 columns
     const int c_begin = 1 - a.nf, c_end = a.xcol[tr.L];
