@@ -126,6 +126,19 @@ int fde1d_step(int batch, int n, const double* alpha, double h, double dt,
                const double* u_prev, double* u_next, double tol, int leaf,
                int coeffs_changed, unsigned flags, fde_hodlr_t* cache, void* stream);
 
+/* K implicit-Euler steps of Eq. (2.5) in one pipelined launch (fused factor + solve every step,
+ * P:1310-1315):  u^(m) = A_m^{-1}(u^(m-1) + dt f^(m)),  m = 1..K.  The coefficient-dependent
+ * leaf work of step m+1 (LU, U columns of the panel, their projection) overlaps the tree levels
+ * of step m; only the rhs column waits for u^(m).  Same arithmetic as fde1d_step.
+ *   d_plus, d_minus [dev]: step m at d_plus + m * coef_stride (batch*n each; coef_stride = 0:
+ *   the same coefficients every step); f [dev] likewise with f_stride; u0 [dev, batch*n];
+ *   u_out [dev, K * batch*n] receives every step's solution (step m at u_out + m*batch*n).
+ *   `cache`, alpha, h, tol, leaf, stream as in fde1d_step.  Asynchronous unless FDE_SYNC. */
+int fde1d_run(int batch, int n, const double* alpha, double h, double dt, int K,
+              const double* d_plus, const double* d_minus, long long coef_stride,
+              const double* f, long long f_stride, const double* u0, double* u_out,
+              double tol, int leaf, unsigned flags, fde_hodlr_t* cache, void* stream);
+
 /* One step of the 2D scheme as a Sylvester equation (Eq. 4.3, reading R11):
  *     A1 X + X A2^T = Uu Uv^T + dt Fu Fv^T,
  *     A1 = 1/2 I + (dt/hx^alpha1)(D1+ T1 + D1- T1^T),  A2 likewise in y,

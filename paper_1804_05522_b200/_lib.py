@@ -27,6 +27,8 @@ SIGNATURES = {
     "hodlr_ranks": (_i, [_p, _i, _pi, _i, _pi]),
     "hodlr_destroy": (None, [_p]),
     "fde1d_step": (_i, [_i, _i, _pd, _d, _d, _p, _p, _p, _p, _p, _d, _i, _i, _u, _ph, _p]),
+    "fde1d_run": (_i, [_i, _i, _pd, _d, _d, _i, _p, _p, ctypes.c_longlong, _p, ctypes.c_longlong, _p, _p,
+                       _d, _i, _u, _ph, _p]),
     "fde2d_step": (_i, [_i, _i, _d, _d, _d, _d, _d, _p, _p, _p, _p, _p, _p, _i, _p, _p, _i,
                         _p, _p, _i, _pi, _d, _d, _i, _i, _ph, _pd, _pi, _u, _p]),
     "fde_last_error": (ctypes.c_char_p, []),

@@ -1,6 +1,7 @@
 // fdehodlr.cu -- host side of the C-ABI (include/fdehodlr.h): argument checking, tree
 // bookkeeping, workspace management and kernel orchestration on the caller's stream.
 // All arithmetic of the method runs in the kernels of k_*.cuh.
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
@@ -19,6 +20,7 @@
 #include "k_tree.cuh"
 #include "k_solve.cuh"
 #include "k_step.cuh"
+#include "k_run.cuh"
 
 // ---------------------------------------------------------------------------------------
 // errors, launch accounting
@@ -138,6 +140,10 @@ struct fde_hodlr {
   long long dofs[LMAX + 1] = {}, ndone = 0, lofs = 0;
   int step_grid = 0;
   size_t step_smem = 0;
+  // pipelined multi-step run (k_run.cuh): second buffer set and stored leaf LUs
+  double *d_X2 = nullptr, *d_Q2 = nullptr, *d_S2 = nullptr, *d_LUr[2] = {nullptr, nullptr};
+  int* d_runctr = nullptr;
+  long long runctr_cap = 0;
   int npost = 0;
   // compression scratch
   PcTask* d_tasks = nullptr;
@@ -1114,6 +1120,101 @@ int fde1d_step(int batch, int n, const double* alpha, double h, double dt, const
   if (flags & FDE_HOST_PTRS) CU(cudaMemcpyAsync(u_next, un, bytes, cudaMemcpyDeviceToHost, s));
   H->last_stream = s;
   if ((flags & FDE_SYNC) || !cache || (flags & FDE_HOST_PTRS)) rc = sync_and_status(H, s);
+  if (!cache) hodlr_destroy(H);
+  return rc;
+}
+
+int fde1d_run(int batch, int n, const double* alpha, double h, double dt, int K, const double* d_plus,
+              const double* d_minus, long long coef_stride, const double* f, long long f_stride,
+              const double* u0, double* u_out, double tol, int leaf, unsigned flags, fde_hodlr_t* cache,
+              void* stream) {
+  g_last_error.clear();
+  TRY(check_common(batch, n, alpha, h, dt, tol, leaf));
+  if (K < 1) return set_err(FDE_EDOMAIN, "K=%d must be >= 1", K);
+  if (!d_plus || !d_minus || !f || !u0 || !u_out) return set_err(FDE_EDOMAIN, "NULL array argument");
+  if (coef_stride < 0 || f_stride < 0) return set_err(FDE_EDOMAIN, "negative stride");
+  cudaStream_t s = (cudaStream_t)stream;
+  fde_hodlr* H = cache ? *cache : nullptr;
+  if (H) {
+    bool same = H->batch == batch && H->n == n && H->h == h && H->leaf == leaf && H->tol == tol &&
+                H->shift == 1.0;
+    for (int b = 0; same && b < batch; ++b) same = H->alpha[b] == alpha[b];
+    if (!same) { hodlr_destroy(H); H = nullptr; if (cache) *cache = nullptr; }
+  }
+  if (!H) {
+    TRY(build_impl(batch, n, alpha, h, dt, nullptr, nullptr, 1.0, tol, leaf, 0, s, &H));
+    if (cache) *cache = H;
+  }
+  const size_t cnt = (size_t)batch * n;
+  int rc = FDE_OK;
+  if (!H->tree_ok || H->L < 1) {                  // no pipelined path: one fused step at a time
+    for (int m = 0; m < K && rc == FDE_OK; ++m)
+      rc = fde1d_step(batch, n, alpha, h, dt, d_plus + m * coef_stride, d_minus + m * coef_stride,
+                      f + m * f_stride, m == 0 ? u0 : u_out + (m - 1) * cnt, u_out + m * cnt, tol, leaf, 1,
+                      flags | FDE_NO_KEEP, &H, stream);
+    if (!cache) hodlr_destroy(H);
+    return rc;
+  }
+  if (H->dt != dt) TRY(set_dt(H, dt, s));
+  const int L = H->L, B = H->batch;
+  // second buffer set + stored leaf LUs (allocated once per handle)
+  if (!H->d_X2) {
+    TRY(dalloc(H, &H->d_X2, (size_t)B * H->xstride));
+    TRY(dalloc(H, &H->d_Q2, (size_t)B * H->qinst));
+    TRY(dalloc(H, &H->d_S2, (size_t)B * H->sinst));
+    TRY(dalloc(H, &H->d_LUr[0], (size_t)B * H->lustride));
+    TRY(dalloc(H, &H->d_LUr[1], (size_t)B * H->lustride));
+  }
+  // per-step counters: A flags [n_leaf], pair counters [B 2^(L-1)], finals [n_fin], levels
+  const long long n_leaf = (long long)B * H->nleaf, n_fin = (n_leaf + TR_NL - 1) / TR_NL;
+  RunArgs ra{};
+  long long o = 0;
+  ra.o_A = o; o += n_leaf;
+  ra.o_pair = o; o += (long long)B << (L - 1);
+  ra.o_fin = o; o += n_fin;
+  for (int m = 0; m < L; ++m) { ra.o_lvl[m] = o; o += (long long)B << m; }
+  ra.per_step = o;
+  const long long need = 1 + (long long)K * o;
+  if (need > H->runctr_cap) {
+    if (H->d_runctr) { cudaStreamSynchronize(s); cudaFree(H->d_runctr); H->allocs.erase(std::find(H->allocs.begin(), H->allocs.end(), (void*)H->d_runctr)); }
+    TRY(dalloc(H, &H->d_runctr, (size_t)need));
+    H->runctr_cap = need;
+  }
+  CU(cudaMemsetAsync(H->d_runctr, 0, need * sizeof(int), s));
+  ra.ctr = reinterpret_cast<unsigned*>(H->d_runctr);
+  ra.done = H->d_runctr + 1;
+  // leaf template
+  LeafArgs& la = ra.la;
+  la.tree = H->tree; la.mode = 0; la.shift = H->shift; la.cfac = H->d_cfac; la.dt = dt;
+  la.g = H->d_g; la.gstride = H->gstride;
+  la.Lf = H->d_Lf; la.lf_stride = H->lf_stride; la.rank = H->d_rank;
+  for (int l = 0; l < L; ++l) { la.kl[l] = H->kl[l]; la.xcol[l] = H->xcol[l]; }
+  la.xcol[L] = H->xcol[L];
+  la.xstride = H->xstride; la.lustride = H->lustride; la.keep = 0; la.st = H->d_status;
+  la.qinst = H->qinst; la.qstride = (long long)(H->xcol[L] - 1) * H->xcol[L];
+  la.trace = nullptr;
+  TrArgs& a = ra.ta;
+  a = H->tr_geo;
+  a.L = L; a.NC = H->xcol[L]; a.nleaf = H->nleaf; a.batch = B; a.kmaxc = H->kmax;
+  for (int l = 0; l <= L; ++l) a.xc[l] = H->xcol[l];
+  for (int m = 0; m < L; ++m) { a.rc[m] = H->trc[m]; a.slev[m] = H->slev[m]; }
+  for (int m = 1; m <= L; ++m) a.qlev[m] = H->qlev[m];
+  a.qinst = H->qinst; a.sinst = H->sinst;
+  a.n = H->n; a.xstride = H->xstride;
+  a.leaf_r0 = H->tree.leaf_r0; a.leaf_n = H->tree.leaf_n;
+  a.bar = H->d_bar; a.st = H->d_status; a.trace = nullptr;
+  ra.K = K;
+  ra.dp = d_plus; ra.dm = d_minus; ra.coef_stride = coef_stride; ra.f = f; ra.f_stride = f_stride;
+  ra.u0 = u0; ra.uout = u_out;
+  ra.X[0] = H->d_X; ra.X[1] = H->d_X2; ra.Q[0] = H->d_Q; ra.Q[1] = H->d_Q2;
+  ra.S[0] = H->d_S; ra.S[1] = H->d_S2; ra.LU[0] = H->d_LUr[0]; ra.LU[1] = H->d_LUr[1];
+  CU(cudaFuncSetAttribute(k_run, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)H->step_smem));
+  void* args[] = {&ra};
+  { PROF("k_run"); CU(cudaLaunchCooperativeKernel((void*)k_run, dim3(H->step_grid), dim3(TR_THREADS), args, H->step_smem, s)); }
+  LAUNCHED();
+  H->last_stream = s;
+  H->factored = false;
+  if ((flags & FDE_SYNC) || !cache) rc = sync_and_status(H, s);
   if (!cache) hodlr_destroy(H);
   return rc;
 }

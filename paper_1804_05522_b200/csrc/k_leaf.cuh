@@ -55,6 +55,7 @@ struct LeafArgs {
   const double* u_prev; const double* f;     // [batch*n], factor mode with nf = 1
   const double* b; double* y; int nrhs; int ld;   // solve mode
   double* Q; long long qstride, qinst;       // factor mode: Q_leaf = V_all^T X_leaf (or null)
+  int store_lu;                              // factor mode: write the LU (inverse-diagonal form)
   DevStatus* st;
   unsigned long long* trace;                 // optional phase clocks (FDE_TRACE_LEVELS)
 };
@@ -376,12 +377,12 @@ __device__ __forceinline__ PanelCol panel_col(const LeafArgs& a, int inst, int l
 // after all stripes: the LU + stripe buffers are reused for V (NV x 128 col-major) and
 // chunks of X re-read from L2.  DMMA tiles: warp unit = (m-tile, 2 n-tiles), A reused.
 __device__ void leaf_project(const LeafArgs& a, double* big, const PanelCol* pcd, int c_begin,
-                             int NC, int s, int sp, const double* Xi, double* Qo) {
+                             int NC, int s, int sp, const double* Xi, double* Qo, int c_lo = 0) {
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31, gid = lane >> 2, tig = lane & 3;
   const int n = a.tree.n, NV = NC - 1, NVP = round_up(NV, 8), MT = NVP >> 3;
   double* Vs = big;                                   // [NVP cols][LDA_LEAF]
   double* Xs = big + NVP * LDA_LEAF;
-  const int XCH = min(((LEAF_BIG - NVP * LDA_LEAF) / LDA_LEAF) & ~15, round_up(NC, 16));
+  const int XCH = min(((LEAF_BIG - NVP * LDA_LEAF) / LDA_LEAF) & ~15, round_up(NC - c_lo, 16));
   __syncthreads();                                    // every warp is done with the LU
   for (int j = warp; j < NVP; j += LEAF_WARPS) {
     const PanelCol pc = j < NV ? pcd[j + 1 - c_begin] : PanelCol{a.Lf, 0, 0, 0, 0, 0};
@@ -393,10 +394,10 @@ __device__ void leaf_project(const LeafArgs& a, double* big, const PanelCol* pcd
   }
   cp_async_commit();
   // balanced column chunks of whole n-tile pairs (16 columns), at most XCH wide
-  const int NPT = round_up(NC, 16) >> 4, maxp = XCH >> 4;
+  const int NPT = round_up(NC - c_lo, 16) >> 4, maxp = XCH >> 4;
   const int nchunk = (NPT + maxp - 1) / maxp;
   const int MP = (MT + 1) >> 1;                       // m-tile pairs
-  int c0 = 0;
+  int c0 = c_lo;                                      // (c_lo = 1: the rhs column is projected later)
   for (int ch = 0; ch < nchunk; ++ch) {
     const int npc = (NPT * (ch + 1)) / nchunk - (NPT * ch) / nchunk;   // n-pairs in this chunk
     const int ncp = 16 * npc;
@@ -540,6 +541,9 @@ __device__ __forceinline__ void leaf_task(const LeafArgs& a, double* smem, int l
     stamp(1);
     // ---- S4: block LU (inverse-diagonal form, off-diagonal blocks negated); block 0 done
     leaf_block_lu(A, sp, S + 272, a.st, where, a.trace, true);
+    if (a.store_lu)                                  // for the deferred rhs column (leaf_rhs_task)
+      for (int j = warp; j < sp; j += LEAF_WARPS)
+        for (int i = lane; i < sp; i += 32) LUg[i + j * sp] = A[i + j * LDA_LEAF];
     stamp(2);
     // ---- panel X = A_leaf^{-1} [b | U_0 .. U_{L-1}] by warp stripes of 8 columns
     const int c_begin = 1 - a.nf, c_end = a.xcol[tr.L];
@@ -697,5 +701,60 @@ __device__ __forceinline__ void leaf_proj_task(const LeafArgs& a, double* smem, 
     pcd[cc] = panel_col(a, inst, leaf, r0, c_begin + cc, c_end);
   const double* Xi = a.X + (long long)inst * a.xstride + r0;
   leaf_project(a, smem + LEAF_FRONT, pcd, c_begin, c_end, s, sp, Xi,
-               a.Q + (long long)inst * a.qinst + (long long)leaf * a.qstride);
+               a.Q + (long long)inst * a.qinst + (long long)leaf * a.qstride, c_begin);
+}
+
+// The deferred right-hand-side column of a leaf (k_run.cuh): x0 = A_leaf^{-1}(u + dt f) with the
+// stored LU (one stripe solve), X[:, 0] = x0, and its projection Q[:, 0] = V_all^T x0.
+__device__ __forceinline__ void leaf_rhs_task(const LeafArgs& a, double* smem, int leaf, int inst) {
+  double* bs = smem + 32 * 33 + 2 * LEAF_MAX;
+  PanelCol* pcd = reinterpret_cast<PanelCol*>(bs + LEAF_MAX);
+  double* A = smem + LEAF_FRONT;
+  const TreeDev& tr = a.tree;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31, gid = lane >> 2, tig = lane & 3;
+  const int n = tr.n, r0 = tr.leaf_r0[leaf], s = tr.leaf_n[leaf], sp = round_up(s, 32), nb = sp >> 5;
+  const int NC = a.xcol[tr.L];
+  const double* LUg = a.LU + (long long)inst * a.lustride + (long long)leaf * LEAF_SLOT;
+  double* Ys = A + LEAF_MAX * LDA_LEAF;             // warp 0's stripe buffer
+  for (int e = t; e < sp * sp; e += LEAF_THREADS) cp_async8(&A[(e % sp) + (e / sp) * LDA_LEAF], LUg + e);
+  cp_async_commit();
+  for (int cc = t; cc < NC - 1; cc += LEAF_THREADS) pcd[cc] = panel_col(a, inst, leaf, r0, 1 + cc, NC);
+  const double* u = a.u_prev + (long long)inst * n + r0;
+  const double* f = a.f + (long long)inst * n + r0;
+  for (int i = t; i < sp; i += LEAF_THREADS) bs[i] = i < s ? u[i] + a.dt * f[i] : 0.0;
+  cp_async_wait_all();
+  __syncthreads();
+  if (warp == 0) {
+    double acc[16][2];
+#pragma unroll
+    for (int tt = 0; tt < 16; ++tt) {
+      const int i = 8 * tt + gid;
+      acc[tt][0] = (tig == 0 && tt < 4 * nb) ? bs[i] : 0.0;
+      acc[tt][1] = 0.0;
+    }
+    stripe_solve(acc, A, nb, Ys);
+    if (tig == 0)
+#pragma unroll
+      for (int tt = 0; tt < 16; ++tt)
+        if (tt < 4 * nb) bs[8 * tt + gid] = acc[tt][0];
+    __syncwarp();
+    double* X0 = a.X + (long long)inst * a.xstride + r0;
+    for (int i = lane; i < s; i += 32) X0[i] = bs[i];
+  }
+  __syncthreads();
+  // Q[j][0] = V_all[:, j]^T x0 : warp per V column, lanes over rows (fixed-order reduction)
+  double* Qo = a.Q + (long long)inst * a.qinst + (long long)leaf * a.qstride;
+  for (int j = warp; j < NC - 1; j += LEAF_WARPS) {
+    const PanelCol pc = pcd[j];
+    double acc = 0.0;
+    for (int i = lane; i < s; i += 32) {
+      double v = 0.0;
+      if (pc.kind == 2) v = __ldg(pc.Lq + pc.li0 + pc.lstep * i);
+      else if (pc.kind == 3) v = (pc.li0 + pc.lstep * i == 0) ? 1.0 : 0.0;
+      acc = fma(v, bs[i], acc);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) Qo[(long long)j * NC] = acc;
+  }
 }

@@ -122,6 +122,27 @@ class Fde1dStepper:
                                      ctypes.byref(self._cache), _stream(stream)))
         return u_next
 
+    def run(self, dt, d_plus, d_minus, f, u0, u_out=None, flags=0, stream=None):
+        """K steps in one pipelined launch (fde1d_run).  d_plus, d_minus, f: CUDA float64
+        (K, batch, n) -- or (1, batch, n) for time-invariant data; u0 (batch, n).
+        Returns u_out (K, batch, n): every step's solution."""
+        cnt = self.batch * self.n
+        K = max(d_plus.shape[0], f.shape[0])
+        for name, t in (("d_plus", d_plus), ("d_minus", d_minus), ("f", f)):
+            if t.shape[0] not in (1, K) or t[0].numel() != cnt:
+                raise ValueError("%s must be (K or 1, batch, n)" % name)
+        cs = cnt if d_plus.shape[0] > 1 else 0
+        if d_minus.shape[0] != d_plus.shape[0]:
+            raise ValueError("d_plus and d_minus must have the same number of time levels")
+        fs = cnt if f.shape[0] > 1 else 0
+        if u_out is None:
+            u_out = torch.empty((K,) + tuple(u0.shape), dtype=torch.float64, device=u0.device)
+        check(_lib.load().fde1d_run(self.batch, self.n, self._ap, self.h, dt, K, _dev(d_plus, "d_plus"),
+                                    _dev(d_minus, "d_minus"), cs, _dev(f, "f"), fs, _dev(u0, "u0", cnt),
+                                    _dev(u_out, "u_out", K * cnt), self.tol, self.leaf, flags,
+                                    ctypes.byref(self._cache), _stream(stream)))
+        return u_out
+
     def ranks(self, inst=0):
         buf = (ctypes.c_int * 64)()
         levels = ctypes.c_int()

@@ -293,3 +293,47 @@ def test_batched_fused_step_matches_oracle():
             assert _rel(ug[b], uo) <= 1e-8, (m, b, _rel(ug[b], uo))
         u = ug
     st.close()
+
+
+@gpu
+@pytest.mark.parametrize("n,alpha,leaf,batch", [(2000, 1.6, 100, 1), (1500, 1.3, 64, 3), (300, 1.9, 40, 2)])
+def test_pipelined_run_matches_steps_and_oracle(n, alpha, leaf, batch):
+    """fde1d_run (K steps in one pipelined launch) = K fused fde1d_step calls (to rounding) and
+    each step matches the dense oracle trajectory."""
+    wl = W.make_1d(n, np.linspace(alpha, min(alpha + 0.2, 2.0), batch), leaf, 1e-12, K=5, batch=batch)
+    st = _stepper(wl)
+    K = wl.K
+    DP = torch.stack([_t(wl.coeffs(m)[0]) for m in range(1, K + 1)])
+    DM = torch.stack([_t(wl.coeffs(m)[1]) for m in range(1, K + 1)])
+    F = torch.stack([_t(wl.source(m)) for m in range(1, K + 1)])
+    out = st.run(wl.dt, DP, DM, F, _t(wl.u0)).cpu().numpy()
+    torch.cuda.synchronize()
+    st2 = _stepper(wl)
+    u = wl.u0
+    uo = wl.u0
+    for m in range(1, K + 1):
+        u = _gpu_step(st2, wl, m, u, flags=NO_KEEP)
+        for b in range(batch):
+            assert _rel(out[m - 1, b], u[b]) <= 1e-12, (m, b, _rel(out[m - 1, b], u[b]))
+        uo = np.stack([_oracle_step(wl, m, uo, b) for b in range(batch)])
+        for b in range(batch):
+            assert _rel(out[m - 1, b], uo[b]) <= 1e-8
+    st.close(); st2.close()
+
+
+@gpu
+def test_cfg3_pipelined_run_backward_error():
+    """cfg3 at full size through fde1d_run (the launch bench.py times): eta <= 1e-10 per step."""
+    wl = W.cfg3(K=4)
+    st = _stepper(wl)
+    DP = torch.stack([_t(wl.coeffs(m)[0]) for m in range(1, 5)])
+    DM = torch.stack([_t(wl.coeffs(m)[1]) for m in range(1, 5)])
+    out = st.run(wl.dt, DP, DM, _t(wl.source(1))[None], _t(wl.u0)).cpu().numpy()
+    u = wl.u0[0]
+    for m in range(1, 5):
+        dp, dm = wl.coeffs(m)
+        b = u + wl.dt * wl.source(m)[0]
+        be = backward_error(float(wl.alpha[0]), wl.h, wl.dt, dp[0], dm[0], out[m - 1, 0], b)
+        assert be["eta"] <= 1e-10, (m, be)
+        u = out[m - 1, 0]
+    st.close()
