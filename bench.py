@@ -1,13 +1,15 @@
 """Benchmark: implicit-Euler HODLR time-steps/s on BASELINE.json's n = 65536 1D workload (cfg3).
 
-One "step" = one pass of the hot path over one time level, through the C-ABI
-fde1d_step with new d+-(x, t_m) every step: assembly of the diagonally scaled HODLR of A_m (S3),
-leaf LU + Sherman-Morrison-Woodbury factorisation (S4-S5), tree solve (S6, fused as an extra
-right-hand-side column) and rhs formation u + dt f (S7).  The GL weights (S1) and the
-compression of T_alpha (S2) depend on (alpha, n, leaf, tol) only -- T is the same matrix at
-every step and the paper builds A_m's HODLR from it by diagonal scaling and shift
- -- so by default they run once when the handle is built; --recompress puts
-S1 + S2 inside every timed step.  Both variants are always measured and reported.
+One "step" = one pass of the hot path over one time level with new
+d+-(x, t_m) every step: assembly of the diagonally scaled HODLR of A_m (S3), leaf LU +
+Sherman-Morrison-Woodbury factorisation (S4-S5), tree solve (S6, fused as an extra right-hand-
+side column) and rhs formation u + dt f (S7).  The headline times `--steps` consecutive time
+levels through the C-ABI fde1d_run: ONE persistent launch (k_run) in which the leaf work of
+step m+1 (which does not depend on u^(m)) runs under the latency-bound tree levels of step m.
+The GL weights (S1) and the compression of T_alpha (S2) depend on (alpha, n, leaf, tol) only
+-- T is the same matrix at every step and the paper builds A_m's HODLR from it by diagonal
+scaling and shift -- so they run once when the handle is built.  Also reported
+(other_variant): one fde1d_step launch per time level, and that with S1 + S2 in every step.
 
 Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 Multi-GPU (torchrun, one rank per GPU): the single-problem path does not shard (DESIGN.md,
@@ -37,8 +39,6 @@ def parse():
     p.add_argument("--steps", type=int, default=64)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--recompress", action="store_true",
-                   help="recompute S1 (GL weights) + S2 (compression of T) inside every timed step")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-extra", action="store_true",
@@ -131,6 +131,8 @@ def algorithmic_work(ranks, n, leaf_sizes, nf=1):
     work["k_tree"] = (ft, bt)
     # k_step = k_leaf + k_tree fused in one persistent dataflow launch (the default path)
     work["k_step"] = (fl + ft, by + bt)
+    # k_run = k_step per time level, K levels pipelined in one launch (per-step figures)
+    work["k_run"] = work["k_step"]
     Wl = [sum(ks[:l]) for l in range(L)]
     fl_l = sum(2.0 * n * k * (nf + w + k) + 2.0 * n * k * (nf + w) for k, w in zip(ks, Wl))
     by_l = sum(8.0 * n * (nf + w + k) + 8.0 * n * (nf + w) for k, w in zip(ks, Wl))
@@ -286,7 +288,7 @@ def run_ours(args, world, rank, local):
     from paper_1804_05522_b200 import workloads as W
     from paper_1804_05522_b200 import _lib
     from paper_1804_05522_b200.hodlr import (Fde1dStepper, launch_count, FDE_RECOMPRESS,
-                                             FDE_NO_KEEP, FDE_HOST_PTRS)
+                                             FDE_NO_KEEP)
     lib = _lib.load()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -299,61 +301,50 @@ def run_ours(args, world, rank, local):
             import torch.distributed as dist
             dist.barrier()
 
-    wl = W.cfg3(K=32)
+    # the timed trajectory: args.steps time levels of cfg3 (new d+-(x, t_m) every step)
+    wl = W.cfg3(K=max(args.steps, args.warmup, 1))
     n = wl.n
-    DP = torch.as_tensor(wl.d_plus[:, 0, :], device=dev).contiguous()
-    DM = torch.as_tensor(wl.d_minus[:, 0, :], device=dev).contiguous()
-    F = torch.as_tensor(wl.f[0, 0, :], device=dev).contiguous()
-    bufs = [torch.zeros(n, dtype=torch.float64, device=dev) for _ in range(2)]
+    DPK = torch.as_tensor(wl.d_plus, device=dev).contiguous()        # (K, 1, n)
+    DMK = torch.as_tensor(wl.d_minus, device=dev).contiguous()
+    F = torch.as_tensor(wl.f[0:1], device=dev).contiguous()           # (1, 1, n): time-invariant
+    U0 = torch.as_tensor(wl.u0, device=dev).contiguous()              # (1, n)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
     st = Fde1dStepper(n, wl.alpha, wl.h, wl.tol, wl.leaf)
-    flags = FDE_NO_KEEP | (FDE_RECOMPRESS if args.recompress else 0)
-    state = {"i": 0}
+    evs = lambda: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
 
-    def one_step():
-        i = state["i"]
-        m = i % wl.K
-        u_prev, u_next = bufs[i % 2], bufs[(i + 1) % 2]
-        st.step(wl.dt, DP[m], DM[m], F, u_prev, u_next=u_next, coeffs_changed=True, flags=flags)
-        state["i"] = i + 1
-
-    one_step()                                   # build the handle (allocation, tree, plan)
-    torch.cuda.synchronize()
-    for _ in range(args.warmup):
+    def run(K, profile=False):
+        """One fde1d_run of K pipelined steps (one k_run launch); device time in ms."""
         flush.zero_()
-        one_step()
-    torch.cuda.synchronize()
-
-    def timed(K, profile=False):
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        a, b = evs()
         if profile:
             lib.fde_profile_enable(1)
         barrier()
         torch.cuda.synchronize()
         l0 = launch_count()
-        for k in range(K):
-            flush.zero_()                        # L2 flush between timed steps (untimed)
-            evs[k][0].record()
-            one_step()
-            evs[k][1].record()
+        a.record()
+        out = st.run(wl.dt, DPK[:K], DMK[:K], F, U0)
+        b.record()
         torch.cuda.synchronize()
         l1 = launch_count()
         barrier()
-        ms = [a.elapsed_time(b) for a, b in evs]
         prof = None
         if profile:
             buf = __import__("ctypes").create_string_buffer(1 << 16)
             lib.fde_profile_dump(buf, 1 << 16)
             lib.fde_profile_enable(0)
             prof = json.loads(buf.value.decode())
-        return ms, l1 - l0, prof
+        return a.elapsed_time(b), l1 - l0, prof, out
+
+    run(args.steps)                               # build the handle, size the run buffers (K)
+    for _ in range(max(3, args.warmup)):          # warm-up: >= 3 untimed runs of the same K
+        run(args.steps)
+    torch.cuda.synchronize()
 
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
-    ms, launches, _ = timed(args.steps)
+    total_ms, launches, _, out = run(args.steps)
     clk = clocks.stop()
-    total_ms = sum(ms)
     if world > 1:
         import torch.distributed as dist
         t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
@@ -361,42 +352,73 @@ def run_ours(args, world, rank, local):
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
     value = world * args.steps / (total_ms / 1e3)
+    if not bool(torch.isfinite(out).all()):
+        raise RuntimeError("non-finite solution in the timed run")
 
-    # per-kernel durations (CUDA events around every launch, same steps again)
-    pms, _, prof = timed(args.steps, profile=True)
+    # per-kernel durations (CUDA events around the launch on its stream, same run again)
+    pms, _, prof, _ = run(args.steps, profile=True)
 
-    # the other variant: S1 + S2 inside every step (or cached, if --recompress is the headline)
-    flags_save = flags
-    flags = FDE_NO_KEEP | (0 if args.recompress else FDE_RECOMPRESS)
-    cms, _, _ = timed(args.steps)
-    flags = flags_save
-    other = {"value": world * args.steps / (sum(cms) / 1e3), "ms_per_step": sum(cms) / args.steps,
-             "what": "S1+S2 cached at build" if args.recompress else
-                     "S1 (GL weights) + S2 (compression of T) recomputed inside every step"}
+    # the per-step variant: one fused k_step launch per fde1d_step call, L2 flushed between
+    bufs = [torch.zeros(n, dtype=torch.float64, device=dev) for _ in range(2)]
 
-    # end to end through the C-ABI with HOST buffers (H2D of d+-, f, u_prev; D2H of u_next)
+    def per_step(K, flags):
+        ms = 0.0
+        for k in range(K):
+            flush.zero_()
+            a, b = evs()
+            a.record()
+            st.step(wl.dt, DPK[k % wl.K, 0], DMK[k % wl.K, 0], F[0, 0], bufs[k % 2],
+                    u_next=bufs[(k + 1) % 2], coeffs_changed=True, flags=flags)
+            b.record()
+            torch.cuda.synchronize()
+            ms += a.elapsed_time(b)
+        return ms
+    per_step(2, FDE_NO_KEEP)
+    vK = min(args.steps, 32)
+    ms_ps = per_step(vK, FDE_NO_KEEP)
+    ms_rc = per_step(max(1, vK // 4), FDE_NO_KEEP | FDE_RECOMPRESS)
+    other = {"per_step_launch": {"value": world * vK / (ms_ps / 1e3), "ms_per_step": ms_ps / vK,
+                                 "what": "fde1d_step per time level (one k_step launch each), "
+                                         "L2 flushed between steps"},
+             "per_step_recompress": {"value": world * max(1, vK // 4) / (ms_rc / 1e3),
+                                     "ms_per_step": ms_rc / max(1, vK // 4),
+                                     "what": "as per_step_launch plus S1 (GL weights) + S2 "
+                                             "(compression of T_alpha) inside every step"}}
+
+    # end to end through the public API: H2D of the K steps' d+-, f, u0 from pinned host memory,
+    # the pipelined run, D2H of every step's solution -- all inside the timed region
     e2e = None
     if not args.no_e2e:
         pin = lambda t: t.cpu().pin_memory()
-        hDP = [pin(DP[m]) for m in range(wl.K)]
-        hDM = [pin(DM[m]) for m in range(wl.K)]
-        hF = pin(F)
-        hu = [torch.zeros(n, dtype=torch.float64).pin_memory() for _ in range(2)]
-        st.step(wl.dt, hDP[0], hDM[0], hF, hu[0], u_next=hu[1], flags=flags | FDE_HOST_PTRS)
+        hDP, hDM, hF, hU0 = pin(DPK[:args.steps]), pin(DMK[:args.steps]), pin(F), pin(U0)
+        hout = torch.empty((args.steps, 1, n), dtype=torch.float64).pin_memory()
+        dDP, dDM, dF, dU0 = (torch.empty_like(x, device=dev) for x in (hDP, hDM, hF, hU0))
+        dout = torch.empty((args.steps, 1, n), dtype=torch.float64, device=dev)
+
+        def e2e_once():
+            dDP.copy_(hDP, non_blocking=True)
+            dDM.copy_(hDM, non_blocking=True)
+            dF.copy_(hF, non_blocking=True)
+            dU0.copy_(hU0, non_blocking=True)
+            st.run(wl.dt, dDP, dDM, dF, dU0, u_out=dout)
+            hout.copy_(dout, non_blocking=True)
+            torch.cuda.synchronize()
+        e2e_once()
+        flush.zero_()
         barrier()
+        torch.cuda.synchronize()
         t0 = time.perf_counter()
-        for k in range(args.steps):
-            m = k % wl.K
-            st.step(wl.dt, hDP[m], hDM[m], hF, hu[k % 2], u_next=hu[(k + 1) % 2],
-                    flags=flags | FDE_HOST_PTRS)          # synchronous: ends with the D2H copy
+        e2e_once()
         el = time.perf_counter() - t0
         if world > 1:
             import torch.distributed as dist
             t = torch.tensor([el], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
+        h2d = sum(x.numel() * 8 for x in (hDP, hDM, hF, hU0))
         e2e = {"value": world * args.steps / el, "unit": "time-steps/s",
-               "h2d_bytes_per_step": 4 * n * 8, "d2h_bytes_per_step": n * 8}
+               "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": n * 8,
+               "timing": "host wall clock, synchronize on both sides, max over ranks"}
 
     ranks = st.ranks()
     leaves = [wl.leaf] * (n // wl.leaf)
@@ -412,35 +434,39 @@ def run_ours(args, world, rank, local):
         t_s = kern[dom]["ms_per_step"] / 1e3
         launches_dom = kern[dom]["launches_per_step"]
         fl, by = work.get(dom, (0.0, 0.0))
-        if dom in ("k_leaf", "k_levels", "k_tree", "k_step"):
+        if dom in ("k_leaf", "k_levels", "k_tree", "k_step", "k_run"):
             # FP64 contractions on the DMMA (FP64 tensor) path; MEASURED_PEAKS has no FP64
             # entry: peak = tools/fp64_peak.cu measurement (profiles/fp64_peak_r01.json),
             # equal to the derived 148 SMs x 64 FMA/clk x 2 x 1.965 GHz = 37.2 TFLOP/s
             roof = {"bound": "tensor", "achieved": fl / t_s / 1e12, "peak": FP64_TENSOR_TFLOPS,
                     "unit": "TFLOP/s", "frac": fl / t_s / 1e12 / FP64_TENSOR_TFLOPS,
                     "traffic": traffic.get(dom), "kernel": dom,
-                    "flops_per_launch": fl / max(1.0, launches_dom),
+                    "flops_per_launch": fl / launches_dom,
                     "achieved_hbm_gbs": by / t_s / 1e9,
                     "peak_source": "measured DMMA m8n8k4 f64 (tools/fp64_peak.cu): 37.05 TFLOP/s"}
         else:
             roof = {"bound": "hbm", "achieved": by / t_s / 1e9, "peak": peaks.get("hbm_gbs"),
                     "unit": "GB/s", "frac": by / t_s / 1e9 / peaks.get("hbm_gbs", 6549.1),
                     "traffic": traffic.get(dom), "kernel": dom,
-                    "bytes_per_launch": by / max(1.0, launches_dom),
+                    "bytes_per_launch": by / launches_dom,
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)"}
-        roof["share_of_step"] = kern[dom]["ms_per_step"] / (sum(pms) / args.steps)
+        roof["share_of_step"] = kern[dom]["ms_per_step"] / (pms / args.steps)
 
     line = {"metric": METRIC, "value": value, "unit": "time-steps/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": "cfg3: 1D FDE n=65536 alpha=1.8 leaf 128 tol 1e-10, d+-(x,t) per "
-                                   "BASELINE configs[2], refactor every step",
+                                   "BASELINE configs[2], new d+-(x,t_m) and refactor every step, "
+                                   "K = steps time levels pipelined in one fde1d_run",
                        "n": n, "leaf": wl.leaf, "tol": wl.tol, "ranks": ranks,
                        "parallelism": "replicas" if world > 1 else "single",
-                       "l2": "flushed between timed steps (512 MiB write, untimed)",
-                       "step": ("S1-S7 every step" if args.recompress else
-                                "S3-S7 every step; S1-S2 (T_alpha compression) once per handle")},
+                       "l2": "flushed (512 MiB write) before the timed launch; inside it every "
+                             "step's working set (panel X %.0f MB + stored leaf LU %.0f MB + "
+                             "d+-, u) exceeds the 126 MB L2" % (8e-6 * n * (sum(ranks) + len(ranks) + 1),
+                                                                 8e-6 * n * wl.leaf),
+                       "step": "S3-S7 every step; S1-S2 (T_alpha compression) once per handle "
+                               "(other_variant.per_step_recompress puts them in every step)"},
             "gpu_launches": launches,
             "clocks": clk, "e2e": e2e, "roofline": roof, "kernels": kern,
             "other_variant": other}

@@ -129,11 +129,17 @@ int fde1d_step(int batch, int n, const double* alpha, double h, double dt,
 /* K implicit-Euler steps of Eq. (2.5) in one pipelined launch (fused factor + solve every step,
  * P:1310-1315):  u^(m) = A_m^{-1}(u^(m-1) + dt f^(m)),  m = 1..K.  The coefficient-dependent
  * leaf work of step m+1 (LU, U columns of the panel, their projection) overlaps the tree levels
- * of step m; only the rhs column waits for u^(m).  Same arithmetic as fde1d_step.
+ * of step m; only the rhs column waits for u^(m).  Same factorisation as fde1d_step; the rhs
+ * column's leaf solve uses the stored LU (results agree with fde1d_step to rounding).
  *   d_plus, d_minus [dev]: step m at d_plus + m * coef_stride (batch*n each; coef_stride = 0:
  *   the same coefficients every step); f [dev] likewise with f_stride; u0 [dev, batch*n];
- *   u_out [dev, K * batch*n] receives every step's solution (step m at u_out + m*batch*n).
- *   `cache`, alpha, h, tol, leaf, stream as in fde1d_step.  Asynchronous unless FDE_SYNC. */
+ *   u_out [dev, K * batch*n] receives every step's solution (step m at u_out + m*batch*n);
+ *   u_out must not alias u0 or the coefficient arrays.
+ *   `cache`, alpha, h, tol, leaf, stream as in fde1d_step.  Asynchronous unless FDE_SYNC.
+ * The handle owns a second panel/projection buffer set, two stored leaf LUs and per-step
+ * counters sized for K: the first call (and any call with a larger K) allocates them, which
+ * synchronises the stream.  Without the tree path (L = 0 or a panel too wide for it) the call
+ * falls back to K fde1d_step calls on the device. */
 int fde1d_run(int batch, int n, const double* alpha, double h, double dt, int K,
               const double* d_plus, const double* d_minus, long long coef_stride,
               const double* f, long long f_stride, const double* u0, double* u_out,

@@ -144,6 +144,12 @@ struct fde_hodlr {
   double *d_X2 = nullptr, *d_Q2 = nullptr, *d_S2 = nullptr, *d_LUr[2] = {nullptr, nullptr};
   int* d_runctr = nullptr;
   long long runctr_cap = 0;
+  unsigned long long* d_runrq = nullptr;
+  long long runrq_cap = 0;
+  std::vector<LeafArgs> run_las;
+  std::vector<TrArgs> run_tas;
+  void* d_run_args = nullptr;
+  size_t run_args_cap = 0;
   int npost = 0;
   // compression scratch
   PcTask* d_tasks = nullptr;
@@ -1165,26 +1171,40 @@ int fde1d_run(int batch, int n, const double* alpha, double h, double dt, int K,
     TRY(dalloc(H, &H->d_LUr[0], (size_t)B * H->lustride));
     TRY(dalloc(H, &H->d_LUr[1], (size_t)B * H->lustride));
   }
-  // per-step counters: A flags [n_leaf], pair counters [B 2^(L-1)], finals [n_fin], levels
-  const long long n_leaf = (long long)B * H->nleaf, n_fin = (n_leaf + TR_NL - 1) / TR_NL;
+  // per-step counters: A done [n_leaf], B' done [n_leaf], pair counters [B 2^(L-1)], per
+  // level m: chunk completions [B 2^m] and completed children [B 2^m]; ready queue: one slot
+  // per tree unit of the run
+  const long long n_leaf = (long long)B * H->nleaf;
   RunArgs ra{};
-  long long o = 0;
+  long long o = 0, units = 0;
   ra.o_A = o; o += n_leaf;
+  ra.o_R = o; o += n_leaf;
   ra.o_pair = o; o += (long long)B << (L - 1);
-  ra.o_fin = o; o += n_fin;
-  for (int m = 0; m < L; ++m) { ra.o_lvl[m] = o; o += (long long)B << m; }
+  for (int m = 0; m < L; ++m) {
+    ra.o_lvl[m] = o; o += (long long)B << m;
+    ra.o_kid[m] = o; o += (long long)B << m;
+    units += ((long long)B << m) * H->trc[m];
+  }
   ra.per_step = o;
-  const long long need = 1 + (long long)K * o;
+  const long long need = 4 + (long long)K * o;
   if (need > H->runctr_cap) {
     if (H->d_runctr) { cudaStreamSynchronize(s); cudaFree(H->d_runctr); H->allocs.erase(std::find(H->allocs.begin(), H->allocs.end(), (void*)H->d_runctr)); }
     TRY(dalloc(H, &H->d_runctr, (size_t)need));
     H->runctr_cap = need;
   }
+  const long long nrq = (long long)K * units;
+  if (nrq > H->runrq_cap) {
+    if (H->d_runrq) { cudaStreamSynchronize(s); cudaFree(H->d_runrq); H->allocs.erase(std::find(H->allocs.begin(), H->allocs.end(), (void*)H->d_runrq)); }
+    TRY(dalloc(H, &H->d_runrq, (size_t)nrq));
+    H->runrq_cap = nrq;
+  }
   CU(cudaMemsetAsync(H->d_runctr, 0, need * sizeof(int), s));
-  ra.ctr = reinterpret_cast<unsigned*>(H->d_runctr);
-  ra.done = H->d_runctr + 1;
-  // leaf template
-  LeafArgs& la = ra.la;
+  CU(cudaMemsetAsync(H->d_runrq, 0, nrq * sizeof(unsigned long long), s));
+  ra.heads = reinterpret_cast<unsigned*>(H->d_runctr);
+  ra.done = H->d_runctr + 4;
+  ra.rq = H->d_runrq;
+  // per-step argument blocks (k_run.cuh RunArgs), copied to the device once per call
+  LeafArgs la{};
   la.tree = H->tree; la.mode = 0; la.shift = H->shift; la.cfac = H->d_cfac; la.dt = dt;
   la.g = H->d_g; la.gstride = H->gstride;
   la.Lf = H->d_Lf; la.lf_stride = H->lf_stride; la.rank = H->d_rank;
@@ -1192,9 +1212,8 @@ int fde1d_run(int batch, int n, const double* alpha, double h, double dt, int K,
   la.xcol[L] = H->xcol[L];
   la.xstride = H->xstride; la.lustride = H->lustride; la.keep = 0; la.st = H->d_status;
   la.qinst = H->qinst; la.qstride = (long long)(H->xcol[L] - 1) * H->xcol[L];
-  la.trace = nullptr;
-  TrArgs& a = ra.ta;
-  a = H->tr_geo;
+  la.trace = nullptr; la.nf = 0; la.store_lu = 1;
+  TrArgs a = H->tr_geo;
   a.L = L; a.NC = H->xcol[L]; a.nleaf = H->nleaf; a.batch = B; a.kmaxc = H->kmax;
   for (int l = 0; l <= L; ++l) a.xc[l] = H->xcol[l];
   for (int m = 0; m < L; ++m) { a.rc[m] = H->trc[m]; a.slev[m] = H->slev[m]; }
@@ -1203,15 +1222,62 @@ int fde1d_run(int batch, int n, const double* alpha, double h, double dt, int K,
   a.n = H->n; a.xstride = H->xstride;
   a.leaf_r0 = H->tree.leaf_r0; a.leaf_n = H->tree.leaf_n;
   a.bar = H->d_bar; a.st = H->d_status; a.trace = nullptr;
+  double* Xp[2] = {H->d_X, H->d_X2};
+  double* Qp[2] = {H->d_Q, H->d_Q2};
+  double* Sp[2] = {H->d_S, H->d_S2};
+  H->run_las.resize(K);
+  H->run_tas.resize(K);
+  for (int m = 0; m < K; ++m) {
+    const int p = m & 1;
+    LeafArgs& lm = H->run_las[m];
+    lm = la;
+    lm.dp = d_plus + m * coef_stride; lm.dm = d_minus + m * coef_stride; lm.f = f + m * f_stride;
+    lm.u_prev = m == 0 ? u0 : u_out + (m - 1) * cnt;
+    lm.X = Xp[p]; lm.LU = H->d_LUr[p]; lm.Q = Qp[p] + H->qlev[L];
+    TrArgs& tm = H->run_tas[m];
+    tm = a;
+    tm.Q = Qp[p]; tm.Qleaf = Qp[p] + H->qlev[L]; tm.Sst = Sp[p]; tm.X = Xp[p];
+    tm.u = u_out + m * cnt;
+  }
+  const size_t args_bytes = (size_t)K * (sizeof(LeafArgs) + sizeof(TrArgs));
+  if (args_bytes > H->run_args_cap) {
+    if (H->d_run_args) { cudaStreamSynchronize(s); cudaFree(H->d_run_args); H->allocs.erase(std::find(H->allocs.begin(), H->allocs.end(), H->d_run_args)); }
+    H->d_run_args = nullptr;
+    CU(cudaMalloc(&H->d_run_args, args_bytes));
+    H->allocs.push_back(H->d_run_args);
+    H->run_args_cap = args_bytes;
+  }
+  // (host blocks are owned by the handle: they stay valid while the asynchronous copy reads them)
+  CU(cudaMemcpyAsync(H->d_run_args, H->run_las.data(), K * sizeof(LeafArgs), cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync((char*)H->d_run_args + K * sizeof(LeafArgs), H->run_tas.data(), K * sizeof(TrArgs),
+                     cudaMemcpyHostToDevice, s));
+  ra.las = reinterpret_cast<const LeafArgs*>(H->d_run_args);
+  ra.tas = reinterpret_cast<const TrArgs*>((char*)H->d_run_args + K * sizeof(LeafArgs));
   ra.K = K;
-  ra.dp = d_plus; ra.dm = d_minus; ra.coef_stride = coef_stride; ra.f = f; ra.f_stride = f_stride;
-  ra.u0 = u0; ra.uout = u_out;
-  ra.X[0] = H->d_X; ra.X[1] = H->d_X2; ra.Q[0] = H->d_Q; ra.Q[1] = H->d_Q2;
-  ra.S[0] = H->d_S; ra.S[1] = H->d_S2; ra.LU[0] = H->d_LUr[0]; ra.LU[1] = H->d_LUr[1];
+  ra.smem_doubles = (int)(H->step_smem / sizeof(double));
   CU(cudaFuncSetAttribute(k_run, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)H->step_smem));
+  static unsigned long long* run_trace = nullptr;
+  const long long run_trace_len = 4 + 4 * 262144;
+  if (getenv("FDE_TRACE_RUN")) {
+    if (!run_trace) CU(cudaMalloc(&run_trace, run_trace_len * sizeof(unsigned long long)));
+    CU(cudaMemsetAsync(run_trace, 0, run_trace_len * sizeof(unsigned long long), s));
+    ra.trace = run_trace; ra.trace_cap = 262144;
+  }
   void* args[] = {&ra};
   { PROF("k_run"); CU(cudaLaunchCooperativeKernel((void*)k_run, dim3(H->step_grid), dim3(TR_THREADS), args, H->step_smem, s)); }
   LAUNCHED();
+  if (ra.trace) {                                 // FDE_TRACE_RUN=<file>: task timeline
+    std::vector<unsigned long long> h(run_trace_len);
+    CU(cudaStreamSynchronize(s));
+    CU(cudaMemcpy(h.data(), ra.trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    FILE* fo = fopen(getenv("FDE_TRACE_RUN"), "w");
+    if (fo) {
+      const long long ne = std::min<long long>((long long)h[0], ra.trace_cap);
+      for (long long e = 0; e < ne; ++e)
+        fprintf(fo, "%llu %llu %llu %llu\n", h[4 + 4 * e], h[5 + 4 * e], h[6 + 4 * e], h[7 + 4 * e]);
+      fclose(fo);
+    }
+  }
   H->last_stream = s;
   H->factored = false;
   if ((flags & FDE_SYNC) || !cache) rc = sync_and_status(H, s);

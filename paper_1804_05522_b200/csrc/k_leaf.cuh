@@ -703,58 +703,3 @@ __device__ __forceinline__ void leaf_proj_task(const LeafArgs& a, double* smem, 
   leaf_project(a, smem + LEAF_FRONT, pcd, c_begin, c_end, s, sp, Xi,
                a.Q + (long long)inst * a.qinst + (long long)leaf * a.qstride, c_begin);
 }
-
-// The deferred right-hand-side column of a leaf (k_run.cuh): x0 = A_leaf^{-1}(u + dt f) with the
-// stored LU (one stripe solve), X[:, 0] = x0, and its projection Q[:, 0] = V_all^T x0.
-__device__ __forceinline__ void leaf_rhs_task(const LeafArgs& a, double* smem, int leaf, int inst) {
-  double* bs = smem + 32 * 33 + 2 * LEAF_MAX;
-  PanelCol* pcd = reinterpret_cast<PanelCol*>(bs + LEAF_MAX);
-  double* A = smem + LEAF_FRONT;
-  const TreeDev& tr = a.tree;
-  const int t = threadIdx.x, warp = t >> 5, lane = t & 31, gid = lane >> 2, tig = lane & 3;
-  const int n = tr.n, r0 = tr.leaf_r0[leaf], s = tr.leaf_n[leaf], sp = round_up(s, 32), nb = sp >> 5;
-  const int NC = a.xcol[tr.L];
-  const double* LUg = a.LU + (long long)inst * a.lustride + (long long)leaf * LEAF_SLOT;
-  double* Ys = A + LEAF_MAX * LDA_LEAF;             // warp 0's stripe buffer
-  for (int e = t; e < sp * sp; e += LEAF_THREADS) cp_async8(&A[(e % sp) + (e / sp) * LDA_LEAF], LUg + e);
-  cp_async_commit();
-  for (int cc = t; cc < NC - 1; cc += LEAF_THREADS) pcd[cc] = panel_col(a, inst, leaf, r0, 1 + cc, NC);
-  const double* u = a.u_prev + (long long)inst * n + r0;
-  const double* f = a.f + (long long)inst * n + r0;
-  for (int i = t; i < sp; i += LEAF_THREADS) bs[i] = i < s ? u[i] + a.dt * f[i] : 0.0;
-  cp_async_wait_all();
-  __syncthreads();
-  if (warp == 0) {
-    double acc[16][2];
-#pragma unroll
-    for (int tt = 0; tt < 16; ++tt) {
-      const int i = 8 * tt + gid;
-      acc[tt][0] = (tig == 0 && tt < 4 * nb) ? bs[i] : 0.0;
-      acc[tt][1] = 0.0;
-    }
-    stripe_solve(acc, A, nb, Ys);
-    if (tig == 0)
-#pragma unroll
-      for (int tt = 0; tt < 16; ++tt)
-        if (tt < 4 * nb) bs[8 * tt + gid] = acc[tt][0];
-    __syncwarp();
-    double* X0 = a.X + (long long)inst * a.xstride + r0;
-    for (int i = lane; i < s; i += 32) X0[i] = bs[i];
-  }
-  __syncthreads();
-  // Q[j][0] = V_all[:, j]^T x0 : warp per V column, lanes over rows (fixed-order reduction)
-  double* Qo = a.Q + (long long)inst * a.qinst + (long long)leaf * a.qstride;
-  for (int j = warp; j < NC - 1; j += LEAF_WARPS) {
-    const PanelCol pc = pcd[j];
-    double acc = 0.0;
-    for (int i = lane; i < s; i += 32) {
-      double v = 0.0;
-      if (pc.kind == 2) v = __ldg(pc.Lq + pc.li0 + pc.lstep * i);
-      else if (pc.kind == 3) v = (pc.li0 + pc.lstep * i == 0) ? 1.0 : 0.0;
-      acc = fma(v, bs[i], acc);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) Qo[(long long)j * NC] = acc;
-  }
-}

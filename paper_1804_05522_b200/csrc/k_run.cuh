@@ -1,118 +1,354 @@
 // k_run.cuh -- K implicit-Euler steps (S3-S7) in ONE persistent dataflow launch, pipelined
-// across time steps.  Only the right-hand-side column of the leaf panel depends on the previous
-// step's solution; everything else of step m (leaf LU, the U columns of the panel and their
-// projection) depends only on d+-(t_m).  So each step is split into
-//   A  (leaf): build + LU + U-column stripes, LU stored          (k_leaf.cuh leaf_task, nf = 0)
-//   B  (leaf): projection Q[:, 1:] = V^T X[:, 1:]                 (leaf_proj_task)
-//   A' (leaf): x0 = A_leaf^{-1}(u^(m-1) + dt f), Q[:, 0] = V^T x0 (leaf_rhs_task)
-//   tree units of every level, then u^(m) = X v per leaf group    (k_tree.cuh)
-// and the task queue of step m+1 follows that of step m: the A and B tasks of step m+1 run on
-// the SMs the latency-bound tree levels of step m leave idle.  Dependencies are per-task
-// counters (release/acquire at gpu scope); a task only waits for tasks with smaller indices
-// (claimed earlier by co-resident CTAs), so progress is guaranteed.  Step parity selects one
-// of two buffer sets (X, LU, Q, S); a step-m task never overwrites data a step m-2 task still
-// reads (A(m) waits for the final(m-2) group of its leaf).  Same arithmetic as k_step.
+// across time steps.  Of step m, only the right-hand-side column depends on u^(m-1); the leaf
+// LUs, the U columns of the panel (X[:, 1:] = A_leaf^{-1} U) and their projections depend on
+// d+-(t_m) alone.  Per leaf and step the work is therefore split into
+//   A  : build + LU (stored, inverse-diagonal form) + U-column stripes   (k_leaf.cuh leaf_task, nf = 0)
+//   B  : projection Q[:, 1:] = V_all^T X[:, 1:]                           (leaf_proj_task)
+//   B' : u^(m-1) on the leaf's rows = X^(m-1) v^(m-1) (the "final" of step m-1, see k_tree.cuh),
+//        x0 = A_leaf^{-1}(u^(m-1) + dt f^(m)) with the stored LU, X[:, 0] = x0,
+//        Q[:, 0] = V_all^T x0                                             (leaf_rhs_final below)
+// and the SMW tree units of every level follow (k_tree.cuh tr_unit).  A virtual step K holds
+// the last finals (u^(K-1)).  Only B' and the tree lie on the step-to-step chain; A and B of
+// step m+1 fill the SMs while the tree of step m climbs its latency-bound upper levels.
+//
+// Scheduling.  Leaf work comes from one ticket queue (atomicAdd): A(m), B(m), B'(m) for
+// m = 0..K-1, then the finals of step K.  Tree units never wait: a unit is released by the task
+// whose completion makes it ready -- the CTA completing the last input of a node runs the
+// node's first row chunk itself next (continuation: the step's critical chain runs without any
+// queue round trip) and publishes the other chunks in a ready queue.  A CTA takes ready-queue
+// work first (a ticket drawn when the queue is non-empty; a ticket drawn by a race past the
+// tail is kept and served by a later release), then continuation, then its leaf ticket, whose
+// inputs it polls.
+// Every dependency points to an earlier task of the order A(0) B(0) B'(0) tree(0) A(1) ..., so
+// the earliest incomplete task can always run: no deadlock for any number of co-resident CTAs.
+// Buffers alternate by step parity (X, stored LU, Q, S); the waits below protect every reuse:
+//   A(m)_i   waits B'(m-1)_i   (X^(m-2) of the leaf was last read by the final in B'(m-1)_i)
+//   B(m)_i   waits A(m)_i
+//   B'(m)_i  waits A(m)_i and root(m-1) of its instance (S^(m-1) complete)
+//   tree(m) level L-1 unit j waits B and B' of leaves 2j, 2j+1; level m units their children.
+// Same arithmetic as k_step except the rhs column: its leaf solve is a plain FMA block sweep
+// (not the DMMA stripe) and u^(m-1) is formed per leaf.
 #pragma once
 #include "k_step.cuh"
 
+#define RN_FRONT (LEAF_MAX + NCOL_MAX + 2 * LEAF_MAX + 32 + 2 * NCOL_MAX)   // b | v | part | z | pcd
+
 struct RunArgs {
-  LeafArgs la;                   // template (tree, g, L_l, ...); per-step fields set per task
-  TrArgs ta;
+  // per-step argument blocks in device memory (host-filled): step m's d+-, f, u^(m-1), u^(m)
+  // and the parity-(m & 1) buffer set (X, stored leaf LU, Q, S).  Read by reference from
+  // global memory, never copied into per-thread local memory.
+  const LeafArgs* las;           // [K]
+  const TrArgs* tas;             // [K]
   int K;
-  const double* dp; const double* dm; long long coef_stride;   // step m: dp + m * coef_stride
-  const double* f; long long f_stride;
-  const double* u0; double* uout;                              // uout + m * batch * n
-  double* X[2]; double* LU[2]; double* Q[2]; double* S[2];
-  unsigned* ctr;
-  int* done; long long per_step;                               // step m counters: done + m * per_step
-  long long o_A, o_pair, o_fin, o_lvl[LMAX];
+  int smem_doubles;              // dynamic shared memory of the launch
+  unsigned* heads;               // [0] tree units done, [1] leaf tickets, [2] rq tail, [3] rq head
+  unsigned long long* rq;        // ready queue: task id + 1 per slot (zeroed), K * units per step
+  int* done; long long per_step; // step m counters: done + m * per_step (m = 0..K-1)
+  long long o_A, o_R, o_pair, o_lvl[LMAX], o_kid[LMAX];   // o_kid[m]: completed children of level-m nodes
+  unsigned long long* trace;     // optional (FDE_TRACE_RUN): [0] count, then [start,end,code,sm]
+  long long trace_cap;
 };
+
+__device__ __forceinline__ bool rn_ready(const int* p, int target) { return st_ld_acquire(p) >= target; }
+
+// Leaf-queue ticket l: per step A of every leaf, B of every leaf, B' of every leaf; step K:
+// finals.  Are its inputs complete?
+__device__ __forceinline__ bool rn_leaf_ready(const RunArgs& ra, long long n_leaf, long long l) {
+  const TrArgs& a = ra.tas[0];
+  const long long step = l / (3 * n_leaf);
+  long long tk = l - step * 3 * n_leaf;
+  const int kind = step == ra.K ? 3 : (int)(tk / n_leaf);
+  tk -= (kind == 3 ? 0 : kind) * n_leaf;
+  const int* dn = ra.done + step * ra.per_step;
+  const int inst = (int)(tk / a.nleaf);
+  if (kind == 0) return step < 2 || rn_ready(dn - ra.per_step + ra.o_R + tk, 1);
+  if (kind == 1) return rn_ready(dn + ra.o_A + tk, 1);
+  if (kind == 2 && !rn_ready(dn + ra.o_A + tk, 1)) return false;
+  return step < 1 || rn_ready(dn - ra.per_step + ra.o_lvl[0] + inst, a.rc[0]);
+}
+
+// Tree task ids: step (16 bits) | level m (8) | chunk (8) | node jj = inst 2^m + j (32).
+__device__ __forceinline__ long long rn_tid(int step, int m, int chunk, long long jj) {
+  return ((long long)step << 48) | ((long long)m << 40) | ((long long)chunk << 32) | jj;
+}
+
+// Node jj of level m (step `step`) just became ready: its chunk 0 is this CTA's continuation,
+// chunks 1.. go to the ready queue.  (thread 0)
+__device__ __forceinline__ long long rn_release(const RunArgs& ra, int step, int m, long long jj) {
+  const int rc = ra.tas[0].rc[m];
+  for (int c = 1; c < rc; ++c) {
+    const unsigned slot = atomicAdd(ra.heads + 2, 1u);
+    const unsigned long long v = (unsigned long long)rn_tid(step, m, c, jj) + 1ULL;
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(ra.rq + slot), "l"(v) : "memory");
+  }
+  return rn_tid(step, m, 0, jj);
+}
+
+// B' (and the finals of step K): see the header.  geo: tree geometry; tp = step m-1's tree
+// arguments (X^(m-1), S^(m-1), u^(m-1) output) or null at m = 0; la = step m's leaf arguments
+// or null at m = K.
+__device__ void leaf_rhs_final(const TrArgs& geo, const TrArgs* tp, const LeafArgs* la, double* sm,
+                               int smem_doubles, int inst, int leaf) {
+  const TrArgs& a = geo;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int L = a.L, n = a.n, NC = a.xc[L];
+  const int r0 = a.leaf_r0[leaf], s = a.leaf_n[leaf], sp = round_up(s, 32), nb = sp >> 5;
+  double* bs = sm;                                    // b, then x0
+  double* vs = bs + LEAF_MAX;                         // v (NC)
+  double* part = vs + NCOL_MAX;                       // [2][128]
+  double* zs = part + 2 * LEAF_MAX;                   // [32]
+  PanelCol* pcd = reinterpret_cast<PanelCol*>(zs + 32);   // V-column descriptors (NC - 1)
+  double* LUs = sm + RN_FRONT;                        // [sp x sp] column-major, ld = sp
+  double* Ss = LUs + LEAF_MAX * LEAF_MAX;             // S_side blocks of a batch of levels
+  const int scap = smem_doubles - RN_FRONT - LEAF_MAX * LEAF_MAX;
+  // ---- stored LU in flight while the final is formed
+  if (la) {
+    const double* LUg = la->LU + (long long)inst * la->lustride + (long long)leaf * LEAF_SLOT;
+    for (int e = 2 * t; e < sp * sp; e += 2 * LEAF_THREADS) cp_async16(LUs + e, LUg + e);
+    cp_async_commit();
+    for (int j = t; j < NC - 1; j += LEAF_THREADS) pcd[j] = panel_col(*la, inst, leaf, r0, 1 + j, NC);
+  }
+  if (tp) {
+    // ---- v = M_{L-1} .. M_0 e_0,  M_m: v[m-cols] = -S_side(m) v[< xc_m]   (k_tree.cuh)
+    for (int c = t; c < NC; c += LEAF_THREADS) vs[c] = c == 0 ? 1.0 : 0.0;
+    const double* Sg = tp->Sst + (long long)inst * tp->sinst;
+    int m0 = 0;
+    while (m0 < L) {
+      int m1 = m0, used = 0;
+      while (m1 < L) {
+        const int sz = (a.xc[m1 + 1] - a.xc[m1]) * a.xc[m1];
+        if (m1 > m0 && used + sz > scap) break;
+        used += sz; ++m1;
+      }
+      int o = 0;
+      for (int m = m0; m < m1; ++m) {
+        const int xm = a.xc[m], k = a.xc[m + 1] - xm;
+        const int jn = leaf >> (L - m), side = (leaf >> (L - m - 1)) & 1;
+        const double* gp = Sg + a.slev[m] + (long long)jn * 2 * k * xm + (long long)side * k * xm;
+        for (int e = t; e < k * xm; e += LEAF_THREADS) cp_async8(Ss + o + e, gp + e);
+        o += k * xm;
+      }
+      cp_async_commit();
+      if (la && m0 == 0) cp_async_wait_group1(); else cp_async_wait_all();
+      __syncthreads();
+      if (warp == 0) {
+        int o2 = 0;
+        for (int m = m0; m < m1; ++m) {
+          const int xm = a.xc[m], k = a.xc[m + 1] - xm;
+          const double* S = Ss + o2;
+          for (int q = lane; q < k; q += 32) {
+            const double* sr = S + q * xm;
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            int c = 0;
+            for (; c + 3 < xm; c += 4) {
+              a0 = fma(sr[c], vs[c], a0); a1 = fma(sr[c + 1], vs[c + 1], a1);
+              a2 = fma(sr[c + 2], vs[c + 2], a2); a3 = fma(sr[c + 3], vs[c + 3], a3);
+            }
+            for (; c < xm; ++c) a0 = fma(sr[c], vs[c], a0);
+            vs[xm + q] = -((a0 + a1) + (a2 + a3));
+          }
+          __syncwarp();
+          o2 += k * xm;
+        }
+      }
+      __syncthreads();
+      m0 = m1;
+    }
+    // ---- u^(m-1) = X^(m-1) v on the leaf rows (two column halves, fixed-order sums)
+    {
+      const int i = t & 127, h = t >> 7;
+      const double* Xi = tp->X + (long long)inst * tp->xstride + r0 + i;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      if (i < s) {                                     // (X is written in this launch:
+        int c = h;                                     //  coherent loads, 4 in flight)
+        for (; c + 6 < NC; c += 8) {
+          const double x0 = Xi[(long long)c * n], x1 = Xi[(long long)(c + 2) * n];
+          const double x2 = Xi[(long long)(c + 4) * n], x3 = Xi[(long long)(c + 6) * n];
+          a0 = fma(x0, vs[c], a0); a1 = fma(x1, vs[c + 2], a1);
+          a2 = fma(x2, vs[c + 4], a2); a3 = fma(x3, vs[c + 6], a3);
+        }
+        for (; c < NC; c += 2) a0 = fma(Xi[(long long)c * n], vs[c], a0);
+      }
+      part[h * LEAF_MAX + i] = (a0 + a1) + (a2 + a3);
+    }
+    __syncthreads();
+    if (t < s) {
+      const double u = part[t] + part[LEAF_MAX + t];
+      tp->u[(long long)inst * n + r0 + t] = u;
+      if (la) bs[t] = u + la->dt * la->f[(long long)inst * n + r0 + t];
+    }
+  } else if (t < s) {
+    bs[t] = la->u_prev[(long long)inst * n + r0 + t] + la->dt * la->f[(long long)inst * n + r0 + t];
+  }
+  if (!la) return;
+  if (t >= s && t < sp) bs[t] = 0.0;
+  cp_async_wait_all();
+  __syncthreads();
+  // ---- x0 = A_leaf^{-1} b with the stored LU (k_leaf.cuh inverse-diagonal form: off-diagonal
+  //      blocks hold -Lt / -Ut, diagonal blocks D_k = A_kk^{-1}); 2 column halves per row
+  const int i = t & 127, h = t >> 7;
+  for (int kb = 0; kb + 1 < nb; ++kb) {              // forward: y_i += (-Lt_ik) y_k
+    const int c0 = 32 * kb + 16 * h;
+    double acc = 0.0;
+    if (i >= 32 * (kb + 1) && i < sp)
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) acc = fma(LUs[i + (c0 + jj) * sp], bs[c0 + jj], acc);
+    part[h * LEAF_MAX + i] = acc;
+    __syncthreads();
+    if (t < sp && t >= 32 * (kb + 1)) bs[t] += part[t] + part[LEAF_MAX + t];
+    __syncthreads();
+  }
+  for (int kb = nb - 1; kb >= 0; --kb) {             // backward: x_k = D_k y_k, y_j += (-Ut_jk) y_k
+    if (t < 32) zs[t] = bs[32 * kb + t];
+    __syncthreads();
+    const int c0 = 32 * kb + 16 * h;
+    double acc = 0.0;
+    if (i < 32 * (kb + 1))
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) acc = fma(LUs[i + (c0 + jj) * sp], zs[16 * h + jj], acc);
+    part[h * LEAF_MAX + i] = acc;
+    __syncthreads();
+    if (t < 32 * (kb + 1)) {
+      const double v = part[t] + part[LEAF_MAX + t];
+      bs[t] = t >= 32 * kb ? v : bs[t] + v;
+    }
+    __syncthreads();
+  }
+  double* X0 = la->X + (long long)inst * la->xstride + r0;
+  if (t < s) X0[t] = bs[t];
+  // ---- Q[j][0] = V_all[:, j]^T x0: a warp per 4 V columns, lanes over rows (fixed order)
+  double* Qo = la->Q + (long long)inst * la->qinst + (long long)leaf * la->qstride;
+  double xr[LEAF_MAX / 32];
+#pragma unroll
+  for (int q = 0; q < LEAF_MAX / 32; ++q) xr[q] = lane + 32 * q < s ? bs[lane + 32 * q] : 0.0;
+  for (int j0 = 4 * warp; j0 < NC - 1; j0 += 4 * LEAF_WARPS) {
+    double vv[4][LEAF_MAX / 32];
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {                  // all 16 loads in flight first
+      const PanelCol pc = j0 + jj < NC - 1 ? pcd[j0 + jj] : PanelCol{la->Lf, 0, 0, 0, 0, 0};
+#pragma unroll
+      for (int q = 0; q < LEAF_MAX / 32; ++q) {
+        const int r = lane + 32 * q, rc = r < s ? r : s - 1;
+        const double x = __ldg(pc.Lq + pc.li0 + pc.lstep * rc);   // (valid address for any kind)
+        vv[jj][q] = pc.kind == 2 ? x : (pc.kind == 3 && pc.li0 + pc.lstep * r == 0 ? 1.0 : 0.0);
+      }
+    }
+    double acc[4];
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      acc[jj] = 0.0;
+#pragma unroll
+      for (int q = 0; q < LEAF_MAX / 32; ++q) acc[jj] = fma(vv[jj][q], xr[q], acc[jj]);
+    }
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      double v = acc[jj];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0 && j0 + jj < NC - 1) Qo[(long long)(j0 + jj) * NC] = v;
+    }
+  }
+}
 
 __global__ void __launch_bounds__(TR_THREADS, 1)
 k_run(const RunArgs ra) {
   extern __shared__ double smem[];
-  __shared__ int task;
-  const TrArgs& a0 = ra.ta;
-  const int B = a0.batch, L = a0.L, nleaf = a0.nleaf, n = a0.n;
-  const long long n_leaf = (long long)B * nleaf;
-  long long n_lvl[LMAX];
-  long long T = 3 * n_leaf;
-  for (int m = L - 1; m >= 0; --m) { n_lvl[m] = (long long)B * (1LL << m) * a0.rc[m]; T += n_lvl[m]; }
-  const long long n_fin = (n_leaf + TR_NL - 1) / TR_NL;
-  T += n_fin;
-  const long long total = T * ra.K;
+  __shared__ long long task;
+  __shared__ int queue;
+  const TrArgs& a0 = ra.tas[0];
+  const int L = a0.L, nleaf = a0.nleaf;
+  const long long n_leaf = (long long)a0.batch * nleaf;
+  long long Tt = 0;
+  for (int m = 0; m < L; ++m) Tt += (long long)a0.batch * (1LL << m) * a0.rc[m];
+  const unsigned tot_t = (unsigned)(Tt * ra.K), tot_l = (unsigned)(3 * n_leaf * ra.K + n_leaf);
+  volatile unsigned* vh = ra.heads;     // [0] tree units completed, [1] leaf tickets, [2] rq tail, [3] rq head
+  long long held = -1;                  // thread 0: leaf ticket not yet runnable
+  long long iou = -1;                   // thread 0: ready-queue ticket not yet served
+  long long cont = -1;                  // thread 0: continuation tree task
+  bool leaf_out = false;                // thread 0: leaf queue exhausted
   while (true) {
-    __syncthreads();
-    if (threadIdx.x == 0) task = (int)atomicAdd(ra.ctr, 1u);
-    __syncthreads();
-    long long tk = task;
-    if (tk >= total) break;
-    const int step = (int)(tk / T), p = step & 1;
-    tk -= (long long)step * T;
-    int* dn = ra.done + (long long)step * ra.per_step;
-    int* dprev = ra.done + (long long)(step - 1) * ra.per_step;     // (valid for step >= 1)
-    int* dprev2 = ra.done + (long long)(step - 2) * ra.per_step;    // (valid for step >= 2)
-    // per-step views
-    LeafArgs la = ra.la;
-    la.dp = ra.dp + (long long)step * ra.coef_stride;
-    la.dm = ra.dm + (long long)step * ra.coef_stride;
-    la.f = ra.f + (long long)step * ra.f_stride;
-    la.u_prev = step == 0 ? ra.u0 : ra.uout + (long long)(step - 1) * B * n;
-    la.X = ra.X[p]; la.LU = ra.LU[p];
-    la.Q = ra.Q[p] + a0.qlev[L];
-    if (tk < n_leaf) {                                  // ---- A: build, LU (stored), U columns
-      const int inst = (int)(tk / nleaf), leaf = (int)(tk % nleaf);
-      if (step >= 2) st_wait(dprev2 + ra.o_fin + tk / TR_NL, 1);
-      la.nf = 0; la.store_lu = 1;
-      leaf_task(la, smem, leaf, inst, false);
-      st_signal(dn + ra.o_A + tk);
-      continue;
-    }
-    tk -= n_leaf;
-    if (tk < n_leaf) {                                  // ---- B: projection of the U columns
-      const int inst = (int)(tk / nleaf), leaf = (int)(tk % nleaf);
-      st_wait(dn + ra.o_A + tk, 1);
-      la.nf = 0;
-      leaf_proj_task(la, smem, leaf, inst);
-      st_signal(dn + ra.o_pair + (long long)inst * (1 << (L - 1)) + (leaf >> 1));
-      continue;
-    }
-    tk -= n_leaf;
-    if (tk < n_leaf) {                                  // ---- A': the rhs column
-      const int inst = (int)(tk / nleaf), leaf = (int)(tk % nleaf);
-      st_wait(dn + ra.o_A + tk, 1);
-      if (step >= 1) st_wait(dprev + ra.o_fin + tk / TR_NL, 1);
-      leaf_rhs_task(la, smem, leaf, inst);
-      st_signal(dn + ra.o_pair + (long long)inst * (1 << (L - 1)) + (leaf >> 1));
-      continue;
-    }
-    tk -= n_leaf;
-    TrArgs a = a0;
-    a.Q = ra.Q[p]; a.Qleaf = ra.Q[p] + a0.qlev[L]; a.Sst = ra.S[p]; a.X = ra.X[p];
-    a.u = ra.uout + (long long)step * B * n;
-    int m = L - 1;
-    while (m >= 0 && tk >= n_lvl[m]) { tk -= n_lvl[m]; --m; }
-    if (m >= 0) {                                       // ---- SMW unit of level m
-      const long long per_inst = (1LL << m) * a.rc[m];
-      const int inst = (int)(tk / per_inst), w = (int)(tk % per_inst);
-      const int j = w / a.rc[m], chunk = w % a.rc[m];
-      if (m == L - 1) {
-        st_wait(dn + ra.o_pair + (long long)inst * (1 << (L - 1)) + j, 4);
-      } else {
-        const int* c = dn + ra.o_lvl[m + 1] + (long long)inst * (1 << (m + 1)) + 2 * j;
-        st_wait(c, a.rc[m + 1]);
-        st_wait(c + 1, a.rc[m + 1]);
+    __syncthreads();                                  // (previous task consumed)
+    if (threadIdx.x == 0) {
+      int q = -1;
+      long long idx = 0;
+      while (true) {
+        if (cont >= 0) { q = 0; idx = cont; cont = -1; break; }
+        if (iou >= 0) {                               // then ready-queue work
+          unsigned long long v;
+          asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ra.rq + iou) : "memory");
+          if (v) { q = 0; idx = (long long)(v - 1); iou = -1; break; }
+        } else if (vh[2] > vh[3]) {
+          iou = atomicAdd(ra.heads + 3, 1u);
+          continue;
+        }
+        if (held < 0 && !leaf_out) {
+          const unsigned l = atomicAdd(ra.heads + 1, 1u);
+          if (l < tot_l) held = l; else leaf_out = true;
+        }
+        if (held >= 0 && rn_leaf_ready(ra, n_leaf, held)) { q = 1; idx = held; held = -1; break; }
+        if (leaf_out && held < 0 && vh[0] >= tot_t) break;
+        __nanosleep(32);
       }
-      tr_unit(a, smem, inst, m, j, chunk);
-      st_signal(dn + ra.o_lvl[m] + (long long)inst * (1 << m) + j);
-      continue;
+      queue = q; task = idx;
     }
-    // ---- final group: u^(step) = X v for TR_NL leaves
-    const long long lu0 = tk * TR_NL;
-    const int nl = (int)min((long long)TR_NL, n_leaf - lu0);
-    const int i0 = (int)(lu0 / nleaf), i1 = (int)((lu0 + nl - 1) / nleaf);
-    for (int inst = i0; inst <= i1; ++inst) st_wait(dn + ra.o_lvl[0] + inst, a.rc[0]);
-    tr_final(a, smem, (int)lu0, nl);
-    st_signal(dn + ra.o_fin + tk);
+    __syncthreads();
+    if (queue < 0) break;
+    unsigned long long t_start = 0;
+    if (ra.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    int code;
+    if (queue == 1) {                                 // ---- leaf ticket
+      const int step = (int)(task / (3 * n_leaf));
+      long long tk = task - (long long)step * 3 * n_leaf;
+      const int kind = step == ra.K ? 3 : (int)(tk / n_leaf);
+      tk -= (kind == 3 ? 0 : kind) * n_leaf;
+      const int inst = (int)(tk / nleaf), leaf = (int)(tk % nleaf);
+      int* dn = ra.done + (long long)step * ra.per_step;
+      if (kind == 0) {                                // A: build, LU (stored), U columns
+        leaf_task(ra.las[step], smem, leaf, inst, false);
+      } else if (kind == 1) {                         // B: projection of the U columns
+        leaf_proj_task(ra.las[step], smem, leaf, inst);
+      } else {                                        // B': final of step-1 + rhs column
+        leaf_rhs_final(a0, step > 0 ? &ra.tas[step - 1] : nullptr, kind == 2 ? &ra.las[step] : nullptr,
+                       smem, ra.smem_doubles, inst, leaf);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0 && kind < 3) {
+        __threadfence();
+        if (kind == 0) atomicAdd(dn + ra.o_A + tk, 1);
+        if (kind == 2) atomicAdd(dn + ra.o_R + tk, 1);
+        if (kind >= 1) {
+          const long long jj = (long long)inst * (1 << (L - 1)) + (leaf >> 1);
+          if (atomicAdd(dn + ra.o_pair + jj, 1) == 3) cont = rn_release(ra, step, L - 1, jj);
+        }
+      }
+      code = 100 + kind + 1000 * step;
+    } else {                                          // ---- tree unit
+      const int step = (int)(task >> 48), m = (int)((task >> 40) & 0xff), chunk = (int)((task >> 32) & 0xff);
+      const long long jj = task & 0xffffffffLL;
+      const int inst = (int)(jj >> m), j = (int)(jj & ((1LL << m) - 1));
+      int* dn = ra.done + (long long)step * ra.per_step;
+      const TrArgs& a = ra.tas[step];
+      tr_unit(a, smem, inst, m, j, chunk);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(dn + ra.o_lvl[m] + jj, 1) == a.rc[m] - 1 && m > 0) {
+          const long long pj = (long long)inst * (1 << (m - 1)) + (j >> 1);   // node complete
+          if (atomicAdd(dn + ra.o_kid[m - 1] + pj, 1) == 1) cont = rn_release(ra, step, m - 1, pj);
+        }
+        atomicAdd(ra.heads, 1u);
+      }
+      code = m + 1000 * step;
+    }
+    if (ra.trace && threadIdx.x == 0) {
+      const unsigned long long e = atomicAdd(ra.trace, 1ULL);
+      if ((long long)e < ra.trace_cap) {
+        unsigned long long te; unsigned smid;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(te));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        unsigned long long* r = ra.trace + 4 + 4 * e;
+        r[0] = t_start; r[1] = te; r[2] = (unsigned long long)code; r[3] = smid;
+      }
+    }
   }
 }

@@ -1,5 +1,5 @@
 #!/bin/bash
-# Round-end style evidence run: tests, smoke, full bench, ncu launch list + full capture of k_step.
+# Round-end style evidence run: tests, smoke, full bench, ncu launch list + full capture of k_run.
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
@@ -9,6 +9,6 @@ CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-extra"
 timeout 300 $CMD > gpurun_out/plain.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
 echo "ncu launches rc=$?" >> gpurun_out/ncu_launch.log
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_step -s 4 -c 1 -o gpurun_out/prof $CMD > gpurun_out/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_run -s 2 -c 1 -o gpurun_out/prof $CMD > gpurun_out/ncu_full.log 2>&1
 echo "ncu full rc=$?" >> gpurun_out/ncu_full.log
 tail -3 gpurun_out/pytest_gpu.log gpurun_out/smoke.log gpurun_out/ncu_full.log
