@@ -440,7 +440,8 @@ def run_ours(args, world, rank, local):
             # equal to the derived 148 SMs x 64 FMA/clk x 2 x 1.965 GHz = 37.2 TFLOP/s
             roof = {"bound": "tensor", "achieved": fl / t_s / 1e12, "peak": FP64_TENSOR_TFLOPS,
                     "unit": "TFLOP/s", "frac": fl / t_s / 1e12 / FP64_TENSOR_TFLOPS,
-                    "traffic": traffic.get(dom), "kernel": dom,
+                    "traffic": (traffic[dom + "_per_step"] * args.steps if dom + "_per_step" in traffic
+                                else traffic.get(dom)), "kernel": dom,
                     "flops_per_launch": fl / launches_dom,
                     "achieved_hbm_gbs": by / t_s / 1e9,
                     "peak_source": "measured DMMA m8n8k4 f64 (tools/fp64_peak.cu): 37.05 TFLOP/s"}
