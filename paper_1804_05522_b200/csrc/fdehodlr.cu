@@ -1262,6 +1262,10 @@ int fde1d_run(int batch, int n, const double* alpha, double h, double dt, int K,
     if (!run_trace) CU(cudaMalloc(&run_trace, run_trace_len * sizeof(unsigned long long)));
     CU(cudaMemsetAsync(run_trace, 0, run_trace_len * sizeof(unsigned long long), s));
     ra.trace = run_trace; ra.trace_cap = 262144;
+    static unsigned long long* run_prof = nullptr;
+    if (!run_prof) CU(cudaMalloc(&run_prof, 16 * sizeof(unsigned long long)));
+    CU(cudaMemsetAsync(run_prof, 0, 16 * sizeof(unsigned long long), s));
+    ra.prof = run_prof;
   }
   void* args[] = {&ra};
   { PROF("k_run"); CU(cudaLaunchCooperativeKernel((void*)k_run, dim3(H->step_grid), dim3(TR_THREADS), args, H->step_smem, s)); }
@@ -1270,6 +1274,14 @@ int fde1d_run(int batch, int n, const double* alpha, double h, double dt, int K,
     std::vector<unsigned long long> h(run_trace_len);
     CU(cudaStreamSynchronize(s));
     CU(cudaMemcpy(h.data(), ra.trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    std::vector<unsigned long long> pf(16);
+    CU(cudaMemcpy(pf.data(), ra.prof, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    for (int g = 0; g < 2; ++g) {
+      const double c = (double)std::max(1ULL, pf[8 * g + 7]);
+      fprintf(stderr, "k_run %s phases (us avg over %llu): S %.2f v %.2f Xv %.2f LUwait %.2f solve %.2f\n",
+              g ? "final-only" : "B'", pf[8 * g + 7], pf[8 * g + 1] / c / 1965.0, pf[8 * g + 2] / c / 1965.0,
+              pf[8 * g + 3] / c / 1965.0, pf[8 * g + 4] / c / 1965.0, pf[8 * g + 5] / c / 1965.0);
+    }
     FILE* fo = fopen(getenv("FDE_TRACE_RUN"), "w");
     if (fo) {
       const long long ne = std::min<long long>((long long)h[0], ra.trace_cap);

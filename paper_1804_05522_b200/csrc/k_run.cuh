@@ -31,7 +31,7 @@
 #pragma once
 #include "k_step.cuh"
 
-#define RN_FRONT (LEAF_MAX + NCOL_MAX + 2 * LEAF_MAX + 32 + 2 * NCOL_MAX)   // b | v | part | z | pcd
+#define RN_FRONT (LEAF_MAX + NCOL_MAX + 4 * LEAF_MAX + 32)   // b | v | part[4] | z
 
 struct RunArgs {
   // per-step argument blocks in device memory (host-filled): step m's d+-, f, u^(m-1), u^(m)
@@ -46,6 +46,7 @@ struct RunArgs {
   int* done; long long per_step; // step m counters: done + m * per_step (m = 0..K-1)
   long long o_A, o_R, o_pair, o_lvl[LMAX], o_kid[LMAX];   // o_kid[m]: completed children of level-m nodes
   unsigned long long* trace;     // optional (FDE_TRACE_RUN): [0] count, then [start,end,code,sm]
+  unsigned long long* prof;      // optional: B' phase cycle sums [16]
   long long trace_cap;
 };
 
@@ -65,6 +66,15 @@ __device__ __forceinline__ bool rn_leaf_ready(const RunArgs& ra, long long n_lea
   if (kind == 1) return rn_ready(dn + ra.o_A + tk, 1);
   if (kind == 2 && !rn_ready(dn + ra.o_A + tk, 1)) return false;
   return step < 1 || rn_ready(dn - ra.per_step + ra.o_lvl[0] + inst, a.rc[0]);
+}
+
+// Block copy of an argument struct into shared memory (whole CTA; ends with a barrier).
+template <class T>
+__device__ __forceinline__ void rn_copy(T* dst, const T* src) {
+  static_assert(sizeof(T) % 8 == 0, "argument block size");
+  for (int i = threadIdx.x; i < (int)(sizeof(T) / 8); i += blockDim.x)
+    reinterpret_cast<unsigned long long*>(dst)[i] = reinterpret_cast<const unsigned long long*>(src)[i];
+  __syncthreads();
 }
 
 // Tree task ids: step (16 bits) | level m (8) | chunk (8) | node jj = inst 2^m + j (32).
@@ -88,31 +98,36 @@ __device__ __forceinline__ long long rn_release(const RunArgs& ra, int step, int
 // arguments (X^(m-1), S^(m-1), u^(m-1) output) or null at m = 0; la = step m's leaf arguments
 // or null at m = K.
 __device__ void leaf_rhs_final(const TrArgs& geo, const TrArgs* tp, const LeafArgs* la, double* sm,
-                               int smem_doubles, int inst, int leaf) {
+                               int smem_doubles, int inst, int leaf, unsigned long long* prof = nullptr) {
   const TrArgs& a = geo;
+  long long ph_t = clock64();
+#define RN_PH(i) do { if (prof && threadIdx.x == 0) { const long long t_ = clock64(); \
+    atomicAdd(prof + (la ? 0 : 8) + (i), (unsigned long long)(t_ - ph_t)); ph_t = t_; } } while (0)
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int L = a.L, n = a.n, NC = a.xc[L];
   const int r0 = a.leaf_r0[leaf], s = a.leaf_n[leaf], sp = round_up(s, 32), nb = sp >> 5;
   double* bs = sm;                                    // b, then x0
   double* vs = bs + LEAF_MAX;                         // v (NC)
-  double* part = vs + NCOL_MAX;                       // [2][128]
-  double* zs = part + 2 * LEAF_MAX;                   // [32]
-  PanelCol* pcd = reinterpret_cast<PanelCol*>(zs + 32);   // V-column descriptors (NC - 1)
+  double* part = vs + NCOL_MAX;                       // [4][128]
+  double* zs = part + 4 * LEAF_MAX;                   // [32]
   double* LUs = sm + RN_FRONT;                        // [sp x sp] column-major, ld = sp
   double* Ss = LUs + LEAF_MAX * LEAF_MAX;             // S_side blocks of a batch of levels
+  PanelCol* pcd = reinterpret_cast<PanelCol*>(Ss);   // then: V-column descriptors (NC - 1)
   const int scap = smem_doubles - RN_FRONT - LEAF_MAX * LEAF_MAX;
-  // ---- stored LU in flight while the final is formed
-  if (la) {
+  // ---- the first batch of S blocks, then the stored LU, in flight while the final is formed
+  auto issue_lu = [&]() {
     const double* LUg = la->LU + (long long)inst * la->lustride + (long long)leaf * LEAF_SLOT;
     for (int e = 2 * t; e < sp * sp; e += 2 * LEAF_THREADS) cp_async16(LUs + e, LUg + e);
     cp_async_commit();
-    for (int j = t; j < NC - 1; j += LEAF_THREADS) pcd[j] = panel_col(*la, inst, leaf, r0, 1 + j, NC);
-  }
+  };
   if (tp) {
-    // ---- v = M_{L-1} .. M_0 e_0,  M_m: v[m-cols] = -S_side(m) v[< xc_m]   (k_tree.cuh)
+    // ---- v = M_{L-1} .. M_0 e_0,  M_m: v[m-cols] = -S_side(m) v[< xc_m]   (k_tree.cuh);
+    //      S_side(m) (k x xm, row-major in HBM) is staged transposed: lane q reads row q
+    //      conflict-free while the warp walks the columns
     for (int c = t; c < NC; c += LEAF_THREADS) vs[c] = c == 0 ? 1.0 : 0.0;
     const double* Sg = tp->Sst + (long long)inst * tp->sinst;
     int m0 = 0;
+    bool lu_issued = la == nullptr;
     while (m0 < L) {
       int m1 = m0, used = 0;
       while (m1 < L) {
@@ -125,65 +140,99 @@ __device__ void leaf_rhs_final(const TrArgs& geo, const TrArgs* tp, const LeafAr
         const int xm = a.xc[m], k = a.xc[m + 1] - xm;
         const int jn = leaf >> (L - m), side = (leaf >> (L - m - 1)) & 1;
         const double* gp = Sg + a.slev[m] + (long long)jn * 2 * k * xm + (long long)side * k * xm;
-        for (int e = t; e < k * xm; e += LEAF_THREADS) cp_async8(Ss + o + e, gp + e);
+        for (int q = warp; q < k; q += LEAF_WARPS)
+          for (int c = lane; c < xm; c += 32) cp_async8(Ss + o + c * k + q, gp + q * xm + c);
         o += k * xm;
       }
       cp_async_commit();
-      if (la && m0 == 0) cp_async_wait_group1(); else cp_async_wait_all();
+      if (!lu_issued) { issue_lu(); lu_issued = true; cp_async_wait_group1(); } else cp_async_wait_all();
       __syncthreads();
-      if (warp == 0) {
+      RN_PH(1);
+      {                                               // lane = row q of S_side, warp = column slice
         int o2 = 0;
+        double* vp = part;                            // [8 warps][32 rows] partial sums
         for (int m = m0; m < m1; ++m) {
           const int xm = a.xc[m], k = a.xc[m + 1] - xm;
-          const double* S = Ss + o2;
-          for (int q = lane; q < k; q += 32) {
-            const double* sr = S + q * xm;
+          const double* St = Ss + o2;                 // [xm][k]
+          const int cw = (xm + LEAF_WARPS - 1) / LEAF_WARPS, c0 = warp * cw, c1 = min(xm, c0 + cw);
+          for (int q0 = 0; q0 < k; q0 += 32) {
+            const int q = q0 + lane;
             double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-            int c = 0;
-            for (; c + 3 < xm; c += 4) {
-              a0 = fma(sr[c], vs[c], a0); a1 = fma(sr[c + 1], vs[c + 1], a1);
-              a2 = fma(sr[c + 2], vs[c + 2], a2); a3 = fma(sr[c + 3], vs[c + 3], a3);
+            if (q < k) {
+              int c = c0;
+#pragma unroll 2
+              for (; c + 3 < c1; c += 4) {
+                a0 = fma(St[c * k + q], vs[c], a0); a1 = fma(St[(c + 1) * k + q], vs[c + 1], a1);
+                a2 = fma(St[(c + 2) * k + q], vs[c + 2], a2); a3 = fma(St[(c + 3) * k + q], vs[c + 3], a3);
+              }
+              for (; c < c1; ++c) a0 = fma(St[c * k + q], vs[c], a0);
             }
-            for (; c < xm; ++c) a0 = fma(sr[c], vs[c], a0);
-            vs[xm + q] = -((a0 + a1) + (a2 + a3));
+            vp[warp * 32 + lane] = (a0 + a1) + (a2 + a3);
+            __syncthreads();
+            if (t < 32 && q0 + t < k) {
+              double v = 0.0;
+#pragma unroll
+              for (int w = 0; w < LEAF_WARPS; ++w) v += vp[w * 32 + t];
+              vs[xm + q0 + t] = -v;
+            }
+            __syncthreads();
           }
-          __syncwarp();
           o2 += k * xm;
         }
       }
       __syncthreads();
+      RN_PH(2);
       m0 = m1;
     }
-    // ---- u^(m-1) = X^(m-1) v on the leaf rows (two column halves, fixed-order sums)
+    // ---- u^(m-1) = X^(m-1) v on the leaf rows: 2 rows per thread (16-byte loads, 16 in flight),
+    //      4 column quarters, fixed-order sums
     {
-      const int i = t & 127, h = t >> 7;
-      const double* Xi = tp->X + (long long)inst * tp->xstride + r0 + i;
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      if (i < s) {                                     // (X is written in this launch:
-        int c = h;                                     //  coherent loads, 4 in flight)
-        for (; c + 6 < NC; c += 8) {
-          const double x0 = Xi[(long long)c * n], x1 = Xi[(long long)(c + 2) * n];
-          const double x2 = Xi[(long long)(c + 4) * n], x3 = Xi[(long long)(c + 6) * n];
-          a0 = fma(x0, vs[c], a0); a1 = fma(x1, vs[c + 2], a1);
-          a2 = fma(x2, vs[c + 4], a2); a3 = fma(x3, vs[c + 6], a3);
+      const int i2 = 2 * (t & 63), h = t >> 6;
+      const double* Xi = tp->X + (long long)inst * tp->xstride + r0 + i2;
+      const bool vec = ((r0 | n | tp->xstride) & 1) == 0;   // 16-byte aligned row pairs
+      double ac0[4] = {0.0, 0.0, 0.0, 0.0}, ac1[4] = {0.0, 0.0, 0.0, 0.0};
+      if (i2 < s) {                                   // (X is written in this launch: coherent loads)
+        int c = h;
+        if (vec && i2 + 1 < s) {
+          for (; c < NC; c += 4 * 24) {               // 24 x 16-byte loads in flight per thread
+            double2 x[24];
+#pragma unroll
+            for (int u = 0; u < 24; ++u)
+              x[u] = c + 4 * u < NC ? *reinterpret_cast<const double2*>(Xi + (long long)(c + 4 * u) * n)
+                                    : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int u = 0; u < 24; ++u) {
+              const double vv = c + 4 * u < NC ? vs[c + 4 * u] : 0.0;
+              ac0[u & 3] = fma(x[u].x, vv, ac0[u & 3]);
+              ac1[u & 3] = fma(x[u].y, vv, ac1[u & 3]);
+            }
+          }
+        } else {
+          for (; c < NC; c += 4) {
+            ac0[0] = fma(Xi[(long long)c * n], vs[c], ac0[0]);
+            if (i2 + 1 < s) ac1[0] = fma(Xi[(long long)c * n + 1], vs[c], ac1[0]);
+          }
         }
-        for (; c < NC; c += 2) a0 = fma(Xi[(long long)c * n], vs[c], a0);
       }
-      part[h * LEAF_MAX + i] = (a0 + a1) + (a2 + a3);
+      part[h * LEAF_MAX + i2] = (ac0[0] + ac0[1]) + (ac0[2] + ac0[3]);
+      part[h * LEAF_MAX + i2 + 1] = (ac1[0] + ac1[1]) + (ac1[2] + ac1[3]);
     }
     __syncthreads();
+    RN_PH(3);
     if (t < s) {
-      const double u = part[t] + part[LEAF_MAX + t];
+      const double u = (part[t] + part[LEAF_MAX + t]) + (part[2 * LEAF_MAX + t] + part[3 * LEAF_MAX + t]);
       tp->u[(long long)inst * n + r0 + t] = u;
       if (la) bs[t] = u + la->dt * la->f[(long long)inst * n + r0 + t];
     }
-  } else if (t < s) {
-    bs[t] = la->u_prev[(long long)inst * n + r0 + t] + la->dt * la->f[(long long)inst * n + r0 + t];
+  } else {
+    if (la) issue_lu();
+    if (t < s) bs[t] = la->u_prev[(long long)inst * n + r0 + t] + la->dt * la->f[(long long)inst * n + r0 + t];
   }
   if (!la) return;
   if (t >= s && t < sp) bs[t] = 0.0;
   cp_async_wait_all();
   __syncthreads();
+  RN_PH(4);
   // ---- x0 = A_leaf^{-1} b with the stored LU (k_leaf.cuh inverse-diagonal form: off-diagonal
   //      blocks hold -Lt / -Ut, diagonal blocks D_k = A_kk^{-1}); 2 column halves per row
   const int i = t & 127, h = t >> 7;
@@ -214,17 +263,21 @@ __device__ void leaf_rhs_final(const TrArgs& geo, const TrArgs* tp, const LeafAr
     }
     __syncthreads();
   }
+  RN_PH(5);
   double* X0 = la->X + (long long)inst * la->xstride + r0;
   if (t < s) X0[t] = bs[t];
+  for (int j = t; j < NC - 1; j += LEAF_THREADS) pcd[j] = panel_col(*la, inst, leaf, r0, 1 + j, NC);
+  __syncthreads();
   // ---- Q[j][0] = V_all[:, j]^T x0: a warp per 4 V columns, lanes over rows (fixed order)
   double* Qo = la->Q + (long long)inst * la->qinst + (long long)leaf * la->qstride;
   double xr[LEAF_MAX / 32];
 #pragma unroll
   for (int q = 0; q < LEAF_MAX / 32; ++q) xr[q] = lane + 32 * q < s ? bs[lane + 32 * q] : 0.0;
-  for (int j0 = 4 * warp; j0 < NC - 1; j0 += 4 * LEAF_WARPS) {
-    double vv[4][LEAF_MAX / 32];
+  constexpr int QG = 6;                               // V columns per warp pass (24 loads in flight)
+  for (int j0 = QG * warp; j0 < NC - 1; j0 += QG * LEAF_WARPS) {
+    double vv[QG][LEAF_MAX / 32];
 #pragma unroll
-    for (int jj = 0; jj < 4; ++jj) {                  // all 16 loads in flight first
+    for (int jj = 0; jj < QG; ++jj) {
       const PanelCol pc = j0 + jj < NC - 1 ? pcd[j0 + jj] : PanelCol{la->Lf, 0, 0, 0, 0, 0};
 #pragma unroll
       for (int q = 0; q < LEAF_MAX / 32; ++q) {
@@ -233,16 +286,11 @@ __device__ void leaf_rhs_final(const TrArgs& geo, const TrArgs* tp, const LeafAr
         vv[jj][q] = pc.kind == 2 ? x : (pc.kind == 3 && pc.li0 + pc.lstep * r == 0 ? 1.0 : 0.0);
       }
     }
-    double acc[4];
 #pragma unroll
-    for (int jj = 0; jj < 4; ++jj) {
-      acc[jj] = 0.0;
+    for (int jj = 0; jj < QG; ++jj) {
+      double v = 0.0;
 #pragma unroll
-      for (int q = 0; q < LEAF_MAX / 32; ++q) acc[jj] = fma(vv[jj][q], xr[q], acc[jj]);
-    }
-#pragma unroll
-    for (int jj = 0; jj < 4; ++jj) {
-      double v = acc[jj];
+      for (int q = 0; q < LEAF_MAX / 32; ++q) v = fma(vv[jj][q], xr[q], v);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
       if (lane == 0 && j0 + jj < NC - 1) Qo[(long long)(j0 + jj) * NC] = v;
@@ -255,6 +303,10 @@ k_run(const RunArgs ra) {
   extern __shared__ double smem[];
   __shared__ long long task;
   __shared__ int queue;
+  // the task's argument blocks, copied from global memory once per task: the kernels read
+  // their geometry (xcol, ranks, offsets, ...) from shared memory, not through the L1
+  __shared__ LeafArgs s_la;
+  __shared__ TrArgs s_ta, s_tp;
   const TrArgs& a0 = ra.tas[0];
   const int L = a0.L, nleaf = a0.nleaf;
   const long long n_leaf = (long long)a0.batch * nleaf;
@@ -304,12 +356,17 @@ k_run(const RunArgs ra) {
       const int inst = (int)(tk / nleaf), leaf = (int)(tk % nleaf);
       int* dn = ra.done + (long long)step * ra.per_step;
       if (kind == 0) {                                // A: build, LU (stored), U columns
-        leaf_task(ra.las[step], smem, leaf, inst, false);
+        rn_copy(&s_la, &ra.las[step]);
+        leaf_task(s_la, smem, leaf, inst, false);
       } else if (kind == 1) {                         // B: projection of the U columns
-        leaf_proj_task(ra.las[step], smem, leaf, inst);
+        rn_copy(&s_la, &ra.las[step]);
+        leaf_proj_task(s_la, smem, leaf, inst);
       } else {                                        // B': final of step-1 + rhs column
-        leaf_rhs_final(a0, step > 0 ? &ra.tas[step - 1] : nullptr, kind == 2 ? &ra.las[step] : nullptr,
-                       smem, ra.smem_doubles, inst, leaf);
+        if (kind == 2) rn_copy(&s_la, &ra.las[step]);
+        if (step > 0) rn_copy(&s_tp, &ra.tas[step - 1]); else rn_copy(&s_tp, &ra.tas[0]);
+        leaf_rhs_final(s_tp, step > 0 ? &s_tp : nullptr, kind == 2 ? &s_la : nullptr,
+                       smem, ra.smem_doubles, inst, leaf, ra.prof);
+        if (ra.prof && threadIdx.x == 0) atomicAdd(ra.prof + (kind == 2 ? 7 : 15), 1ULL);
       }
       __syncthreads();
       if (threadIdx.x == 0 && kind < 3) {
@@ -327,7 +384,8 @@ k_run(const RunArgs ra) {
       const long long jj = task & 0xffffffffLL;
       const int inst = (int)(jj >> m), j = (int)(jj & ((1LL << m) - 1));
       int* dn = ra.done + (long long)step * ra.per_step;
-      const TrArgs& a = ra.tas[step];
+      rn_copy(&s_ta, &ra.tas[step]);
+      const TrArgs& a = s_ta;
       tr_unit(a, smem, inst, m, j, chunk);
       __syncthreads();
       if (threadIdx.x == 0) {
