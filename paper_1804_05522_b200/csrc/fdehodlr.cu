@@ -1239,6 +1239,18 @@ int fde1d_run(int batch, int n, const double* alpha, double h, double dt, int K,
     tm.Q = Qp[p]; tm.Qleaf = Qp[p] + H->qlev[L]; tm.Sst = Sp[p]; tm.X = Xp[p];
     tm.u = u_out + m * cnt;
   }
+  static unsigned long long* run_trace = nullptr;
+  const long long run_trace_len = 4 + 4 * 262144;
+  if (getenv("FDE_TRACE_RUN")) {
+    if (!run_trace) CU(cudaMalloc(&run_trace, run_trace_len * sizeof(unsigned long long)));
+    CU(cudaMemsetAsync(run_trace, 0, run_trace_len * sizeof(unsigned long long), s));
+    ra.trace = run_trace; ra.trace_cap = 262144;
+    static unsigned long long* run_prof = nullptr;
+    if (!run_prof) CU(cudaMalloc(&run_prof, 32 * sizeof(unsigned long long)));
+    CU(cudaMemsetAsync(run_prof, 0, 32 * sizeof(unsigned long long), s));
+    ra.prof = run_prof;
+    for (int m = 0; m < K; ++m) H->run_las[m].prof = run_prof + 16;
+  }
   const size_t args_bytes = (size_t)K * (sizeof(LeafArgs) + sizeof(TrArgs));
   if (args_bytes > H->run_args_cap) {
     if (H->d_run_args) { cudaStreamSynchronize(s); cudaFree(H->d_run_args); H->allocs.erase(std::find(H->allocs.begin(), H->allocs.end(), H->d_run_args)); }
@@ -1256,17 +1268,6 @@ int fde1d_run(int batch, int n, const double* alpha, double h, double dt, int K,
   ra.K = K;
   ra.smem_doubles = (int)(H->step_smem / sizeof(double));
   CU(cudaFuncSetAttribute(k_run, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)H->step_smem));
-  static unsigned long long* run_trace = nullptr;
-  const long long run_trace_len = 4 + 4 * 262144;
-  if (getenv("FDE_TRACE_RUN")) {
-    if (!run_trace) CU(cudaMalloc(&run_trace, run_trace_len * sizeof(unsigned long long)));
-    CU(cudaMemsetAsync(run_trace, 0, run_trace_len * sizeof(unsigned long long), s));
-    ra.trace = run_trace; ra.trace_cap = 262144;
-    static unsigned long long* run_prof = nullptr;
-    if (!run_prof) CU(cudaMalloc(&run_prof, 16 * sizeof(unsigned long long)));
-    CU(cudaMemsetAsync(run_prof, 0, 16 * sizeof(unsigned long long), s));
-    ra.prof = run_prof;
-  }
   void* args[] = {&ra};
   { PROF("k_run"); CU(cudaLaunchCooperativeKernel((void*)k_run, dim3(H->step_grid), dim3(TR_THREADS), args, H->step_smem, s)); }
   LAUNCHED();
@@ -1274,12 +1275,17 @@ int fde1d_run(int batch, int n, const double* alpha, double h, double dt, int K,
     std::vector<unsigned long long> h(run_trace_len);
     CU(cudaStreamSynchronize(s));
     CU(cudaMemcpy(h.data(), ra.trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-    std::vector<unsigned long long> pf(16);
-    CU(cudaMemcpy(pf.data(), ra.prof, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    std::vector<unsigned long long> pf(32);
+    CU(cudaMemcpy(pf.data(), ra.prof, 32 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    {
+      const double c = (double)K * B * H->nleaf * 1965.0;
+      fprintf(stderr, "k_run A phases (us avg per leaf): build+gj0 %.2f lu+store %.2f gen %.2f fwd %.2f bwd+store %.2f sync %.2f\n",
+              pf[16] / c, pf[17] / c, pf[18] / c, pf[19] / c, pf[20] / c, pf[21] / c);
+    }
     for (int g = 0; g < 2; ++g) {
       const double c = (double)std::max(1ULL, pf[8 * g + 7]);
-      fprintf(stderr, "k_run %s phases (us avg over %llu): S %.2f v %.2f Xv %.2f LUwait %.2f solve %.2f\n",
-              g ? "final-only" : "B'", pf[8 * g + 7], pf[8 * g + 1] / c / 1965.0, pf[8 * g + 2] / c / 1965.0,
+      fprintf(stderr, "k_run %s phases (us avg over %llu): issue %.2f S %.2f v %.2f Xv %.2f LUwait %.2f solve %.2f\n",
+              g ? "final-only" : "B'", pf[8 * g + 7], pf[8 * g + 6] / c / 1965.0, pf[8 * g + 1] / c / 1965.0, pf[8 * g + 2] / c / 1965.0,
               pf[8 * g + 3] / c / 1965.0, pf[8 * g + 4] / c / 1965.0, pf[8 * g + 5] / c / 1965.0);
     }
     FILE* fo = fopen(getenv("FDE_TRACE_RUN"), "w");

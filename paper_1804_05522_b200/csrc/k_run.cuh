@@ -145,7 +145,7 @@ __device__ void leaf_rhs_final(const TrArgs& geo, const TrArgs* tp, const LeafAr
         o += k * xm;
       }
       cp_async_commit();
-      if (!lu_issued) { issue_lu(); lu_issued = true; cp_async_wait_group1(); } else cp_async_wait_all();
+      if (!lu_issued) { issue_lu(); lu_issued = true; RN_PH(6); cp_async_wait_group1(); } else { RN_PH(6); cp_async_wait_all(); }
       __syncthreads();
       RN_PH(1);
       {                                               // lane = row q of S_side, warp = column slice
