@@ -131,7 +131,7 @@ __device__ void leaf_rhs_final(const TrArgs& geo, const TrArgs* tp, const LeafAr
     while (m0 < L) {
       int m1 = m0, used = 0;
       while (m1 < L) {
-        const int sz = (a.xc[m1 + 1] - a.xc[m1]) * a.xc[m1];
+        const int sz = ((a.xc[m1 + 1] - a.xc[m1]) | 1) * a.xc[m1];   // (odd row pitch kp)
         if (m1 > m0 && used + sz > scap) break;
         used += sz; ++m1;
       }
@@ -141,8 +141,8 @@ __device__ void leaf_rhs_final(const TrArgs& geo, const TrArgs* tp, const LeafAr
         const int jn = leaf >> (L - m), side = (leaf >> (L - m - 1)) & 1;
         const double* gp = Sg + a.slev[m] + (long long)jn * 2 * k * xm + (long long)side * k * xm;
         for (int q = warp; q < k; q += LEAF_WARPS)
-          for (int c = lane; c < xm; c += 32) cp_async8(Ss + o + c * k + q, gp + q * xm + c);
-        o += k * xm;
+          for (int c = lane; c < xm; c += 32) cp_async8(Ss + o + c * (k | 1) + q, gp + q * xm + c);
+        o += (k | 1) * xm;
       }
       cp_async_commit();
       if (!lu_issued) { issue_lu(); lu_issued = true; RN_PH(6); cp_async_wait_group1(); } else { RN_PH(6); cp_async_wait_all(); }
@@ -153,7 +153,8 @@ __device__ void leaf_rhs_final(const TrArgs& geo, const TrArgs* tp, const LeafAr
         double* vp = part;                            // [8 warps][32 rows] partial sums
         for (int m = m0; m < m1; ++m) {
           const int xm = a.xc[m], k = a.xc[m + 1] - xm;
-          const double* St = Ss + o2;                 // [xm][k]
+          const int kp = k | 1;                      // odd pitch: conflict-free stores and loads
+          const double* St = Ss + o2;                 // [xm][kp]
           const int cw = (xm + LEAF_WARPS - 1) / LEAF_WARPS, c0 = warp * cw, c1 = min(xm, c0 + cw);
           for (int q0 = 0; q0 < k; q0 += 32) {
             const int q = q0 + lane;
@@ -162,10 +163,10 @@ __device__ void leaf_rhs_final(const TrArgs& geo, const TrArgs* tp, const LeafAr
               int c = c0;
 #pragma unroll 2
               for (; c + 3 < c1; c += 4) {
-                a0 = fma(St[c * k + q], vs[c], a0); a1 = fma(St[(c + 1) * k + q], vs[c + 1], a1);
-                a2 = fma(St[(c + 2) * k + q], vs[c + 2], a2); a3 = fma(St[(c + 3) * k + q], vs[c + 3], a3);
+                a0 = fma(St[c * kp + q], vs[c], a0); a1 = fma(St[(c + 1) * kp + q], vs[c + 1], a1);
+                a2 = fma(St[(c + 2) * kp + q], vs[c + 2], a2); a3 = fma(St[(c + 3) * kp + q], vs[c + 3], a3);
               }
-              for (; c < c1; ++c) a0 = fma(St[c * k + q], vs[c], a0);
+              for (; c < c1; ++c) a0 = fma(St[c * kp + q], vs[c], a0);
             }
             vp[warp * 32 + lane] = (a0 + a1) + (a2 + a3);
             __syncthreads();
@@ -177,7 +178,7 @@ __device__ void leaf_rhs_final(const TrArgs& geo, const TrArgs* tp, const LeafAr
             }
             __syncthreads();
           }
-          o2 += k * xm;
+          o2 += (k | 1) * xm;
         }
       }
       __syncthreads();

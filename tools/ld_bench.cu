@@ -33,6 +33,23 @@ __global__ void __launch_bounds__(256, 1) k_ld(const double* __restrict__ X, lon
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
     acc = sm[t];
+  } else if (MODE == 3) {                 // cp.async 8 B into smem, one wait
+    for (int e = t; e < NC * 128; e += 256) {
+      const int c = e >> 7, i = e & 127;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(su32(sm + c * 128 + i)), "l"(Xi + (long long)c * n + i) : "memory");
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    acc = sm[t];
+  } else if (MODE == 4) {                 // plain 8-byte loads, 32 in flight per thread
+    const int i = t & 127, h = t >> 7;
+    for (int c = h; c < NC; c += 2 * 32) {
+      double x[32];
+#pragma unroll
+      for (int u = 0; u < 32; ++u) x[u] = c + 2 * u < NC ? Xi[(long long)(c + 2 * u) * n + i] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 32; ++u) acc += x[u];
+    }
   } else {                                // TMA 1D bulk copies (1 KB per column), one mbarrier
     if (t == 0) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
@@ -62,9 +79,9 @@ int main(int argc, char** argv) {
   cudaMalloc(&X, n * NC * 8 * 4); cudaMemset(X, 0, n * NC * 8 * 4);
   cudaMalloc(&out, 4096); cudaMalloc(&cyc, 4096 * 8);
   void* flush; cudaMalloc(&flush, 512 << 20);
-  for (int mode = 0; mode < 3; ++mode)
+  for (int mode = 0; mode < 5; ++mode)
     for (int nct : {1, 16, 148}) {
-      auto f = mode == 0 ? k_ld<0> : mode == 1 ? k_ld<1> : k_ld<2>;
+      auto f = mode == 0 ? k_ld<0> : mode == 1 ? k_ld<1> : mode == 2 ? k_ld<2> : mode == 3 ? k_ld<3> : k_ld<4>;
       cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
       unsigned long long h[148];
       double best = 1e30, avg = 0;
@@ -77,7 +94,7 @@ int main(int argc, char** argv) {
         avg = a;
       }
       printf("mode %d (%s) ctas %3d: %.2f us per CTA for %d KB -> %.1f GB/s per SM  [%s]\n", mode,
-             mode == 0 ? "ld.v2 x24" : mode == 1 ? "cp.async16" : "TMA 1D", nct, avg / 1965.0, NC, NC * 1024 / (avg / 1965.0) / 1e3,
+             mode == 0 ? "ld.v2 x24" : mode == 1 ? "cp.async16" : mode == 2 ? "TMA 1D" : mode == 3 ? "cp.async8" : "ld.f64 x32", nct, avg / 1965.0, NC, NC * 1024 / (avg / 1965.0) / 1e3,
              cudaGetErrorString(cudaGetLastError()));
     }
   return 0;
