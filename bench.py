@@ -281,6 +281,64 @@ def measure_cfg5(dev, steps=4):
             "final_rank": int(Xu.shape[0]), "timing": "host wall clock around synchronous fde2d_step calls"}
 
 
+def measure_small(dev, name, reps=3):
+    """BASELINE configs[0] / configs[1] (latency-bound sizes): the whole K-step trajectory through
+    fde1d_run (refactor every step), CUDA events around the launch after a warm-up run."""
+    import torch
+    from paper_1804_05522_b200 import workloads as W
+    from paper_1804_05522_b200.hodlr import Fde1dStepper
+    wl = getattr(W, name)()
+    t = lambda a: torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device=dev)
+    DP, DM, F, U0 = t(wl.d_plus), t(wl.d_minus), t(wl.f), t(wl.u0)
+    st = Fde1dStepper(wl.n, wl.alpha, wl.h, wl.tol, wl.leaf, batch=wl.batch)
+    st.run(wl.dt, DP, DM, F, U0)
+    torch.cuda.synchronize()
+    best = None
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        st.run(wl.dt, DP, DM, F, U0)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b)
+        best = ms if best is None else min(best, ms)
+    ranks = st.ranks()
+    st.close()
+    return {"workload": "%s: n=%d alpha=%g leaf %d tol %g, %d steps (BASELINE configs)" % (
+                name, wl.n, float(wl.alpha[0]), wl.leaf, wl.tol, wl.K),
+            "metric": "time-steps/s", "value": wl.K / (best / 1e3), "us_per_step": 1e3 * best / wl.K,
+            "ranks": ranks, "timing": "CUDA events around one fde1d_run of all K steps, best of %d" % reps}
+
+
+def task_profile(st, wl, DPK, DMK, F, U0, K=16):
+    """Per-task durations inside k_run (untimed diagnostic run with FDE_TRACE_RUN): mean us per
+    task and SM-us per step / 148 for the leaf tasks A, B, B' and the tree levels."""
+    import collections
+    import tempfile
+    import torch
+    path = os.path.join(tempfile.gettempdir(), "fde_run_trace_%d.txt" % os.getpid())
+    os.environ["FDE_TRACE_RUN"] = path
+    try:
+        st.run(wl.dt, DPK[:K], DMK[:K], F, U0)
+        torch.cuda.synchronize()
+    finally:
+        del os.environ["FDE_TRACE_RUN"]
+    rows = [tuple(int(x) for x in ln.split()) for ln in open(path)]
+    os.remove(path)
+    names = {100: "A", 101: "B", 102: "B'", 103: "final"}
+    by = collections.defaultdict(list)
+    t0, t1 = min(r[0] for r in rows), max(r[1] for r in rows)
+    nsm = len(set(r[3] for r in rows))
+    for s_, e_, code, sm in rows:
+        kind = code % 1000
+        by[names.get(kind, "L%d" % kind)].append((e_ - s_) / 1e3)
+    busy = sum(sum(v) for v in by.values())
+    return {"steps": K, "us_per_step": (t1 - t0) / 1e3 / K, "sm_busy": busy / ((t1 - t0) / 1e3 * nsm),
+            "tasks": {k: {"n": len(v), "mean_us": sum(v) / len(v), "sm_us_per_step_per_sm": sum(v) / nsm / K}
+                      for k, v in sorted(by.items())},
+            "note": "diagnostic run with per-task globaltimer stamps (not the timed run)"}
+
+
 def run_ours(args, world, rank, local):
     import torch
     from paper_1804_05522_b200 import build as B
@@ -472,7 +530,16 @@ def run_ours(args, world, rank, local):
             "clocks": clk, "e2e": e2e, "roofline": roof, "kernels": kern,
             "other_variant": other}
     if not args.no_extra:
+        try:
+            line["task_profile"] = task_profile(st, wl, DPK, DMK, F, U0)
+        except Exception as e:
+            line["task_profile"] = {"error": str(e)[:200]}
         extra = {}
+        for name in ("cfg1", "cfg2"):
+            try:
+                extra[name] = measure_small(dev, name)
+            except Exception as e:
+                extra[name] = {"error": str(e)[:200]}
         try:
             extra["cfg4"] = measure_cfg4(dev, world, rank)
         except Exception as e:                              # reported, not fatal for the headline
