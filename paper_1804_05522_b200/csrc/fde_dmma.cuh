@@ -28,3 +28,19 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {   // 
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_group1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// Contiguous run of `count` doubles -> shared memory with 16-byte cp.async for the aligned body
+// (8-byte copies for an odd head / tail).  dst_base: 16-byte aligned with one spare double; the
+// run lands at dst_base + (src parity), which is returned (the same for every thread).
+__device__ __forceinline__ double* cp_contig_dst(double* dst_base, const double* src) {
+  return dst_base + (int)((reinterpret_cast<unsigned long long>(src) >> 3) & 1);
+}
+__device__ __forceinline__ void cp_contig(double* dst_base, const double* src, int count, int t, int nt) {
+  double* dst = cp_contig_dst(dst_base, src);
+  const int h = (int)(dst - dst_base);               // 1: odd head element
+  if (h && t == 0 && count > 0) cp_async8(dst, src);
+  const int body = (count - h) >> 1;
+  for (int e = t; e < body; e += nt) cp_async16(dst + h + 2 * e, src + h + 2 * e);
+  const int done = h + 2 * body;
+  if (done < count && t == nt - 1) cp_async8(dst + done, src + done);
+}

@@ -541,7 +541,7 @@ static int tree_layout(fde_hodlr* H) {
   g.off_T = (int)o;                                   // union { T + Z (S phase), U (Q update) }
   g.off_Z = (int)(o + (long long)kp * g.lds);
   g.off_U = (int)o;
-  o += std::max((long long)kp * g.lds + 2LL * H->kmax * NC, 2LL * 2 * TR_SUB * NC);
+  o += std::max((long long)kp * g.lds + 2LL * H->kmax * NC, 2LL * 2 * (TR_SUB * NC + 2));
   // final pass: 4 v vectors + max(4 warps x 2 S buffers, X block + partials)
   const long long fin = 4LL * round_up(NC, 8) + std::max(8LL * H->kmax * NC, (long long)NC * 128 + 256);
   const size_t bytes = (size_t)std::max(o, fin) * sizeof(double);
@@ -1246,10 +1246,10 @@ int fde1d_run(int batch, int n, const double* alpha, double h, double dt, int K,
     CU(cudaMemsetAsync(run_trace, 0, run_trace_len * sizeof(unsigned long long), s));
     ra.trace = run_trace; ra.trace_cap = 262144;
     static unsigned long long* run_prof = nullptr;
-    if (!run_prof) CU(cudaMalloc(&run_prof, 32 * sizeof(unsigned long long)));
-    CU(cudaMemsetAsync(run_prof, 0, 32 * sizeof(unsigned long long), s));
+    if (!run_prof) CU(cudaMalloc(&run_prof, 1200 * sizeof(unsigned long long)));
+    CU(cudaMemsetAsync(run_prof, 0, 1200 * sizeof(unsigned long long), s));
     ra.prof = run_prof;
-    for (int m = 0; m < K; ++m) H->run_las[m].prof = run_prof + 16;
+    for (int m = 0; m < K; ++m) { H->run_las[m].prof = run_prof + 16; H->run_tas[m].trace = run_prof; }
   }
   const size_t args_bytes = (size_t)K * (sizeof(LeafArgs) + sizeof(TrArgs));
   if (args_bytes > H->run_args_cap) {
@@ -1275,8 +1275,14 @@ int fde1d_run(int batch, int n, const double* alpha, double h, double dt, int K,
     std::vector<unsigned long long> h(run_trace_len);
     CU(cudaStreamSynchronize(s));
     CU(cudaMemcpy(h.data(), ra.trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-    std::vector<unsigned long long> pf(32);
-    CU(cudaMemcpy(pf.data(), ra.prof, 32 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    std::vector<unsigned long long> pf(1200);
+    CU(cudaMemcpy(pf.data(), ra.prof, 1200 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    for (int g = 0; g < 2; ++g) {
+      const unsigned long long* q = pf.data() + 1100 + 8 * g;
+      const double c = (double)std::max(1ULL, q[7]) * 1965.0;
+      fprintf(stderr, "k_run tree %s units (%llu): stage %.2f sc+T %.2f gj %.2f S %.2f Qupd %.2f us\n",
+              g ? "upper" : "bottom", q[7], q[0] / c, q[1] / c, q[2] / c, q[3] / c, q[4] / c);
+    }
     {
       const double c = (double)K * B * H->nleaf * 1965.0;
       fprintf(stderr, "k_run A phases (us avg per leaf): build+gj0 %.2f lu+store %.2f gen %.2f fwd %.2f bwd+store %.2f sync %.2f\n",

@@ -209,18 +209,23 @@ __device__ void tr_unit(const TrArgs& a, double* sm, int inst, int m, int j, int
   const int rch = m > 0 ? round_up((nrow + a.rc[m] - 1) / a.rc[m], 8) : 0;
   const int ra = chunk * rch, rb = m > 0 ? min(nrow, ra + rch) : 0;
   const int nsub = rb > ra ? (rb - ra + TR_SUB - 1) / TR_SUB : 0;
+  // sub-chunk buffers: [U1 | U2] x 2, each TR_SUB x ncol1 (+2 spare doubles: 16-byte copies)
+  const int usz = TR_SUB * ncol1 + 2;
+  auto ubuf = [&](int sc, int which) -> double* {
+    const int rs = ra + sc * TR_SUB;
+    return cp_contig_dst(Ub + (sc & 1) * 2 * usz + which * usz, (which ? Q2 : Q1) + (long long)rs * ncol1);
+  };
   auto issue_sub = [&](int sc) {
     const int rs = ra + sc * TR_SUB, nr = min(TR_SUB, rb - rs);
-    double* U1 = Ub + (sc & 1) * 2 * TR_SUB * ncol1;
-    double* U2 = U1 + TR_SUB * ncol1;
-    const double* g1 = Q1 + (long long)rs * ncol1;
-    const double* g2 = Q2 + (long long)rs * ncol1;
-    for (int e = t; e < nr * ncol1; e += TR_THREADS) { cp_async8(U1 + e, g1 + e); cp_async8(U2 + e, g2 + e); }
+    cp_contig(Ub + (sc & 1) * 2 * usz, Q1 + (long long)rs * ncol1, nr * ncol1, t, TR_THREADS);
+    cp_contig(Ub + (sc & 1) * 2 * usz + usz, Q2 + (long long)rs * ncol1, nr * ncol1, t, TR_THREADS);
     cp_async_commit();
   };
-  const bool tdbg = a.trace && blockIdx.x == 0 && t == 0;
+  const bool tdbg = a.trace && t == 0;
   long long tcl = clock64();
-#define TPH(i) do { if (tdbg) { const long long t_ = clock64(); a.trace[1100 + (i)] += t_ - tcl; tcl = t_; } } while (0)
+  const int tsl = 1100 + (m == a.L - 1 ? 0 : 8);   // phase clocks: bottom level / the others
+#define TPH(i) do { if (tdbg) { const long long t_ = clock64(); atomicAdd(a.trace + tsl + (i), (unsigned long long)(t_ - tcl)); tcl = t_; } } while (0)
+  if (tdbg) atomicAdd(a.trace + tsl + 7, 1ULL);
   // 1. stage the level-m rows of both children (+ the first Q sub-chunk, in flight meanwhile)
   for (int e = t; e < k * ncol1; e += TR_THREADS) {
     cp_async8(Z1 + e, Q1 + (long long)r0 * ncol1 + e);
@@ -308,8 +313,8 @@ __device__ void tr_unit(const TrArgs& a, double* sm, int inst, int m, int j, int
     if (sc + 1 < nsub) { issue_sub(sc + 1); cp_async_wait_group1(); } else cp_async_wait_all();
     __syncthreads();
     const int rs = ra + sc * TR_SUB, nr = min(TR_SUB, rb - rs);
-    const double* U1 = Ub + (sc & 1) * 2 * TR_SUB * ncol1;
-    const double* U2 = U1 + TR_SUB * ncol1;
+    const double* U1 = ubuf(sc, 0);
+    const double* U2 = ubuf(sc, 1);
     // warp -> m-tile (warp & 3) x n-tiles (warp >> 2) + 2 i: A fragment reused TR_NT times
     const int mt = warp & 3, nt0 = warp >> 2, NT8 = xmp >> 3;
     const int r = 8 * mt + gid;
