@@ -541,7 +541,7 @@ static int tree_layout(fde_hodlr* H) {
   g.off_T = (int)o;                                   // union { T + Z (S phase), U (Q update) }
   g.off_Z = (int)(o + (long long)kp * g.lds);
   g.off_U = (int)o;
-  o += std::max((long long)kp * g.lds + 2LL * H->kmax * NC, 2LL * 2 * (TR_SUB * NC + 2));
+  o += std::max((long long)kp * g.lds + 2LL * H->kmax * NC, 2LL * TR_STG * (TR_SUB * NC + 2));
   // final pass: 4 v vectors + max(4 warps x 2 S buffers, X block + partials)
   const long long fin = 4LL * round_up(NC, 8) + std::max(8LL * H->kmax * NC, (long long)NC * 128 + 256);
   const size_t bytes = (size_t)std::max(o, fin) * sizeof(double);

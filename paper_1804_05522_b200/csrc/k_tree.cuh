@@ -66,8 +66,11 @@ __device__ __forceinline__ void tr_grid_barrier(unsigned* bar, unsigned target) 
   __syncthreads();
 }
 
-#define TR_SUB 32                // Q_mu rows per streamed sub-chunk (double buffered)
-#define TR_NT 12                 // n-tiles per warp in the Q update (2 warp columns x 12 = 24 n-tiles)
+#define TR_SUB 16                // Q_mu rows per streamed sub-chunk
+#define TR_STG 4                 // sub-chunk pipeline stages (3 sub-chunks in flight)
+#define TR_MW (TR_SUB / 8)       // m-tiles per sub-chunk
+#define TR_NS (8 / TR_MW)        // warps per m-tile (n-tile stride)
+#define TR_NT (24 / TR_NS)       // n-tiles per warp in the Q update (24 n-tiles = 192 columns)
 
 // O[q][c] = Cin[q][c] + sgn * sum_p A[q][p] B[p][c]  (q < M, c < N; Cin may be null = 0).
 // Row-major shared-memory operands.  A warp item = 4 rows x 32 consecutive columns (lane =
@@ -198,7 +201,7 @@ __device__ void tr_unit(const TrArgs& a, double* sm, int inst, int m, int j, int
   double* Ts = sm + a.off_T;      // k x xm scratch (S_bot before it moves into Ss)
   double* Z1 = sm + a.off_Z;      // level-m rows of Q_c1 / Q_c2 (k x ncol1 each)
   double* Z2 = Z1 + k * ncol1;
-  double* Ub = sm + a.off_U;      // 2 buffers x [Q_c1 rows | Q_c2 rows] (TR_SUB x ncol1 each);
+  double* Ub = sm + a.off_U;      // TR_STG buffers x [Q_c1 rows | Q_c2 rows] (TR_SUB x ncol1 each);
                                   // aliases Ts and Z: streamed only after the S phase
   const long long qs1 = (long long)(ncol1 - 1) * ncol1;
   const double* Q1 = a.Q + (long long)inst * a.qinst + a.qlev[m + 1] + (long long)(2 * j) * qs1;
@@ -209,16 +212,16 @@ __device__ void tr_unit(const TrArgs& a, double* sm, int inst, int m, int j, int
   const int rch = m > 0 ? round_up((nrow + a.rc[m] - 1) / a.rc[m], 8) : 0;
   const int ra = chunk * rch, rb = m > 0 ? min(nrow, ra + rch) : 0;
   const int nsub = rb > ra ? (rb - ra + TR_SUB - 1) / TR_SUB : 0;
-  // sub-chunk buffers: [U1 | U2] x 2, each TR_SUB x ncol1 (+2 spare doubles: 16-byte copies)
+  // sub-chunk buffers: [U1 | U2] x TR_STG, each TR_SUB x ncol1 (+2 spare doubles: 16-byte copies)
   const int usz = TR_SUB * ncol1 + 2;
   auto ubuf = [&](int sc, int which) -> double* {
     const int rs = ra + sc * TR_SUB;
-    return cp_contig_dst(Ub + (sc & 1) * 2 * usz + which * usz, (which ? Q2 : Q1) + (long long)rs * ncol1);
+    return cp_contig_dst(Ub + (sc % TR_STG) * 2 * usz + which * usz, (which ? Q2 : Q1) + (long long)rs * ncol1);
   };
   auto issue_sub = [&](int sc) {
     const int rs = ra + sc * TR_SUB, nr = min(TR_SUB, rb - rs);
-    cp_contig(Ub + (sc & 1) * 2 * usz, Q1 + (long long)rs * ncol1, nr * ncol1, t, TR_THREADS);
-    cp_contig(Ub + (sc & 1) * 2 * usz + usz, Q2 + (long long)rs * ncol1, nr * ncol1, t, TR_THREADS);
+    cp_contig(Ub + (sc % TR_STG) * 2 * usz, Q1 + (long long)rs * ncol1, nr * ncol1, t, TR_THREADS);
+    cp_contig(Ub + (sc % TR_STG) * 2 * usz + usz, Q2 + (long long)rs * ncol1, nr * ncol1, t, TR_THREADS);
     cp_async_commit();
   };
   const bool tdbg = a.trace && t == 0;
@@ -306,24 +309,29 @@ __device__ void tr_unit(const TrArgs& a, double* sm, int inst, int m, int j, int
   TPH(3);
   if (nsub == 0) { __syncthreads(); return; }
   // 5. Q_mu rows [ra, rb) = Q1 + Q2 - [Q1 m-cols | Q2 m-cols] [S_top; S_bot], streamed in
-  //    sub-chunks of TR_SUB rows (the next sub-chunk's copies overlap this one's DMMA)
+  //    sub-chunks of TR_SUB rows (TR_STG - 1 sub-chunks' copies in flight during one's DMMA)
   double* Qo = a.Q + (long long)inst * a.qinst + a.qlev[m] + (long long)j * (long long)nrow * xm;
-  issue_sub(0);
+  for (int sc = 0; sc < TR_STG - 1 && sc < nsub; ++sc) issue_sub(sc);
   for (int sc = 0; sc < nsub; ++sc) {
-    if (sc + 1 < nsub) { issue_sub(sc + 1); cp_async_wait_group1(); } else cp_async_wait_all();
+    if (sc + TR_STG - 1 < nsub) issue_sub(sc + TR_STG - 1);
+    const int ahead = min(TR_STG - 1, nsub - 1 - sc);   // groups allowed to stay in flight
+    if (ahead >= 3) asm volatile("cp.async.wait_group 3;" ::: "memory");
+    else if (ahead == 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
+    else if (ahead == 1) cp_async_wait_group1();
+    else cp_async_wait_all();
     __syncthreads();
     const int rs = ra + sc * TR_SUB, nr = min(TR_SUB, rb - rs);
     const double* U1 = ubuf(sc, 0);
     const double* U2 = ubuf(sc, 1);
-    // warp -> m-tile (warp & 3) x n-tiles (warp >> 2) + 2 i: A fragment reused TR_NT times
-    const int mt = warp & 3, nt0 = warp >> 2, NT8 = xmp >> 3;
+    // warp -> m-tile (warp % TR_MW) x n-tiles (warp / TR_MW) + TR_NS i: A fragment reused TR_NT times
+    const int mt = warp % TR_MW, nt0 = warp / TR_MW, NT8 = xmp >> 3;
     const int r = 8 * mt + gid;
     const bool rok = r < nr;
     if (8 * mt < nr) {
       double d[TR_NT][2];
 #pragma unroll
       for (int i = 0; i < TR_NT; ++i) {
-        const int c = 8 * (nt0 + 2 * i) + 2 * tig;
+        const int c = 8 * (nt0 + TR_NS * i) + 2 * tig;
         d[i][0] = (rok && c < xm) ? U1[r * ncol1 + c] + U2[r * ncol1 + c] : 0.0;
         d[i][1] = (rok && c + 1 < xm) ? U1[r * ncol1 + c + 1] + U2[r * ncol1 + c + 1] : 0.0;
       }
@@ -333,13 +341,13 @@ __device__ void tr_unit(const TrArgs& a, double* sm, int inst, int m, int j, int
         const double av = (rok && q < 2 * k) ? -(q < k ? U1[r * ncol1 + xm + q] : U2[r * ncol1 + xm + q - k]) : 0.0;
 #pragma unroll
         for (int i = 0; i < TR_NT; ++i)
-          if (nt0 + 2 * i < NT8) dmma884(d[i][0], d[i][1], av, bp[k0 * lds + 16 * i]);
+          if (nt0 + TR_NS * i < NT8) dmma884(d[i][0], d[i][1], av, bp[k0 * lds + 8 * TR_NS * i]);
       }
       if (rok) {
         double* qr = Qo + (long long)(rs + r) * xm;
 #pragma unroll
         for (int i = 0; i < TR_NT; ++i) {
-          const int c = 8 * (nt0 + 2 * i) + 2 * tig;
+          const int c = 8 * (nt0 + TR_NS * i) + 2 * tig;
           if (c < xm) qr[c] = d[i][0];
           if (c + 1 < xm) qr[c + 1] = d[i][1];
         }
