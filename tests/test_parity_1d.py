@@ -321,6 +321,54 @@ def test_pipelined_run_matches_steps_and_oracle(n, alpha, leaf, batch):
     st.close(); st2.close()
 
 
+RUN_EDGE = [  # n, alpha, leaf, K, batch
+    (300, 1.3, 40, 3, 1),      # ragged leaves, odd leaf offsets
+    (1001, 1.9, 100, 4, 2),    # odd n (misaligned row pairs), batch
+    (513, 1.1, 16, 3, 1),      # deep tree, small leaves
+    (100, 1.5, 128, 3, 1),     # single leaf (L = 0): device fallback to fused steps
+    (1, 1.5, 2, 2, 1),         # n = 1
+    (257, 2.0, 32, 3, 1),      # classical limit
+    (1000, 1.7, 64, 1, 1),     # K = 1 (only the finals of step K after the first step)
+]
+
+
+@gpu
+@pytest.mark.parametrize("n,alpha,leaf,K,batch", RUN_EDGE)
+def test_pipelined_run_edge_cases(n, alpha, leaf, K, batch):
+    """fde1d_run on ragged / odd / degenerate trees and K = 1: every step against the dense
+    oracle trajectory (each side propagates its own state)."""
+    wl = W.make_1d(n, np.linspace(alpha, min(alpha + 0.1, 2.0), batch), leaf, 1e-12, K=K, batch=batch)
+    st = _stepper(wl)
+    DP = torch.stack([_t(wl.coeffs(m)[0]) for m in range(1, K + 1)])
+    DM = torch.stack([_t(wl.coeffs(m)[1]) for m in range(1, K + 1)])
+    F = torch.stack([_t(wl.source(m)) for m in range(1, K + 1)])
+    out = st.run(wl.dt, DP, DM, F, _t(wl.u0)).cpu().numpy()
+    uo = wl.u0
+    for m in range(1, K + 1):
+        uo = np.stack([_oracle_step(wl, m, uo, b) for b in range(batch)])
+        for b in range(batch):
+            assert _rel(out[m - 1, b], uo[b]) <= 1e-8, (m, b, _rel(out[m - 1, b], uo[b]))
+    st.close()
+
+
+@gpu
+def test_pipelined_run_invariant_coefficients_and_dt0():
+    """Stride-0 coefficients / source (one time level for all K steps) equal the explicit
+    K-level arrays bitwise; dt = 0 gives u^(m) = u0 (A = I)."""
+    wl = W.make_1d(777, 1.6, 64, 1e-12, K=4)
+    st = _stepper(wl)
+    dp, dm = wl.coeffs(1)
+    f = wl.source(1)
+    u0 = _t(np.random.default_rng(11).standard_normal((1, wl.n)))
+    one = st.run(wl.dt, _t(dp)[None], _t(dm)[None], _t(f)[None], u0)
+    rep = lambda a: _t(a)[None].repeat(4, 1, 1).contiguous()
+    full = st.run(wl.dt, rep(dp), rep(dm), rep(f), u0)
+    assert torch.equal(one, full)
+    z = st.run(0.0, rep(dp), rep(dm), rep(f), u0)
+    assert torch.allclose(z, u0[None].expand_as(z), rtol=0, atol=1e-14)
+    st.close()
+
+
 @gpu
 def test_cfg3_pipelined_run_backward_error():
     """cfg3 at full size through fde1d_run (the launch bench.py times): eta <= 1e-10 per step."""
