@@ -1203,6 +1203,7 @@ int fde1d_run(int batch, int n, const double* alpha, double h, double dt, int K,
   ra.heads = reinterpret_cast<unsigned*>(H->d_runctr);
   ra.done = H->d_runctr + 4;
   ra.rq = H->d_runrq;
+  ra.rq_cap = nrq;
   // per-step argument blocks (k_run.cuh RunArgs), copied to the device once per call
   LeafArgs la{};
   la.tree = H->tree; la.mode = 0; la.shift = H->shift; la.cfac = H->d_cfac; la.dt = dt;
@@ -1285,8 +1286,8 @@ int fde1d_run(int batch, int n, const double* alpha, double h, double dt, int K,
     }
     {
       const double c = (double)K * B * H->nleaf * 1965.0;
-      fprintf(stderr, "k_run A phases (us avg per leaf): build+gj0 %.2f lu+store %.2f gen %.2f fwd %.2f bwd+store %.2f sync %.2f\n",
-              pf[16] / c, pf[17] / c, pf[18] / c, pf[19] / c, pf[20] / c, pf[21] / c);
+      fprintf(stderr, "k_run A phases (us avg per leaf): build+gj0 %.2f lu+store %.2f panel %.2f\n",
+              pf[16] / c, pf[17] / c, pf[20] / c);
     }
     for (int g = 0; g < 2; ++g) {
       const double c = (double)std::max(1ULL, pf[8 * g + 7]);

@@ -43,6 +43,7 @@ struct RunArgs {
   int smem_doubles;              // dynamic shared memory of the launch
   unsigned* heads;               // [0] tree units done, [1] leaf tickets, [2] rq tail, [3] rq head
   unsigned long long* rq;        // ready queue: task id + 1 per slot (zeroed), K * units per step
+  long long rq_cap;              // slots
   int* done; long long per_step; // step m counters: done + m * per_step (m = 0..K-1)
   long long o_A, o_R, o_pair, o_lvl[LMAX], o_kid[LMAX];   // o_kid[m]: completed children of level-m nodes
   unsigned long long* trace;     // optional (FDE_TRACE_RUN): [0] count, then [start,end,code,sm]
@@ -332,7 +333,8 @@ k_run(const RunArgs ra) {
           if (v) { q = 0; idx = (long long)(v - 1); iou = -1; break; }
         } else if (vh[2] > vh[3]) {
           iou = atomicAdd(ra.heads + 3, 1u);
-          continue;
+          if (iou >= ra.rq_cap) iou = -1;             // (a race past the last slot: never filled)
+          else continue;
         }
         if (held < 0 && !leaf_out) {
           const unsigned l = atomicAdd(ra.heads + 1, 1u);

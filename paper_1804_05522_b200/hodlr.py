@@ -122,12 +122,13 @@ class Fde1dStepper:
                                      ctypes.byref(self._cache), _stream(stream)))
         return u_next
 
-    def run(self, dt, d_plus, d_minus, f, u0, u_out=None, flags=0, stream=None):
+    def run(self, dt, d_plus, d_minus, f, u0, u_out=None, flags=0, stream=None, K=None):
         """K steps in one pipelined launch (fde1d_run).  d_plus, d_minus, f: CUDA float64
-        (K, batch, n) -- or (1, batch, n) for time-invariant data; u0 (batch, n).
-        Returns u_out (K, batch, n): every step's solution."""
+        (K, batch, n) -- or (1, batch, n) for time-invariant data; u0 (batch, n).  K defaults
+        to the largest leading dimension.  Returns u_out (K, batch, n): every step's solution."""
         cnt = self.batch * self.n
-        K = max(d_plus.shape[0], f.shape[0])
+        if K is None:
+            K = max(d_plus.shape[0], f.shape[0])
         for name, t in (("d_plus", d_plus), ("d_minus", d_minus), ("f", f)):
             if t.shape[0] not in (1, K) or t[0].numel() != cnt:
                 raise ValueError("%s must be (K or 1, batch, n)" % name)

@@ -360,7 +360,7 @@ def test_pipelined_run_invariant_coefficients_and_dt0():
     dp, dm = wl.coeffs(1)
     f = wl.source(1)
     u0 = _t(np.random.default_rng(11).standard_normal((1, wl.n)))
-    one = st.run(wl.dt, _t(dp)[None], _t(dm)[None], _t(f)[None], u0)
+    one = st.run(wl.dt, _t(dp)[None], _t(dm)[None], _t(f)[None], u0, K=4)
     rep = lambda a: _t(a)[None].repeat(4, 1, 1).contiguous()
     full = st.run(wl.dt, rep(dp), rep(dm), rep(f), u0)
     assert torch.equal(one, full)
