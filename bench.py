@@ -244,10 +244,32 @@ def measure_cfg4(dev, world, rank, steps=16):
     go(False)
     v_reuse, ms_reuse = go(False)
     v_ref, ms_ref = go(True)
+
+    def go_run():                                   # refactor every step, K steps in one k_run
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        a.record()
+        st.run(wl.dt, DP[None], DM[None], F[None], u[0], K=steps)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b)
+        if world > 1:
+            x = torch.tensor([ms], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(x, op=torch.distributed.ReduceOp.MAX)
+            ms = float(x.item())
+        return wl.batch * steps / (ms / 1e3), ms
+    try:
+        go_run()
+        v_run, ms_run = go_run()
+    except Exception as e:                          # (memory for the second buffer set)
+        v_run, ms_run = None, str(e)[:120]
     st.close()
     return {"workload": "cfg4: 512 x n=8192, alpha_i~U(1.1,1.9), 16 steps, leaf 128, tol 1e-13 (R18)",
             "metric": "instance-steps/s", "value_factor_once": v_reuse, "ms_16_steps_factor_once": ms_reuse,
             "value_refactor_every_step": v_ref, "ms_16_steps_refactor": ms_ref,
+            "value_refactor_pipelined_run": v_run, "ms_16_steps_refactor_pipelined_run": ms_run,
             "sharding": "%d instances per rank (shard.py), no data-path collective" % run.count}
 
 
