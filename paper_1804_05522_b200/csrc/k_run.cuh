@@ -6,7 +6,7 @@
 //   B  : projection Q[:, 1:] = V_all^T X[:, 1:]                           (leaf_proj_task)
 //   B' : u^(m-1) on the leaf's rows = X^(m-1) v^(m-1) (the "final" of step m-1, see k_tree.cuh),
 //        x0 = A_leaf^{-1}(u^(m-1) + dt f^(m)) with the stored LU, X[:, 0] = x0,
-//        Q[:, 0] = V_all^T x0                                             (leaf_rhs_final below)
+//        Q[:, 0] = V_all^T x0                                             (leaf_rhs_final, k_final.cuh)
 // and the SMW tree units of every level follow (k_tree.cuh tr_unit).  A virtual step K holds
 // the last finals (u^(K-1)).  Only B' and the tree lie on the step-to-step chain; A and B of
 // step m+1 fill the SMs while the tree of step m climbs its latency-bound upper levels.
@@ -29,9 +29,8 @@
 // Same arithmetic as k_step except the rhs column: its leaf solve is a plain FMA block sweep
 // (not the DMMA stripe) and u^(m-1) is formed per leaf.
 #pragma once
-#include "k_step.cuh"
+#include "k_step.cuh"   // (k_final.cuh: leaf_rhs_final, rn_copy)
 
-#define RN_FRONT (LEAF_MAX + NCOL_MAX + 4 * LEAF_MAX + 32)   // b | v | part[4] | z
 
 struct RunArgs {
   // per-step argument blocks in device memory (host-filled): step m's d+-, f, u^(m-1), u^(m)
@@ -69,15 +68,6 @@ __device__ __forceinline__ bool rn_leaf_ready(const RunArgs& ra, long long n_lea
   return step < 1 || rn_ready(dn - ra.per_step + ra.o_lvl[0] + inst, a.rc[0]);
 }
 
-// Block copy of an argument struct into shared memory (whole CTA; ends with a barrier).
-template <class T>
-__device__ __forceinline__ void rn_copy(T* dst, const T* src) {
-  static_assert(sizeof(T) % 8 == 0, "argument block size");
-  for (int i = threadIdx.x; i < (int)(sizeof(T) / 8); i += blockDim.x)
-    reinterpret_cast<unsigned long long*>(dst)[i] = reinterpret_cast<const unsigned long long*>(src)[i];
-  __syncthreads();
-}
-
 // Tree task ids: step (16 bits) | level m (8) | chunk (8) | node jj = inst 2^m + j (32).
 __device__ __forceinline__ long long rn_tid(int step, int m, int chunk, long long jj) {
   return ((long long)step << 48) | ((long long)m << 40) | ((long long)chunk << 32) | jj;
@@ -93,211 +83,6 @@ __device__ __forceinline__ long long rn_release(const RunArgs& ra, int step, int
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(ra.rq + slot), "l"(v) : "memory");
   }
   return rn_tid(step, m, 0, jj);
-}
-
-// B' (and the finals of step K): see the header.  geo: tree geometry; tp = step m-1's tree
-// arguments (X^(m-1), S^(m-1), u^(m-1) output) or null at m = 0; la = step m's leaf arguments
-// or null at m = K.
-__device__ void leaf_rhs_final(const TrArgs& geo, const TrArgs* tp, const LeafArgs* la, double* sm,
-                               int smem_doubles, int inst, int leaf, unsigned long long* prof = nullptr) {
-  const TrArgs& a = geo;
-  long long ph_t = clock64();
-#define RN_PH(i) do { if (prof && threadIdx.x == 0) { const long long t_ = clock64(); \
-    atomicAdd(prof + (la ? 0 : 8) + (i), (unsigned long long)(t_ - ph_t)); ph_t = t_; } } while (0)
-  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  const int L = a.L, n = a.n, NC = a.xc[L];
-  const int r0 = a.leaf_r0[leaf], s = a.leaf_n[leaf], sp = round_up(s, 32), nb = sp >> 5;
-  double* bs = sm;                                    // b, then x0
-  double* vs = bs + LEAF_MAX;                         // v (NC)
-  double* part = vs + NCOL_MAX;                       // [4][128]
-  double* zs = part + 4 * LEAF_MAX;                   // [32]
-  double* LUs = sm + RN_FRONT;                        // [sp x sp] column-major, ld = sp
-  double* Ss = LUs + LEAF_MAX * LEAF_MAX;             // S_side blocks of a batch of levels
-  PanelCol* pcd = reinterpret_cast<PanelCol*>(Ss);   // then: V-column descriptors (NC - 1)
-  const int scap = smem_doubles - RN_FRONT - LEAF_MAX * LEAF_MAX;
-  // ---- the first batch of S blocks, then the stored LU, in flight while the final is formed
-  auto issue_lu = [&]() {
-    const double* LUg = la->LU + (long long)inst * la->lustride + (long long)leaf * LEAF_SLOT;
-    for (int e = 2 * t; e < sp * sp; e += 2 * LEAF_THREADS) cp_async16(LUs + e, LUg + e);
-    cp_async_commit();
-  };
-  if (tp) {
-    // ---- v = M_{L-1} .. M_0 e_0,  M_m: v[m-cols] = -S_side(m) v[< xc_m]   (k_tree.cuh);
-    //      S_side(m) (k x xm, row-major in HBM) is staged transposed: lane q reads row q
-    //      conflict-free while the warp walks the columns
-    for (int c = t; c < NC; c += LEAF_THREADS) vs[c] = c == 0 ? 1.0 : 0.0;
-    const double* Sg = tp->Sst + (long long)inst * tp->sinst;
-    int m0 = 0;
-    bool lu_issued = la == nullptr;
-    while (m0 < L) {
-      int m1 = m0, used = 0;
-      while (m1 < L) {
-        const int sz = ((a.xc[m1 + 1] - a.xc[m1]) | 1) * a.xc[m1];   // (odd row pitch kp)
-        if (m1 > m0 && used + sz > scap) break;
-        used += sz; ++m1;
-      }
-      int o = 0;
-      for (int m = m0; m < m1; ++m) {
-        const int xm = a.xc[m], k = a.xc[m + 1] - xm;
-        const int jn = leaf >> (L - m), side = (leaf >> (L - m - 1)) & 1;
-        const double* gp = Sg + a.slev[m] + (long long)jn * 2 * k * xm + (long long)side * k * xm;
-        for (int q = warp; q < k; q += LEAF_WARPS)
-          for (int c = lane; c < xm; c += 32) cp_async8(Ss + o + c * (k | 1) + q, gp + q * xm + c);
-        o += (k | 1) * xm;
-      }
-      cp_async_commit();
-      if (!lu_issued) { issue_lu(); lu_issued = true; RN_PH(6); cp_async_wait_group1(); } else { RN_PH(6); cp_async_wait_all(); }
-      __syncthreads();
-      RN_PH(1);
-      {                                               // lane = row q of S_side, warp = column slice
-        int o2 = 0;
-        double* vp = part;                            // [8 warps][32 rows] partial sums
-        for (int m = m0; m < m1; ++m) {
-          const int xm = a.xc[m], k = a.xc[m + 1] - xm;
-          const int kp = k | 1;                      // odd pitch: conflict-free stores and loads
-          const double* St = Ss + o2;                 // [xm][kp]
-          const int cw = (xm + LEAF_WARPS - 1) / LEAF_WARPS, c0 = warp * cw, c1 = min(xm, c0 + cw);
-          for (int q0 = 0; q0 < k; q0 += 32) {
-            const int q = q0 + lane;
-            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-            if (q < k) {
-              int c = c0;
-#pragma unroll 2
-              for (; c + 3 < c1; c += 4) {
-                a0 = fma(St[c * kp + q], vs[c], a0); a1 = fma(St[(c + 1) * kp + q], vs[c + 1], a1);
-                a2 = fma(St[(c + 2) * kp + q], vs[c + 2], a2); a3 = fma(St[(c + 3) * kp + q], vs[c + 3], a3);
-              }
-              for (; c < c1; ++c) a0 = fma(St[c * kp + q], vs[c], a0);
-            }
-            vp[warp * 32 + lane] = (a0 + a1) + (a2 + a3);
-            __syncthreads();
-            if (t < 32 && q0 + t < k) {
-              double v = 0.0;
-#pragma unroll
-              for (int w = 0; w < LEAF_WARPS; ++w) v += vp[w * 32 + t];
-              vs[xm + q0 + t] = -v;
-            }
-            __syncthreads();
-          }
-          o2 += (k | 1) * xm;
-        }
-      }
-      __syncthreads();
-      RN_PH(2);
-      m0 = m1;
-    }
-    // ---- u^(m-1) = X^(m-1) v on the leaf rows: 2 rows per thread (16-byte loads, 16 in flight),
-    //      4 column quarters, fixed-order sums
-    {
-      const int i2 = 2 * (t & 63), h = t >> 6;
-      const double* Xi = tp->X + (long long)inst * tp->xstride + r0 + i2;
-      const bool vec = ((r0 | n | tp->xstride) & 1) == 0;   // 16-byte aligned row pairs
-      double ac0[4] = {0.0, 0.0, 0.0, 0.0}, ac1[4] = {0.0, 0.0, 0.0, 0.0};
-      if (i2 < s) {                                   // (X is written in this launch: coherent loads)
-        int c = h;
-        if (vec && i2 + 1 < s) {
-          for (; c < NC; c += 4 * 24) {               // 24 x 16-byte loads in flight per thread
-            double2 x[24];
-#pragma unroll
-            for (int u = 0; u < 24; ++u)
-              x[u] = c + 4 * u < NC ? *reinterpret_cast<const double2*>(Xi + (long long)(c + 4 * u) * n)
-                                    : make_double2(0.0, 0.0);
-#pragma unroll
-            for (int u = 0; u < 24; ++u) {
-              const double vv = c + 4 * u < NC ? vs[c + 4 * u] : 0.0;
-              ac0[u & 3] = fma(x[u].x, vv, ac0[u & 3]);
-              ac1[u & 3] = fma(x[u].y, vv, ac1[u & 3]);
-            }
-          }
-        } else {
-          for (; c < NC; c += 4) {
-            ac0[0] = fma(Xi[(long long)c * n], vs[c], ac0[0]);
-            if (i2 + 1 < s) ac1[0] = fma(Xi[(long long)c * n + 1], vs[c], ac1[0]);
-          }
-        }
-      }
-      part[h * LEAF_MAX + i2] = (ac0[0] + ac0[1]) + (ac0[2] + ac0[3]);
-      part[h * LEAF_MAX + i2 + 1] = (ac1[0] + ac1[1]) + (ac1[2] + ac1[3]);
-    }
-    __syncthreads();
-    RN_PH(3);
-    if (t < s) {
-      const double u = (part[t] + part[LEAF_MAX + t]) + (part[2 * LEAF_MAX + t] + part[3 * LEAF_MAX + t]);
-      tp->u[(long long)inst * n + r0 + t] = u;
-      if (la) bs[t] = u + la->dt * la->f[(long long)inst * n + r0 + t];
-    }
-  } else {
-    if (la) issue_lu();
-    if (t < s) bs[t] = la->u_prev[(long long)inst * n + r0 + t] + la->dt * la->f[(long long)inst * n + r0 + t];
-  }
-  if (!la) return;
-  if (t >= s && t < sp) bs[t] = 0.0;
-  cp_async_wait_all();
-  __syncthreads();
-  RN_PH(4);
-  // ---- x0 = A_leaf^{-1} b with the stored LU (k_leaf.cuh inverse-diagonal form: off-diagonal
-  //      blocks hold -Lt / -Ut, diagonal blocks D_k = A_kk^{-1}); 2 column halves per row
-  const int i = t & 127, h = t >> 7;
-  for (int kb = 0; kb + 1 < nb; ++kb) {              // forward: y_i += (-Lt_ik) y_k
-    const int c0 = 32 * kb + 16 * h;
-    double acc = 0.0;
-    if (i >= 32 * (kb + 1) && i < sp)
-#pragma unroll
-      for (int jj = 0; jj < 16; ++jj) acc = fma(LUs[i + (c0 + jj) * sp], bs[c0 + jj], acc);
-    part[h * LEAF_MAX + i] = acc;
-    __syncthreads();
-    if (t < sp && t >= 32 * (kb + 1)) bs[t] += part[t] + part[LEAF_MAX + t];
-    __syncthreads();
-  }
-  for (int kb = nb - 1; kb >= 0; --kb) {             // backward: x_k = D_k y_k, y_j += (-Ut_jk) y_k
-    if (t < 32) zs[t] = bs[32 * kb + t];
-    __syncthreads();
-    const int c0 = 32 * kb + 16 * h;
-    double acc = 0.0;
-    if (i < 32 * (kb + 1))
-#pragma unroll
-      for (int jj = 0; jj < 16; ++jj) acc = fma(LUs[i + (c0 + jj) * sp], zs[16 * h + jj], acc);
-    part[h * LEAF_MAX + i] = acc;
-    __syncthreads();
-    if (t < 32 * (kb + 1)) {
-      const double v = part[t] + part[LEAF_MAX + t];
-      bs[t] = t >= 32 * kb ? v : bs[t] + v;
-    }
-    __syncthreads();
-  }
-  RN_PH(5);
-  double* X0 = la->X + (long long)inst * la->xstride + r0;
-  if (t < s) X0[t] = bs[t];
-  for (int j = t; j < NC - 1; j += LEAF_THREADS) pcd[j] = panel_col(*la, inst, leaf, r0, 1 + j, NC);
-  __syncthreads();
-  // ---- Q[j][0] = V_all[:, j]^T x0: a warp per 4 V columns, lanes over rows (fixed order)
-  double* Qo = la->Q + (long long)inst * la->qinst + (long long)leaf * la->qstride;
-  double xr[LEAF_MAX / 32];
-#pragma unroll
-  for (int q = 0; q < LEAF_MAX / 32; ++q) xr[q] = lane + 32 * q < s ? bs[lane + 32 * q] : 0.0;
-  constexpr int QG = 6;                               // V columns per warp pass (24 loads in flight)
-  for (int j0 = QG * warp; j0 < NC - 1; j0 += QG * LEAF_WARPS) {
-    double vv[QG][LEAF_MAX / 32];
-#pragma unroll
-    for (int jj = 0; jj < QG; ++jj) {
-      const PanelCol pc = j0 + jj < NC - 1 ? pcd[j0 + jj] : PanelCol{la->Lf, 0, 0, 0, 0, 0};
-#pragma unroll
-      for (int q = 0; q < LEAF_MAX / 32; ++q) {
-        const int r = lane + 32 * q, rc = r < s ? r : s - 1;
-        const double x = __ldg(pc.Lq + pc.li0 + pc.lstep * rc);   // (valid address for any kind)
-        vv[jj][q] = pc.kind == 2 ? x : (pc.kind == 3 && pc.li0 + pc.lstep * r == 0 ? 1.0 : 0.0);
-      }
-    }
-#pragma unroll
-    for (int jj = 0; jj < QG; ++jj) {
-      double v = 0.0;
-#pragma unroll
-      for (int q = 0; q < LEAF_MAX / 32; ++q) v = fma(vv[jj][q], xr[q], v);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0 && j0 + jj < NC - 1) Qo[(long long)(j0 + jj) * NC] = v;
-    }
-  }
 }
 
 __global__ void __launch_bounds__(TR_THREADS, 1)

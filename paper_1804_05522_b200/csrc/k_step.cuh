@@ -10,6 +10,7 @@
 #pragma once
 #include "k_leaf.cuh"
 #include "k_tree.cuh"
+#include "k_final.cuh"
 
 struct StepArgs {
   LeafArgs la;
