@@ -57,6 +57,9 @@ extern "C" {
                              even when the cached handle already holds them */
 
 /* Compile-time capacities of this build. */
+#define FDE_COMPRESS_ONLY 32u /* hodlr_build: stop after S1-S2 (GL weights + compression); the handle
+                                 serves hodlr_ranks / hodlr_status / hodlr_destroy only (rank
+                                 studies beyond the factorisation's width limits) */
 #define FDE_LEAF_MAX  128 /* largest leaf (dense diagonal block) held in shared memory */
 #define FDE_RANK_MAX  47  /* largest compressed rank of one level's T-block */
 

@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libfdehodlr.so")
 
 FDE_OK, FDE_EDOMAIN, FDE_EDIM, FDE_ESINGULAR, FDE_ENOCONV, FDE_ECUDA, FDE_ENOMEM = range(7)
-FDE_SYNC, FDE_CHECK, FDE_HOST_PTRS, FDE_NO_KEEP, FDE_RECOMPRESS = 1, 2, 4, 8, 16
+FDE_SYNC, FDE_CHECK, FDE_HOST_PTRS, FDE_NO_KEEP, FDE_RECOMPRESS, FDE_COMPRESS_ONLY = 1, 2, 4, 8, 16, 32
 FDE_LEAF_MAX, FDE_RANK_MAX = 128, 47
 
 # every symbol the header declares, with its ctypes signature

@@ -138,6 +138,7 @@ struct fde_hodlr {
   size_t tr_smem = 0;
   int* d_done = nullptr;            // k_step task counter + completion counters
   long long dofs[LMAX + 1] = {}, ndone = 0, lofs = 0;
+  bool compress_only = false;       // built with FDE_COMPRESS_ONLY (hodlr_ranks only)
   int step_grid = 0;
   size_t step_smem = 0;
   // pipelined multi-step run (k_run.cuh): second buffer set and stored leaf LUs
@@ -809,6 +810,12 @@ static int build_impl(int batch, int n, const double* alpha, double h, double dt
   g_launches++;
   // S2: compression
   if ((rc = run_compression(H, s)) != FDE_OK) return fail(rc);
+  if (flags & FDE_COMPRESS_ONLY) {                  // S1-S2 only (rank studies): no factor layout
+    H->compress_only = true;
+    H->last_stream = s;
+    *out = H;
+    return FDE_OK;
+  }
   // one synchronisation per build: the ranks fix the column layout of the factorisation
   if ((rc = finalize_layout(H, s)) != FDE_OK) return fail(rc);
   H->last_stream = s;
@@ -996,6 +1003,7 @@ int hodlr_update(fde_hodlr_t H, double dt, const double* d_plus, const double* d
                  void* stream) {
   g_last_error.clear();
   if (!H) return set_err(FDE_EDOMAIN, "handle is NULL");
+  if (H->compress_only) return set_err(FDE_EDIM, "handle built with FDE_COMPRESS_ONLY");
   if (!(dt >= 0.0) || !std::isfinite(dt)) return set_err(FDE_EDOMAIN, "dt=%g must be >= 0", dt);
   cudaStream_t s = (cudaStream_t)stream;
   const size_t bytes = (size_t)H->batch * H->n * sizeof(double);
@@ -1012,6 +1020,7 @@ int hodlr_update(fde_hodlr_t H, double dt, const double* d_plus, const double* d
 int hodlr_factor(fde_hodlr_t H, unsigned flags, void* stream) {
   g_last_error.clear();
   if (!H) return set_err(FDE_EDOMAIN, "handle is NULL");
+  if (H->compress_only) return set_err(FDE_EDIM, "handle built with FDE_COMPRESS_ONLY");
   cudaStream_t s = (cudaStream_t)stream;
   TRY(factor_impl(H, H->d_dp, H->d_dm, 0, nullptr, nullptr, nullptr, 1, s));
   H->factored = true;
@@ -1023,6 +1032,7 @@ int hodlr_factor(fde_hodlr_t H, unsigned flags, void* stream) {
 int hodlr_solve(fde_hodlr_t H, const double* b, double* x, int nrhs, int ld, unsigned flags, void* stream) {
   g_last_error.clear();
   if (!H) return set_err(FDE_EDOMAIN, "handle is NULL");
+  if (H->compress_only) return set_err(FDE_EDIM, "handle built with FDE_COMPRESS_ONLY");
   if (!H->factored) return set_err(FDE_EDOMAIN, "hodlr_solve before hodlr_factor");
   if (!b || !x) return set_err(FDE_EDOMAIN, "b / x is NULL");
   if (nrhs < 1 || nrhs > NRHS_MAX) return set_err(FDE_EDIM, "nrhs=%d outside [1, %d]", nrhs, NRHS_MAX);
@@ -1037,6 +1047,7 @@ int hodlr_solve(fde_hodlr_t H, const double* b, double* x, int nrhs, int ld, uns
 int hodlr_matvec(fde_hodlr_t H, const double* x, double* y, int nrhs, int ld, unsigned flags, void* stream) {
   g_last_error.clear();
   if (!H) return set_err(FDE_EDOMAIN, "handle is NULL");
+  if (H->compress_only) return set_err(FDE_EDIM, "handle built with FDE_COMPRESS_ONLY");
   if (!x || !y) return set_err(FDE_EDOMAIN, "x / y is NULL");
   if (x == y) return set_err(FDE_EDOMAIN, "y must not alias x");
   if (nrhs < 1 || nrhs > NRHS_MAX) return set_err(FDE_EDIM, "nrhs=%d outside [1, %d]", nrhs, NRHS_MAX);
