@@ -503,10 +503,33 @@ extern "C" int fde2d_step(int nx, int ny, double alpha1, double alpha2, double h
     if ((rc = transpose(s, sa, sbb, Ym, sa, Zm, sbb)) != FDE_OK) return rc;
     if ((rc = ts_nn(s, ny, sa, sbb, 1.0, Wt, ny, Zm, sbb, 0.0, w.M2, ny)) != FDE_OK) return rc;
     if ((rc = sumsq(s, ny, sa, w.M2, ny, w.dv + 8, &rb2)) != FDE_OK) return rc;
-    rel = std::sqrt((ra2 + rb2) / cnorm2);
-    if (getenv("FDE_DEBUG2D"))
-      fprintf(stderr, "fde2d it %d: sa %d sb %d rc %d sign-its %d rel %.3e (ra2 %.3e rb2 %.3e c2 %.3e)\n", it, sa,
-              sbb, rcr, sit, rel, ra2, rb2, cnorm2);
+    // the projected equation's own residual P = A~ Y + Y B~ - C~ (the splitting assumes P = 0;
+    // the sign iteration leaves a rounding-level P, which is added here, not assumed away)
+    CU(cudaMemcpyAsync(w.M1, Cm, (size_t)sa * sbb * 8, cudaMemcpyDeviceToDevice, s));
+    if ((rc = ts_nn(s, sa, sbb, sa, 1.0, Lc, sa, Ym, sa, -1.0, w.M1, sa)) != FDE_OK) return rc;
+    if ((rc = transpose(s, sbb, sbb, Rc, sbb, w.G, sbb)) != FDE_OK) return rc;
+    if ((rc = ts_nn(s, sa, sbb, sbb, 1.0, Ym, sa, w.G, sbb, 1.0, w.M1, sa)) != FDE_OK) return rc;
+    double rp2 = 0.0;
+    if ((rc = sumsq(s, sa, sbb, w.M1, sa, w.dv + 8, &rp2)) != FDE_OK) return rc;
+    rel = std::sqrt((ra2 + rb2 + rp2) / cnorm2);
+    if (getenv("FDE_DEBUG2D")) {
+      double oe[2] = {0.0, 0.0};
+      for (int side = 0; side < 2; ++side) {
+        const int ss = side ? sbb : sa, nn2 = side ? ny : nx;
+        const double* Ub = side ? Vy : Ux;
+        std::vector<double> g((size_t)ss * ss);
+        if ((rc = ts_tn(s, ss, ss, nn2, 1.0, Ub, nn2, Ub, nn2, 0.0, w.G, ss)) != FDE_OK) return rc;
+        CU(cudaMemcpy(g.data(), w.G, g.size() * 8, cudaMemcpyDeviceToHost));
+        for (int i = 0; i < ss; ++i) for (int j = 0; j < ss; ++j) oe[side] = std::max(oe[side], std::fabs(g[(size_t)i * ss + j] - (i == j)));
+      }
+      double yy2 = 0.0;
+      if ((rc = sumsq(s, sa, sbb, Ym, sa, w.dv + 8, &yy2)) != FDE_OK) return rc;
+      fprintf(stderr, "fde2d it %d: |U^T U - I| %.3e |V^T V - I| %.3e |Y| %.6e\n", it, oe[0], oe[1], std::sqrt(yy2));
+      double ct2 = 0.0;
+      if ((rc = sumsq(s, sa, sbb, Cm, sa, w.dv + 8, &ct2)) != FDE_OK) return rc;
+      fprintf(stderr, "fde2d it %d: sa %d sb %d rc %d sign-its %d rel %.3e (ra2 %.3e rb2 %.3e rp2 %.3e c2 %.3e "
+              "|C~|^2 - c2 %.3e)\n", it, sa, sbb, rcr, sit, rel, ra2, rb2, rp2, cnorm2, ct2 - cnorm2);
+    }
     solved_x = sx.s; solved_y = sy.s;
     return FDE_OK;
   };
@@ -539,10 +562,20 @@ extern "C" int fde2d_step(int nx, int ny, double alpha1, double alpha2, double h
   if (iters_out) *iters_out = std::min(it, ek_maxit);
   // ---- truncation: Y Z = W Sigma (one-sided Jacobi), X = (U W Sigma)(V Z)^T, keep sigma > tol sigma_1
   const int sa = sx.s, sbb = sy.s;
+  const bool dbg2 = getenv("FDE_DEBUG2D") != nullptr;
+  if (dbg2) CU(cudaMemcpyAsync(w.M3, Ym, (size_t)sa * sbb * 8, cudaMemcpyDeviceToDevice, s));
   { PROF("k_osj_svd"); k_osj_svd<<<1, DN_BIG, dn_smem((long long)sa * sbb, sbb + 2), s>>>(sa, sbb, Ym, sa, Zm, sig, 60); }
   if ((rc = dn_check("k_osj_svd")) != FDE_OK) return fail(rc);
   CU(cudaMemcpyAsync(hs.data(), sig, sbb * sizeof(double), cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
+  if (getenv("FDE_DEBUG2D")) {                      // orthogonality of the right singular vectors
+    std::vector<double> g((size_t)sbb * sbb);
+    if ((rc = ts_tn(s, sbb, sbb, sbb, 1.0, Zm, sbb, Zm, sbb, 0.0, w.G, sbb)) != FDE_OK) return fail(rc);
+    CU(cudaMemcpy(g.data(), w.G, g.size() * 8, cudaMemcpyDeviceToHost));
+    double e = 0.0;
+    for (int i = 0; i < sbb; ++i) for (int j = 0; j < sbb; ++j) e = std::max(e, std::fabs(g[(size_t)i * sbb + j] - (i == j)));
+    fprintf(stderr, "fde2d svd: sa %d sb %d |Z^T Z - I|max %.3e sig1 %.3e\n", sa, sbb, e, hs[0]);
+  }
   ord.assign(sbb, 0);
   for (int i = 0; i < sbb; ++i) ord[i] = i;
   std::sort(ord.begin(), ord.end(), [&](int a, int c) { return hs[a] > hs[c] || (hs[a] == hs[c] && a < c); });
@@ -555,6 +588,15 @@ extern "C" int fde2d_step(int nx, int ny, double alpha1, double alpha2, double h
     { PROF("k_gather_cols"); k_gather_cols<<<(sa * rk + 255) / 256, 256, 0, s>>>(sa, rk, Ym, sa, w.idx, nullptr, w.M5, sa); }
     { PROF("k_gather_cols"); k_gather_cols<<<(sbb * rk + 255) / 256, 256, 0, s>>>(sbb, rk, Zm, sbb, w.idx, nullptr, w.M6, sbb); }
     if ((rc = dn_check("k_gather_cols")) != FDE_OK) return fail(rc);
+    if (dbg2) {                                     // |M5 M6^T - Y| / |Y|: the truncated assembly
+      if ((rc = transpose(s, sbb, rk, w.M6, sbb, w.G, rk)) != FDE_OK) return fail(rc);
+      if ((rc = ts_nn(s, sa, sbb, rk, 1.0, w.M5, sa, w.G, rk, -1.0, w.M3, sa)) != FDE_OK) return fail(rc);
+      double d2 = 0.0, y2 = 0.0;
+      if ((rc = sumsq(s, sa, sbb, w.M3, sa, w.dv + 8, &d2)) != FDE_OK) return fail(rc);
+      for (int i = 0; i < sbb; ++i) y2 += hs[i] * hs[i];
+      fprintf(stderr, "fde2d assembly: rk %d of %d, |M5 M6^T - Y|/|Y| %.3e, |Y| %.6e sig max %.3e min kept %.3e\n", rk, sbb,
+              std::sqrt(d2 / y2), std::sqrt(y2), hs[ord[0]], hs[keep[rk - 1]]);
+    }
     if ((rc = ts_nn(s, nx, rk, sa, 1.0, Ux, nx, w.M5, sa, 0.0, Xu, nx)) != FDE_OK) return fail(rc);
     if ((rc = ts_nn(s, ny, rk, sbb, 1.0, Vy, ny, w.M6, sbb, 0.0, Xv, ny)) != FDE_OK) return fail(rc);
   }

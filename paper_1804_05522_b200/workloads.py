@@ -168,9 +168,10 @@ class Workload2D:
     tfac: object = None  # t -> scalar multiplying the separable source
 
     def source_factors(self, m):
-        """F^(m) = Fu Fv^T at t_m (m = 1..K): returns (Fu, Fv)."""
+        """F^(m) = Fu Fv^T at t_m (m = 1..K): returns (Fu, Fv).  tfac(t) is a scalar or one
+        factor per separable term."""
         tm = m * self.dt
-        return self.Fa, self.Fb * self.tfac(tm)
+        return self.Fa, self.Fb * np.asarray(self.tfac(tm))
 
 
 def cfg5(n=2048, K=16):
@@ -185,3 +186,24 @@ def cfg5(n=2048, K=16):
     return Workload2D("cfg5", n, n, h, h, 1.3, 1.7, K, 1.0 / K, 128, 1e-12, 1e-11,
                       x, x.copy(), 1 + x, 2 - x, 1 + x ** 2, 2 - x ** 2, Fa, Fb,
                       lambda t: 1.0 + t)
+
+
+def paper2d(n, alpha1=1.3, alpha2=1.7, variable=False, K=8, tol=1e-8, ek_tol=1e-6, leaf=128):
+    """The paper's 2D test problem (Sec. 5.1, from Breiten et al.): [0,1]^2,
+    f = 100 (sin(10 pi x) cos(pi y) + sin(10 t) sin(pi x) y (1 - y)) -- rank 2 on the grid for
+    every t --, implicit Euler with dt = 1, 8 steps, u0 = 0, HODLR tol 1e-8 and EK tolerance 1e-6
+    (P:1626-1630); d = 1 (constant case) or Eq. (5.1): d1+ = G(1.2)(1+x)^a1, d1- = G(1.2)(2-x)^a1,
+    d2+- likewise in y with a2.  Grid: h = 1/(n+1) (reading R5; the paper writes 1/(N+2))."""
+    h = 1.0 / (n + 1)
+    x = h * np.arange(1, n + 1)
+    if variable:
+        g = math.gamma(1.2)
+        d1p, d1m = g * (1 + x) ** alpha1, g * (2 - x) ** alpha1
+        d2p, d2m = g * (1 + x) ** alpha2, g * (2 - x) ** alpha2
+    else:
+        d1p = d1m = d2p = d2m = np.ones(n)
+    Fa = np.stack([100.0 * np.sin(10 * np.pi * x), 100.0 * np.sin(np.pi * x)], axis=1)
+    Fb = np.stack([np.cos(np.pi * x), x * (1 - x)], axis=1)
+    return Workload2D("paper2d-%s" % ("var" if variable else "const"), n, n, h, h, alpha1, alpha2,
+                      K, 1.0, leaf, tol, ek_tol, x, x.copy(), d1p, d1m.copy(), d2p, d2m.copy(),
+                      Fa, Fb, lambda t: np.array([1.0, math.sin(10.0 * t)]))
