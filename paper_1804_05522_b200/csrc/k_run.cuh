@@ -94,6 +94,8 @@ k_run(const RunArgs ra) {
   // their geometry (xcol, ranks, offsets, ...) from shared memory, not through the L1
   __shared__ LeafArgs s_la;
   __shared__ TrArgs s_ta, s_tp;
+  __shared__ int s_la_step, s_ta_step, s_tp_step;   // which step's block each copy holds
+  if (threadIdx.x == 0) { s_la_step = -1; s_ta_step = -1; s_tp_step = -1; }
   const TrArgs& a0 = ra.tas[0];
   const int L = a0.L, nleaf = a0.nleaf;
   const long long n_leaf = (long long)a0.batch * nleaf;
@@ -144,14 +146,15 @@ k_run(const RunArgs ra) {
       const int inst = (int)(tk / nleaf), leaf = (int)(tk % nleaf);
       int* dn = ra.done + (long long)step * ra.per_step;
       if (kind == 0) {                                // A: build, LU (stored), U columns
-        rn_copy(&s_la, &ra.las[step]);
+        if (s_la_step != step) { rn_copy(&s_la, &ra.las[step]); if (threadIdx.x == 0) s_la_step = step; }
         leaf_task(s_la, smem, leaf, inst, false);
       } else if (kind == 1) {                         // B: projection of the U columns
-        rn_copy(&s_la, &ra.las[step]);
+        if (s_la_step != step) { rn_copy(&s_la, &ra.las[step]); if (threadIdx.x == 0) s_la_step = step; }
         leaf_proj_task(s_la, smem, leaf, inst);
       } else {                                        // B': final of step-1 + rhs column
-        if (kind == 2) rn_copy(&s_la, &ra.las[step]);
-        if (step > 0) rn_copy(&s_tp, &ra.tas[step - 1]); else rn_copy(&s_tp, &ra.tas[0]);
+        if (kind == 2 && s_la_step != step) { rn_copy(&s_la, &ra.las[step]); if (threadIdx.x == 0) s_la_step = step; }
+        const int tps = step > 0 ? step - 1 : 0;
+        if (s_tp_step != tps) { rn_copy(&s_tp, &ra.tas[tps]); if (threadIdx.x == 0) s_tp_step = tps; }
         leaf_rhs_final(s_tp, step > 0 ? &s_tp : nullptr, kind == 2 ? &s_la : nullptr,
                        smem, ra.smem_doubles, inst, leaf, ra.prof);
         if (ra.prof && threadIdx.x == 0) atomicAdd(ra.prof + (kind == 2 ? 7 : 15), 1ULL);
@@ -172,7 +175,7 @@ k_run(const RunArgs ra) {
       const long long jj = task & 0xffffffffLL;
       const int inst = (int)(jj >> m), j = (int)(jj & ((1LL << m) - 1));
       int* dn = ra.done + (long long)step * ra.per_step;
-      rn_copy(&s_ta, &ra.tas[step]);
+      if (s_ta_step != step) { rn_copy(&s_ta, &ra.tas[step]); if (threadIdx.x == 0) s_ta_step = step; }
       const TrArgs& a = s_ta;
       tr_unit(a, smem, inst, m, j, chunk);
       __syncthreads();
