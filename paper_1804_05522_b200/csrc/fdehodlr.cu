@@ -1248,6 +1248,11 @@ int fde1d_run(int batch, int n, const double* alpha, double h, double dt, int K,
     lm.X = Xp[p]; lm.LU = H->d_LUr[p]; lm.Q = Qp[p] + H->qlev[L];
     TrArgs& tm = H->run_tas[m];
     tm = a;
+    // one unit per node in the pipelined run: the row-chunk split that shortens k_step's exposed
+    // tree chain would put the extra chunks in the ready queue, where they wait for a CTA to
+    // come free from leaf work; measured 630 vs 663 us/step at cfg3 (FDE_RUN_RC overrides)
+    const int rcap = getenv("FDE_RUN_RC") ? std::max(1, atoi(getenv("FDE_RUN_RC"))) : 1;
+    for (int l = 0; l < L; ++l) tm.rc[l] = std::min(tm.rc[l], rcap);
     tm.Q = Qp[p]; tm.Qleaf = Qp[p] + H->qlev[L]; tm.Sst = Sp[p]; tm.X = Xp[p];
     tm.u = u_out + m * cnt;
   }
