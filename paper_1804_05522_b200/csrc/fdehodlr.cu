@@ -853,6 +853,8 @@ static int factor_impl(fde_hodlr* H, const double* dp, const double* dm, int nf,
     a.L = L; a.NC = H->xcol[L]; a.nleaf = H->nleaf; a.batch = H->batch; a.kmaxc = H->kmax;
     for (int l = 0; l <= L; ++l) a.xc[l] = H->xcol[l];
     for (int m = 0; m < L; ++m) { a.rc[m] = H->trc[m]; a.slev[m] = H->slev[m]; }
+    if (const char* e = getenv("FDE_STEP_RC"))       // experiment: cap the row chunks per node
+      for (int m = 0; m < L; ++m) a.rc[m] = std::min(a.rc[m], std::max(1, atoi(e)));
     for (int m = 1; m <= L; ++m) a.qlev[m] = H->qlev[m];
     a.qinst = H->qinst; a.sinst = H->sinst;
     a.Qleaf = H->d_Q + H->qlev[L]; a.Q = H->d_Q; a.Sst = H->d_S;
