@@ -371,6 +371,107 @@ __device__ __forceinline__ PanelCol panel_col(const LeafArgs& a, int inst, int l
   return pc;
 }
 
+// One panel stripe (8 columns) solved by a group of 4 warps (named barrier 2 + group): warp w of
+// the group owns row block w (4 DMMA m-tiles).  Same block sweeps as stripe_solve -- forward
+// z_i += (-Lt_ik) z_k, backward x_k = D_k z_k, z_j += (-Ut_jk) z_k -- with each finished block
+// published through a double-buffered 32 x 8 shared buffer; identical arithmetic per element
+// (same DMMA chains in the same order), so results equal the single-warp stripe bitwise.
+//   buf: 3 warp-private stripe buffers of the group (8 x YLD each): [stripe | pub0 | pub1]
+__device__ __noinline__ void leaf_coop_stripe(const double* __restrict__ A, int nb, int s, double c,
+                                              const LeafArgs& a, const PanelCol* pcd, int c_begin,
+                                              int c_end, int st, const double* dps, const double* dms,
+                                              const double* bs, double* buf, double* Xi, int n) {
+  const int lane = threadIdx.x & 31, gid = lane >> 2, tig = lane & 3;
+  const int w = (threadIdx.x >> 5) & 3, bar = 2 + (threadIdx.x >> 7);
+  double* Sb = buf;                                   // stripe columns (rows 0..127, pitch YLD)
+  double* Pb[2] = {buf + 8 * YLD, buf + 16 * YLD};    // published blocks (32 rows, pitch YLD)
+  const int cs = c_begin + 8 * st;
+  auto gsync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(bar), "n"(128) : "memory"); };
+  // generate: warp w scales columns 2w, 2w+1
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int cc = 2 * w + h;
+    const PanelCol pc = cs + cc < c_end ? pcd[cs + cc - c_begin] : PanelCol{a.Lf, 0, 0, 0, 0, 0};
+    const double* sc = pc.sel ? dms : dps;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = lane + 32 * q;
+      const int ic = i < s ? i : s - 1;
+      const double x = __ldg(pc.Lq + pc.li0 + pc.lstep * ic);
+      double v = 0.0;
+      if (i < s) {
+        if (pc.kind == 2) v = x * (-c * sc[i]);
+        else if (pc.kind == 3) v = (pc.li0 + pc.lstep * i == 0) ? -c * sc[i] : 0.0;
+        else if (pc.kind == 1) v = bs[i];
+      }
+      Sb[i + cc * YLD] = v;
+    }
+  }
+  gsync();
+  double acc[4][2];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int i = 32 * w + 8 * u + gid;
+    acc[u][0] = w < nb ? Sb[i + 2 * tig * YLD] : 0.0;
+    acc[u][1] = w < nb ? Sb[i + (2 * tig + 1) * YLD] : 0.0;
+  }
+  auto publish = [&](double* P) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      P[8 * u + gid + (2 * tig) * YLD] = acc[u][0];
+      P[8 * u + gid + (2 * tig + 1) * YLD] = acc[u][1];
+    }
+  };
+  int pb = 0;
+  for (int kb = 0; kb + 1 < nb; ++kb) {               // forward
+    if (w == kb) publish(Pb[pb]);
+    gsync();
+    if (w > kb && w < nb) {
+#pragma unroll
+      for (int k4 = 0; k4 < 8; ++k4) {
+        const double b = Pb[pb][4 * k4 + tig + gid * YLD];
+        const double* Ak = A + (kb * 32 + 4 * k4 + tig) * LDA_LEAF + gid;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) dmma884(acc[u][0], acc[u][1], Ak[8 * (4 * w + u)], b);
+      }
+    }
+    pb ^= 1;
+  }
+  for (int kb = nb - 1; kb >= 0; --kb) {              // backward
+    if (w == kb) publish(Pb[pb]);
+    gsync();
+    if (w <= kb) {
+      if (w == kb) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) { acc[u][0] = 0.0; acc[u][1] = 0.0; }
+      }
+#pragma unroll
+      for (int k4 = 0; k4 < 8; ++k4) {
+        const double b = Pb[pb][4 * k4 + tig + gid * YLD];
+        const double* Ak = A + (kb * 32 + 4 * k4 + tig) * LDA_LEAF + gid;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) dmma884(acc[u][0], acc[u][1], Ak[8 * (4 * w + u)], b);
+      }
+    }
+    pb ^= 1;
+  }
+  // each warp's rows -> stripe buffer -> X (columns contiguous over rows)
+  if (w < nb) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = 32 * w + 8 * u + gid;
+      Sb[i + 2 * tig * YLD] = acc[u][0];
+      Sb[i + (2 * tig + 1) * YLD] = acc[u][1];
+    }
+  }
+  __syncwarp();
+  if (w < nb)
+    for (int cc = 0; cc < 8 && cs + cc < c_end; ++cc) {
+      const int i = 32 * w + lane;
+      if (i < s) Xi[(long long)(cs + cc) * n + i] = Sb[i + cc * YLD];
+    }
+}
+
 // ---- S5 input: projection of the leaf panel on every ancestor's V factor -----------------
 // Q_leaf = V_all[leaf rows]^T X_leaf  ((NC-1) x NC, row-major, ld NC), where V-column j is
 // the V factor column of X column j+1 (level l, q): child 0 rows of a level-l node carry
@@ -447,6 +548,9 @@ __device__ void leaf_project(const LeafArgs& a, double* big, const PanelCol* pcd
   }
 }
 
+// COOP: solve a last round of 1-2 stripes with 4-warp groups (k_run; the extra call raises the
+// register pressure of the fused k_step kernel into spills, so it stays off there)
+template <bool COOP = false>
 __device__ __forceinline__ void leaf_task(const LeafArgs& a, double* smem, int leaf, int inst,
                                           bool do_proj = true) {
   double* S = smem;                               // 32 x 33 scratch (g staging, Gauss-Jordan)
@@ -580,8 +684,13 @@ __device__ __forceinline__ void leaf_task(const LeafArgs& a, double* smem, int l
         }
       }
     };
-    if (warp < nstripe) load_raw(warp);
-    for (int st = warp; st < nstripe; st += LEAF_WARPS) {
+    // The last round of stripes (nstripe % 8 of them) would keep only that many warps busy: when
+    // it holds at most 2 stripes, each is solved by a group of 4 warps that split its row blocks
+    // (leaf_coop_stripe), and the per-warp loop stops at the last full round.
+    const int ntail = nstripe % LEAF_WARPS;
+    const int nsolo = (COOP && ntail >= 1 && ntail <= 2 && nb > 1) ? nstripe - ntail : nstripe;
+    if (warp < nsolo) load_raw(warp);
+    for (int st = warp; st < nsolo; st += LEAF_WARPS) {
       // scale the 8 panel columns into the warp's stripe buffer, then into registers
       const int cs = c_begin + 8 * st;
 #pragma unroll
@@ -610,7 +719,7 @@ __device__ __forceinline__ void leaf_task(const LeafArgs& a, double* smem, int l
       }
       __syncwarp();
       PTR(1);
-      if (st + LEAF_WARPS < nstripe) load_raw(st + LEAF_WARPS);
+      if (st + LEAF_WARPS < nsolo) load_raw(st + LEAF_WARPS);
       stripe_solve(acc, A, nb, Ys);
       PTR(2);
 #pragma unroll
@@ -632,6 +741,14 @@ __device__ __forceinline__ void leaf_task(const LeafArgs& a, double* smem, int l
       PTR(3);
     }
 #undef PTR
+    if (COOP && nsolo < nstripe) {
+      __syncthreads();                               // (every warp-private stripe buffer free)
+      const int g = warp >> 2;                       // group g solves stripe nsolo + g
+      if (nsolo + g < nstripe)
+        leaf_coop_stripe(A, nb, s, c, a, pcd, c_begin, c_end, nsolo + g, dps, dms, bs,
+                         A + LEAF_MAX * LDA_LEAF + (4 * g) * 8 * YLD, Xi, n);
+      __syncthreads();
+    }
     lph(4);
     if (a.keep) {
       // kept factor = the explicit leaf inverse (stripe solves of the identity): a later solve

@@ -147,7 +147,7 @@ k_run(const RunArgs ra) {
       int* dn = ra.done + (long long)step * ra.per_step;
       if (kind == 0) {                                // A: build, LU (stored), U columns
         if (s_la_step != step) { rn_copy(&s_la, &ra.las[step]); if (threadIdx.x == 0) s_la_step = step; }
-        leaf_task(s_la, smem, leaf, inst, false);
+        leaf_task<true>(s_la, smem, leaf, inst, false);
       } else if (kind == 1) {                         // B: projection of the U columns
         if (s_la_step != step) { rn_copy(&s_la, &ra.las[step]); if (threadIdx.x == 0) s_la_step = step; }
         leaf_proj_task(s_la, smem, leaf, inst);
