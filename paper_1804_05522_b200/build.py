@@ -16,6 +16,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
            "-shared", "-Xcompiler", "-fPIC", "-o", OUT + ".tmp", SRC]
+    cmd[1:1] = os.environ.get("FDE_NVCC_FLAGS", "").split()        # (experiments: -D...)
     if verbose:
         cmd[1:1] = ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)

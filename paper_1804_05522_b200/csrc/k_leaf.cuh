@@ -267,11 +267,20 @@ __device__ void leaf_block_lu(double* A, int sp, double* prow, DevStatus* st, in
       cm_gemm_sub<true>(Akk, LDA_LEAF, Lk, LDA_LEAF, Uk, LDA_LEAF, 32, 32, 32, 0, LEAF_WARPS);
       __syncthreads();
       LUT(2);
+#ifdef FDE_LU_SERIAL
+      if (warp < GJ_WARPS) quad_gj_inv32(Akk, LDA_LEAF, prow, st, where);
+      __syncthreads();
+      if (sp - k1 > 32)
+        cm_gemm_sub<true>(Akk, LDA_LEAF, Lk, LDA_LEAF, Uk, LDA_LEAF, sp - k1, sp - k1, 32, 0,
+                          LEAF_WARPS, 0, 0);
+      __syncthreads();
+#else
       if (warp < GJ_WARPS) quad_gj_inv32(Akk, LDA_LEAF, prow, st, where);
       else if (sp - k1 > 32)
         cm_gemm_sub<true>(Akk, LDA_LEAF, Lk, LDA_LEAF, Uk, LDA_LEAF, sp - k1, sp - k1, 32, GJ_WARPS,
                           LEAF_WARPS - GJ_WARPS, 0, 0);
       __syncthreads();
+#endif
       LUT(3);
     }
   }

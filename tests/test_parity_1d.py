@@ -385,3 +385,24 @@ def test_cfg3_pipelined_run_backward_error():
         assert be["eta"] <= 1e-10, (m, be)
         u = out[m - 1, 0]
     st.close()
+
+
+@gpu
+def test_cfg4_pipelined_run_full_size():
+    """cfg4 at full size (batch 512, n = 8192) through fde1d_run, 3 steps: dense oracle on the
+    first step of the alpha extremes, eta <= 1e-12 on every 7th instance at every step."""
+    wl = W.cfg4(K=3)
+    st = _stepper(wl)
+    dp, dm = wl.coeffs(1)
+    f = wl.source(1)
+    out = st.run(wl.dt, _t(dp)[None], _t(dm)[None], _t(f)[None], _t(wl.u0), K=3).cpu().numpy()
+    for b in (int(np.argmax(wl.alpha)), int(np.argmin(wl.alpha))):
+        uo = _oracle_step(wl, 1, wl.u0, b)
+        assert _rel(out[0, b], uo) <= 1e-8, (b, wl.alpha[b], _rel(out[0, b], uo))
+    u = wl.u0
+    for m in range(3):
+        for b in range(0, 512, 7):
+            be = backward_error(float(wl.alpha[b]), wl.h, wl.dt, dp[b], dm[b], out[m, b], u[b] + wl.dt * f[b])
+            assert be["eta"] <= 1e-12, (m, b, be)
+        u = out[m]
+    st.close()
