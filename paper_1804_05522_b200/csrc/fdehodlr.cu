@@ -1191,7 +1191,7 @@ int fde1d_run(int batch, int n, const double* alpha, double h, double dt, int K,
   RunArgs ra{};
   long long o = 0, units = 0;
   ra.o_A = o; o += n_leaf;
-  ra.o_R = o; o += n_leaf / 2;                     // B' runs per sibling pair
+  ra.o_R = o; o += n_leaf;
   ra.o_pair = o; o += (long long)B << (L - 1);
   for (int m = 0; m < L; ++m) {
     ra.o_lvl[m] = o; o += (long long)B << m;

@@ -4,15 +4,14 @@
 // d+-(t_m) alone.  Per leaf and step the work is therefore split into
 //   A  : build + LU (stored, inverse-diagonal form) + U-column stripes   (k_leaf.cuh leaf_task, nf = 0)
 //   B  : projection Q[:, 1:] = V_all^T X[:, 1:]                           (leaf_proj_task)
-//   B' : per sibling pair of leaves: u^(m-1) on the leaves' rows = X^(m-1) v^(m-1) (the "final"
-//        of step m-1, see k_tree.cuh; the pair shares the S blocks and v recursion of every
-//        level but the last), x0 = A_leaf^{-1}(u^(m-1) + dt f^(m)) with the stored LU,
-//        X[:, 0] = x0, Q[:, 0] = V_all^T x0                              (leaf_rhs_final_pair, k_final.cuh)
+//   B' : u^(m-1) on the leaf's rows = X^(m-1) v^(m-1) (the "final" of step m-1, see k_tree.cuh),
+//        x0 = A_leaf^{-1}(u^(m-1) + dt f^(m)) with the stored LU, X[:, 0] = x0,
+//        Q[:, 0] = V_all^T x0                                             (leaf_rhs_final, k_final.cuh)
 // and the SMW tree units of every level follow (k_tree.cuh tr_unit).  A virtual step K holds
 // the last finals (u^(K-1)).  Only B' and the tree lie on the step-to-step chain; A and B of
 // step m+1 fill the SMs while the tree of step m climbs its latency-bound upper levels.
 //
-// Scheduling.  Leaf work comes from one ticket queue (atomicAdd): A(m), B(m), B'(m) (pairs) for
+// Scheduling.  Leaf work comes from one ticket queue (atomicAdd): A(m), B(m), B'(m) for
 // m = 0..K-1, then the finals of step K.  Tree units never wait: a unit is released by the task
 // whose completion makes it ready -- the CTA completing the last input of a node runs the
 // node's first row chunk itself next (continuation: the step's critical chain runs without any
@@ -23,14 +22,14 @@
 // Every dependency points to an earlier task of the order A(0) B(0) B'(0) tree(0) A(1) ..., so
 // the earliest incomplete task can always run: no deadlock for any number of co-resident CTAs.
 // Buffers alternate by step parity (X, stored LU, Q, S); the waits below protect every reuse:
-//   A(m)_i   waits B'(m-1) of its pair (X^(m-2) of the leaf was last read by that final)
+//   A(m)_i   waits B'(m-1)_i   (X^(m-2) of the leaf was last read by the final in B'(m-1)_i)
 //   B(m)_i   waits A(m)_i
-//   B'(m)    waits A(m) of both leaves and root(m-1) of its instance (S^(m-1) complete)
+//   B'(m)_i  waits A(m)_i and root(m-1) of its instance (S^(m-1) complete)
 //   tree(m) level L-1 unit j waits B and B' of leaves 2j, 2j+1; level m units their children.
 // Same arithmetic as k_step except the rhs column: its leaf solve is a plain FMA block sweep
 // (not the DMMA stripe) and u^(m-1) is formed per leaf.
 #pragma once
-#include "k_step.cuh"   // (k_final.cuh: leaf_rhs_final_pair, rn_copy)
+#include "k_step.cuh"   // (k_final.cuh: leaf_rhs_final, rn_copy)
 
 
 struct RunArgs {
@@ -53,29 +52,19 @@ struct RunArgs {
 
 __device__ __forceinline__ bool rn_ready(const int* p, int target) { return st_ld_acquire(p) >= target; }
 
-// Leaf-queue ticket l: per step A of every leaf, B of every leaf, B' of every sibling pair
-// (tk = pair index = leaf >> 1 over the batch); step K: the finals, per pair.  Decoded into
-// (step, kind, tk); the queue's stride per step is Tl = 2 n_leaf + n_leaf / 2.
-__device__ __forceinline__ void rn_leaf_decode(const RunArgs& ra, long long n_leaf, long long l, int& step,
-                                               int& kind, long long& tk) {
-  const long long Tl = 2 * n_leaf + n_leaf / 2;
-  step = (int)(l / Tl);
-  tk = l - (long long)step * Tl;
-  kind = step == ra.K ? 3 : tk < n_leaf ? 0 : tk < 2 * n_leaf ? 1 : 2;
-  if (kind == 1) tk -= n_leaf;
-  else if (kind == 2) tk -= 2 * n_leaf;
-}
-// Are its inputs complete?
+// Leaf-queue ticket l: per step A of every leaf, B of every leaf, B' of every leaf; step K:
+// finals.  Are its inputs complete?
 __device__ __forceinline__ bool rn_leaf_ready(const RunArgs& ra, long long n_leaf, long long l) {
   const TrArgs& a = ra.tas[0];
-  int step, kind;
-  long long tk;
-  rn_leaf_decode(ra, n_leaf, l, step, kind, tk);
-  const int* dn = ra.done + (long long)step * ra.per_step;
-  if (kind == 0) return step < 2 || rn_ready(dn - ra.per_step + ra.o_R + (tk >> 1), 1);
+  const long long step = l / (3 * n_leaf);
+  long long tk = l - step * 3 * n_leaf;
+  const int kind = step == ra.K ? 3 : (int)(tk / n_leaf);
+  tk -= (kind == 3 ? 0 : kind) * n_leaf;
+  const int* dn = ra.done + step * ra.per_step;
+  const int inst = (int)(tk / a.nleaf);
+  if (kind == 0) return step < 2 || rn_ready(dn - ra.per_step + ra.o_R + tk, 1);
   if (kind == 1) return rn_ready(dn + ra.o_A + tk, 1);
-  if (kind == 2 && !(rn_ready(dn + ra.o_A + 2 * tk, 1) && rn_ready(dn + ra.o_A + 2 * tk + 1, 1))) return false;
-  const int inst = (int)(2 * tk / a.nleaf);
+  if (kind == 2 && !rn_ready(dn + ra.o_A + tk, 1)) return false;
   return step < 1 || rn_ready(dn - ra.per_step + ra.o_lvl[0] + inst, a.rc[0]);
 }
 
@@ -112,7 +101,7 @@ k_run(const RunArgs ra) {
   const long long n_leaf = (long long)a0.batch * nleaf;
   long long Tt = 0;
   for (int m = 0; m < L; ++m) Tt += (long long)a0.batch * (1LL << m) * a0.rc[m];
-  const unsigned tot_t = (unsigned)(Tt * ra.K), tot_l = (unsigned)((2 * n_leaf + n_leaf / 2) * ra.K + n_leaf / 2);
+  const unsigned tot_t = (unsigned)(Tt * ra.K), tot_l = (unsigned)(3 * n_leaf * ra.K + n_leaf);
   volatile unsigned* vh = ra.heads;     // [0] tree units completed, [1] leaf tickets, [2] rq tail, [3] rq head
   long long held = -1;                  // thread 0: leaf ticket not yet runnable
   long long iou = -1;                   // thread 0: ready-queue ticket not yet served
@@ -150,11 +139,11 @@ k_run(const RunArgs ra) {
     if (ra.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     int code;
     if (queue == 1) {                                 // ---- leaf ticket
-      int step, kind;
-      long long tk;
-      rn_leaf_decode(ra, n_leaf, task, step, kind, tk);
-      const long long lt = kind >= 2 ? 2 * tk : tk;   // (first) leaf of the task over the batch
-      const int inst = (int)(lt / nleaf), leaf = (int)(lt % nleaf);
+      const int step = (int)(task / (3 * n_leaf));
+      long long tk = task - (long long)step * 3 * n_leaf;
+      const int kind = step == ra.K ? 3 : (int)(tk / n_leaf);
+      tk -= (kind == 3 ? 0 : kind) * n_leaf;
+      const int inst = (int)(tk / nleaf), leaf = (int)(tk % nleaf);
       int* dn = ra.done + (long long)step * ra.per_step;
       if (kind == 0) {                                // A: build, LU (stored), U columns
         if (s_la_step != step) { rn_copy(&s_la, &ra.las[step]); if (threadIdx.x == 0) s_la_step = step; }
@@ -162,12 +151,12 @@ k_run(const RunArgs ra) {
       } else if (kind == 1) {                         // B: projection of the U columns
         if (s_la_step != step) { rn_copy(&s_la, &ra.las[step]); if (threadIdx.x == 0) s_la_step = step; }
         leaf_proj_task(s_la, smem, leaf, inst);
-      } else {                                        // B' (a sibling pair): final of step-1 + rhs column
+      } else {                                        // B': final of step-1 + rhs column
         if (kind == 2 && s_la_step != step) { rn_copy(&s_la, &ra.las[step]); if (threadIdx.x == 0) s_la_step = step; }
         const int tps = step > 0 ? step - 1 : 0;
         if (s_tp_step != tps) { rn_copy(&s_tp, &ra.tas[tps]); if (threadIdx.x == 0) s_tp_step = tps; }
-        leaf_rhs_final_pair(s_tp, step > 0 ? &s_tp : nullptr, kind == 2 ? &s_la : nullptr,
-                            smem, ra.smem_doubles, inst, leaf, ra.prof);
+        leaf_rhs_final(s_tp, step > 0 ? &s_tp : nullptr, kind == 2 ? &s_la : nullptr,
+                       smem, ra.smem_doubles, inst, leaf, ra.prof);
         if (ra.prof && threadIdx.x == 0) atomicAdd(ra.prof + (kind == 2 ? 7 : 15), 1ULL);
       }
       __syncthreads();
@@ -175,10 +164,9 @@ k_run(const RunArgs ra) {
         __threadfence();
         if (kind == 0) atomicAdd(dn + ra.o_A + tk, 1);
         if (kind == 2) atomicAdd(dn + ra.o_R + tk, 1);
-        if (kind >= 1) {                              // pair counter: B of each leaf (1) + B' (2)
-          const int inc = kind == 2 ? 2 : 1;
+        if (kind >= 1) {
           const long long jj = (long long)inst * (1 << (L - 1)) + (leaf >> 1);
-          if (atomicAdd(dn + ra.o_pair + jj, inc) + inc == 4) cont = rn_release(ra, step, L - 1, jj);
+          if (atomicAdd(dn + ra.o_pair + jj, 1) == 3) cont = rn_release(ra, step, L - 1, jj);
         }
       }
       code = 100 + kind + 1000 * step;
