@@ -688,8 +688,9 @@ __device__ __forceinline__ void leaf_task(const LeafArgs& a, double* smem, int l
           const int i = lane + 32 * q;
           // branch-free: every descriptor carries a valid pointer (kind != 2: step 0 at a.Lf)
           const int ic = i < s ? i : s - 1;
-          const double x = __ldg(pc.Lq + pc.li0 + pc.lstep * ic);
-          pv[cc][q] = (i < s && pc.kind == 2) ? x : 0.0;
+          // (no use of the value here: the load stays in flight over the current stripe's solve;
+          //  the kind / row masks are applied where the value is scaled)
+          pv[cc][q] = __ldg(pc.Lq + pc.li0 + pc.lstep * ic);
         }
       }
     };
