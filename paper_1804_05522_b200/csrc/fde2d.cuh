@@ -563,6 +563,24 @@ extern "C" int fde2d_step(int nx, int ny, double alpha1, double alpha2, double h
   // ---- truncation: Y Z = W Sigma (one-sided Jacobi), X = (U W Sigma)(V Z)^T, keep sigma > tol sigma_1
   const int sa = sx.s, sbb = sy.s;
   const bool dbg2 = getenv("FDE_DEBUG2D") != nullptr;
+  if (dbg2) {                                       // stored A U vs a fresh product, both sides
+    for (EkSide* e : {&sx, &sy}) {
+      if ((rc = hodlr_mv_cols(e->H, e->U, Wt, e->s, s)) != FDE_OK) return fail(rc);
+      std::vector<double> h1((size_t)e->n * e->s), h2((size_t)e->n * e->s);
+      CU(cudaMemcpy(h1.data(), Wt, h1.size() * 8, cudaMemcpyDeviceToHost));
+      CU(cudaMemcpy(h2.data(), e->AU, h2.size() * 8, cudaMemcpyDeviceToHost));
+      double dmax = 0.0, amax = 0.0;
+      int worst = -1;
+      for (int j = 0; j < e->s; ++j)
+        for (int i = 0; i < e->n; ++i) {
+          const double d = std::fabs(h1[(size_t)j * e->n + i] - h2[(size_t)j * e->n + i]);
+          if (d > dmax) { dmax = d; worst = j; }
+          amax = std::max(amax, std::fabs(h1[(size_t)j * e->n + i]));
+        }
+      fprintf(stderr, "fde2d AU check side %d: s %d max|AU - A U| %.3e (col %d) max|A U| %.3e\n",
+              e == &sx ? 0 : 1, e->s, dmax, worst, amax);
+    }
+  }
   if (dbg2) CU(cudaMemcpyAsync(w.M3, Ym, (size_t)sa * sbb * 8, cudaMemcpyDeviceToDevice, s));
   { PROF("k_osj_svd"); k_osj_svd<<<1, DN_BIG, dn_smem((long long)sa * sbb, sbb + 2), s>>>(sa, sbb, Ym, sa, Zm, sig, 60); }
   if ((rc = dn_check("k_osj_svd")) != FDE_OK) return fail(rc);
