@@ -26,6 +26,10 @@ for ek in (1e-11,):
         if os.environ.get("DBG_FRESH"):
             st.close()
             st = Fde2dStepper(wl.nx, wl.ny, wl.alpha1, wl.alpha2, wl.hx, wl.hy, wl.dt, t(wl.d1p), t(wl.d1m), t(wl.d2p), t(wl.d2m), wl.tol, ek_tol=ek, leaf=wl.leaf)
+        if Xu is not None and os.environ.get("DBG_ORTHO"):   # hand the step an orthonormal U factor
+            Aq, Bq = Xu.cpu().numpy().T, Xv.cpu().numpy().T
+            Q, R = np.linalg.qr(Aq)
+            Xu, Xv = t(Q.T), t((Bq @ R.T).T)
         Xu, Xv, res, its = st.step(Fu, Fv) if Xu is None else st.step(Fu, Fv, Xu, Xv)
         Xg = Xu.cpu().numpy().T @ Xv.cpu().numpy()
         Uo = bs.solve(Uo + wl.dt * Fa @ Fb.T)
