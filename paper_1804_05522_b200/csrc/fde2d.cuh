@@ -191,6 +191,19 @@ static int orth_append(cudaStream_t s, const DenseWs& w, int n, double* W, int b
   ref = std::sqrt(ref);
   if (!(ref > 0.0)) return FDE_OK;
   if (W0) CU(cudaMemcpyAsync(W0, W, (size_t)n * b * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  if (coef && W0 && sb == 0) {
+    // right-hand-side compression: unit columns before the Gram-based steps.  The Gram matrix
+    // resolves directions only down to ~1e-8 of its largest column, and [U_u, dt F_u] mixes a
+    // low-rank factor whose columns carry the singular values (1e2 .. 1e-10) with dt F_u; after
+    // the scaling its conditioning reflects angles only (coef is taken from the unscaled W0).
+    std::vector<double> sc(b);
+    for (int i = 0; i < b; ++i) sc[i] = h[i] > 0.0 ? 1.0 / std::sqrt(h[i]) : 0.0;
+    CU(cudaMemcpyAsync(w.lam, sc.data(), b * sizeof(double), cudaMemcpyHostToDevice, s));
+    { PROF("k_scale_cols"); k_scale_cols<<<(unsigned)(((long long)n * b + 255) / 256), 256, 0, s>>>(n, b, W, n, w.lam); }
+    TRY(dn_check("k_scale_cols"));
+    CU(cudaStreamSynchronize(s));                      // (sc is a host temporary)
+    ref = 1.0;
+  }
   // (project, normalise) twice: "twice is enough" block Gram-Schmidt with SVQB normalisation;
   // pass 0 deflates directions below dtol * ref, pass 1 drops any that lost half their norm
   int cur = b;

@@ -103,6 +103,15 @@ k_ts_gemm_nn(int M, int n, int K, double alpha, const double* __restrict__ A, in
 }
 
 // Y (m x n) = alpha X (m x n), column-major with leading dims (copy / scale).
+// X[:, j] *= sc[j] (column scaling, m x n, ld ldx)
+__global__ void k_scale_cols(int m, int n, double* __restrict__ X, int ldx, const double* __restrict__ sc) {
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e < (long long)m * n) {
+    const int j = (int)(e / m), i = (int)(e - (long long)j * m);
+    X[(long long)j * ldx + i] *= sc[j];
+  }
+}
+
 __global__ void k_scale_copy(int m, int n, double alpha, const double* __restrict__ X, int ldx,
                              double* __restrict__ Y, int ldy) {
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
