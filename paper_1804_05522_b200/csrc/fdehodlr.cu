@@ -1299,8 +1299,8 @@ int fde1d_run(int batch, int n, const double* alpha, double h, double dt, int K,
     for (int g = 0; g < 2; ++g) {
       const unsigned long long* q = pf.data() + 1100 + 8 * g;
       const double c = (double)std::max(1ULL, q[7]) * 1965.0;
-      fprintf(stderr, "k_run tree %s units (%llu): stage %.2f sc+T %.2f gj %.2f S %.2f Qupd %.2f us\n",
-              g ? "upper" : "bottom", q[7], q[0] / c, q[1] / c, q[2] / c, q[3] / c, q[4] / c);
+      fprintf(stderr, "k_run tree %s units (%llu): stage %.2f sc+T %.2f gj %.2f S %.2f Qupd %.2f (issue %.2f wait %.2f) us\n",
+              g ? "upper" : "bottom", q[7], q[0] / c, q[1] / c, q[2] / c, q[3] / c, q[4] / c, q[5] / c, q[6] / c);
     }
     {
       const double c = (double)K * B * H->nleaf * 1965.0;

@@ -314,12 +314,14 @@ __device__ void tr_unit(const TrArgs& a, double* sm, int inst, int m, int j, int
   for (int sc = 0; sc < TR_STG - 1 && sc < nsub; ++sc) issue_sub(sc);
   for (int sc = 0; sc < nsub; ++sc) {
     if (sc + TR_STG - 1 < nsub) issue_sub(sc + TR_STG - 1);
+    TPH(5);                                            // (issue)
     const int ahead = min(TR_STG - 1, nsub - 1 - sc);   // groups allowed to stay in flight
     if (ahead >= 3) asm volatile("cp.async.wait_group 3;" ::: "memory");
     else if (ahead == 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
     else if (ahead == 1) cp_async_wait_group1();
     else cp_async_wait_all();
     __syncthreads();
+    TPH(6);                                            // (wait)
     const int rs = ra + sc * TR_SUB, nr = min(TR_SUB, rb - rs);
     const double* U1 = ubuf(sc, 0);
     const double* U2 = ubuf(sc, 1);
