@@ -1217,6 +1217,7 @@ int fde1d_run(int batch, int n, const double* alpha, double h, double dt, int K,
   ra.done = H->d_runctr + 4;
   ra.rq = H->d_runrq;
   ra.rq_cap = nrq;
+  ra.use_rq = 0;
   // per-step argument blocks (k_run.cuh RunArgs), copied to the device once per call
   LeafArgs la{};
   la.tree = H->tree; la.mode = 0; la.shift = H->shift; la.cfac = H->d_cfac; la.dt = dt;
@@ -1254,7 +1255,7 @@ int fde1d_run(int batch, int n, const double* alpha, double h, double dt, int K,
     // tree chain would put the extra chunks in the ready queue, where they wait for a CTA to
     // come free from leaf work; measured 630 vs 663 us/step at cfg3 (FDE_RUN_RC overrides)
     const int rcap = getenv("FDE_RUN_RC") ? std::max(1, atoi(getenv("FDE_RUN_RC"))) : 1;
-    for (int l = 0; l < L; ++l) tm.rc[l] = std::min(tm.rc[l], rcap);
+    for (int l = 0; l < L; ++l) { tm.rc[l] = std::min(tm.rc[l], rcap); if (tm.rc[l] > 1) ra.use_rq = 1; }
     tm.Q = Qp[p]; tm.Qleaf = Qp[p] + H->qlev[L]; tm.Sst = Sp[p]; tm.X = Xp[p];
     tm.u = u_out + m * cnt;
   }

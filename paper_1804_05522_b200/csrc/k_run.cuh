@@ -43,6 +43,7 @@ struct RunArgs {
   unsigned* heads;               // [0] tree units done, [1] leaf tickets, [2] rq tail, [3] rq head
   unsigned long long* rq;        // ready queue: task id + 1 per slot (zeroed), K * units per step
   long long rq_cap;              // slots
+  int use_rq;                    // some level splits its nodes into row chunks
   int* done; long long per_step; // step m counters: done + m * per_step (m = 0..K-1)
   long long o_A, o_R, o_pair, o_lvl[LMAX], o_kid[LMAX];   // o_kid[m]: completed children of level-m nodes
   unsigned long long* trace;     // optional (FDE_TRACE_RUN): [0] count, then [start,end,code,sm]
@@ -114,7 +115,8 @@ k_run(const RunArgs ra) {
       long long idx = 0;
       while (true) {
         if (cont >= 0) { q = 0; idx = cont; cont = -1; break; }
-        if (iou >= 0) {                               // then ready-queue work
+        if (!ra.use_rq) {                             // (one unit per node: nothing is ever queued)
+        } else if (iou >= 0) {                        // then ready-queue work
           unsigned long long v;
           asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ra.rq + iou) : "memory");
           if (v) { q = 0; idx = (long long)(v - 1); iou = -1; break; }
