@@ -64,6 +64,17 @@ struct LeafArgs {
 // ---- DMMA GEMMs on column-major shared-memory operands ---------------------------------
 // C[M x N] -= A[M x K] B[K x N]; tiles round-robin over warps [w0, w0 + nw); M, N % 8 == 0,
 // K % 4 == 0.  Optionally skips the tile block (skip_m0.., skip_n0..) of size 32 x 32.
+// Warp roles of the overlapped Gauss-Jordan.  Warp w runs on SM sub-partition w % 4, whose
+// FP64 pipe is shared by DFMA and DMMA (tools/gj_bench.cu: 233 cycles per pivot alone, 928
+// with DMMA warps on the same SMSPs, 306 with them on the other two).  SPLIT puts the GJ on
+// warps 0,1,4,5 (SMSPs 0,1) and the other work on SMSPs 2,3: used while the leaf is built
+// (FMA work), not in the LU, where the DMMA trailing update needs all four pipes
+// (measured: build+gj0 10.6 -> 9.6 us, but lu+store 27.1 -> 29.1 us per leaf with SPLIT).
+template <bool SPLIT>
+__device__ __forceinline__ bool gj_role(int warp) { return SPLIT ? (warp & 2) == 0 : warp < GJ_WARPS; }
+template <bool SPLIT>
+__device__ __forceinline__ int role_idx(int warp) { return SPLIT ? (warp & 1) | ((warp >> 2) << 1) : warp & 3; }
+
 template <bool ADD = false>
 __device__ __forceinline__ void cm_gemm_sub(double* C, int ldc, const double* A, int lda,
                                             const double* B, int ldb, int M, int N, int K, int w0,
@@ -182,14 +193,15 @@ __device__ __forceinline__ double fast_rcp(double x) {
   return fma(y, e, y);
 }
 
-// In-place inverse of a 32 x 32 column-major block by warps 0..3 (named barrier 1): unpivoted
-// Gauss-Jordan in registers, lane r of warp w owns A[r, 8w .. 8w+7].  Per pivot the pivot
+// In-place inverse of a 32 x 32 column-major block by the gj_role warps (named barrier 1): unpivoted
+// Gauss-Jordan in registers, lane r of role warp w owns A[r, 8w .. 8w+7].  Per pivot the pivot
 // row and column are published through a double-buffered shared scratch (buf, 128 doubles)
 // and one 128-thread barrier.  The blocks are diagonal blocks of Schur complements of a
 // strictly diagonally dominant matrix: no pivoting; a zero / non-finite pivot
 // latches FDE_ESINGULAR.
+template <bool SPLIT>
 __device__ __noinline__ void quad_gj_inv32(double* D, int ld, double* buf, DevStatus* st, int where) {
-  const int w = threadIdx.x >> 5, r = threadIdx.x & 31;
+  const int w = role_idx<SPLIT>(threadIdx.x >> 5), r = threadIdx.x & 31;
   double col[8];
 #pragma unroll
   for (int c = 0; c < 8; ++c) col[c] = D[r + (8 * w + c) * ld];
@@ -235,8 +247,8 @@ __device__ __noinline__ void quad_gj_inv32(double* D, int ld, double* buf, DevSt
 // off-diagonal blocks are stored negated (-Lt, -Ut) for the accumulate-only stripe solve:
 //   for kb:  D_k = (A_kk)^{-1} ;  -Lt_ik = -A_ik D_k (i > k) ;  -Ut_jk = -A_jk D_k (j < k)
 //            A_ij += (-Lt_ik) A_kj   (i, j > k)
-// With lookahead: the next diagonal block is updated first and inverted by warps 0..3 while
-// warps 4..7 finish the trailing update (three CTA barriers per block column).
+// With lookahead: the next diagonal block is updated first and inverted by warps 0..3
+// while the other four finish the trailing update (three CTA barriers per block column).
 __device__ void leaf_block_lu(double* A, int sp, double* prow, DevStatus* st, int where,
                               unsigned long long* trace = nullptr, bool gj0_done = false) {
   const int nb = sp >> 5, warp = threadIdx.x >> 5;
@@ -244,7 +256,7 @@ __device__ void leaf_block_lu(double* A, int sp, double* prow, DevStatus* st, in
   long long tl = clock64();
 #define LUT(i) do { if (tr) { const long long t_ = clock64(); trace[960 + (i)] += t_ - tl; tl = t_; } } while (0)
   if (!gj0_done) {
-    if (warp < GJ_WARPS) quad_gj_inv32(A, LDA_LEAF, prow, st, where);
+    if (warp < GJ_WARPS) quad_gj_inv32<false>(A, LDA_LEAF, prow, st, where);
     __syncthreads();
   }
   LUT(0);
@@ -268,14 +280,14 @@ __device__ void leaf_block_lu(double* A, int sp, double* prow, DevStatus* st, in
       __syncthreads();
       LUT(2);
 #ifdef FDE_LU_SERIAL
-      if (warp < GJ_WARPS) quad_gj_inv32(Akk, LDA_LEAF, prow, st, where);
+      if (warp < GJ_WARPS) quad_gj_inv32<false>(Akk, LDA_LEAF, prow, st, where);
       __syncthreads();
       if (sp - k1 > 32)
         cm_gemm_sub<true>(Akk, LDA_LEAF, Lk, LDA_LEAF, Uk, LDA_LEAF, sp - k1, sp - k1, 32, 0,
                           LEAF_WARPS, 0, 0);
       __syncthreads();
 #else
-      if (warp < GJ_WARPS) quad_gj_inv32(Akk, LDA_LEAF, prow, st, where);
+      if (warp < GJ_WARPS) quad_gj_inv32<false>(Akk, LDA_LEAF, prow, st, where);
       else if (sp - k1 > 32)
         cm_gemm_sub<true>(Akk, LDA_LEAF, Lk, LDA_LEAF, Uk, LDA_LEAF, sp - k1, sp - k1, 32, GJ_WARPS,
                           LEAF_WARPS - GJ_WARPS, 0, 0);
@@ -634,11 +646,13 @@ __device__ __forceinline__ void leaf_task(const LeafArgs& a, double* smem, int l
         dpr[u] = i < s ? dps[i] : 0.0;
         dmr[u] = i < s ? dms[i] : 0.0;
       }
-      // warps 0..3 build block column 0 first and invert its diagonal block (quad GJ) while
-      // warps 4..7 build the remaining columns (the first pivot chain overlaps the build)
-      const int jlo = warp < GJ_WARPS ? 8 * warp : 32 + (warp - GJ_WARPS);
-      const int jhi = warp < GJ_WARPS ? min(8 * warp + 8, sp) : sp;
-      const int jst = warp < GJ_WARPS ? 1 : LEAF_WARPS - GJ_WARPS;
+      // the gj_role warps build block column 0 first and invert its diagonal block (quad GJ)
+      // while the others build the remaining columns (the first pivot chain overlaps the build)
+      const bool gjw = gj_role<true>(warp);
+      const int rw = role_idx<true>(warp);
+      const int jlo = gjw ? 8 * rw : 32 + rw;
+      const int jhi = gjw ? min(8 * rw + 8, sp) : sp;
+      const int jst = gjw ? 1 : LEAF_WARPS - GJ_WARPS;
       for (int j = jlo; j < jhi; j += jst) {
 #pragma unroll
         for (int u = 0; u < LEAF_MAX / 32; ++u) {
@@ -652,9 +666,9 @@ __device__ __forceinline__ void leaf_task(const LeafArgs& a, double* smem, int l
         }
       }
       if (btr) { const long long t_ = clock64(); a.trace[981 + (t >> 7) * 4] = t_ - bt0; bt0 = t_; }
-      if (warp < GJ_WARPS) {
+      if (gjw) {
         asm volatile("bar.sync 1, %0;" ::"n"(GJ_WARPS * 32) : "memory");
-        quad_gj_inv32(A, LDA_LEAF, S + 272, a.st, where);    // (S + 272: clear of the staged tt)
+        quad_gj_inv32<true>(A, LDA_LEAF, S + 272, a.st, where);    // (S + 272: clear of the staged tt)
         if (btr) { const long long t_ = clock64(); a.trace[982] = t_ - bt0; }
       }
     }
