@@ -114,7 +114,10 @@ k_run(const RunArgs ra) {
       int q = -1;
       long long idx = 0;
       while (true) {
-        if (cont >= 0) { q = 0; idx = cont; cont = -1; break; }
+        if (cont >= 0) {                              // (released by our relaxed RMW on the
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");   // children's counters: acquire here)
+          q = 0; idx = cont; cont = -1; break;
+        }
         if (!ra.use_rq) {                             // (one unit per node: nothing is ever queued)
         } else if (iou >= 0) {                        // then ready-queue work
           unsigned long long v;
