@@ -125,6 +125,75 @@ __global__ void k_gather_cols(int m, int nk, const double* __restrict__ X, int l
   Y[(long long)j * ldy + i] = X[(long long)c * ldx + i] * (sc ? 1.0 / sc[c] : 1.0);
 }
 
+// Rank-revealing Householder QR with column pivoting (one CTA), truncation step of S10: W (m x n,
+// ld m, overwritten) <- H_k .. H_1 W, stopping at the first step k whose largest remaining column
+// norm is <= rtol * the largest initial column norm (the dropped block then has Frobenius norm
+// <= sqrt(n) rtol |W|_max-col).  Pivoting is by index (no column swaps), so rows 0..k-1 are
+// Q_k^T W in the original column order; they are written transposed to AT (n x k, ld n) and k
+// to *kout.  Residual column norms are recomputed every step (no downdating).
+__global__ void __launch_bounds__(DN_BIG)
+k_qrcp_rows(int m, int n, double* __restrict__ W, double rtol, double* __restrict__ AT, int* __restrict__ kout) {
+  __shared__ double v[EK_SMAX], nrm[EK_SMAX];
+  __shared__ double s_tau, s_n0;
+  __shared__ int s_jp, s_stop;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31, nw = DN_BIG / 32;
+  const int kmax = min(m, n);
+  int k = 0;
+  for (int step = 0; step < kmax; ++step) {
+    for (int j = warp; j < n; j += nw) {               // residual column norms, rows step..m-1
+      double a = 0.0;
+      for (int i = step + lane; i < m; i += 32) { const double x = W[(long long)j * m + i]; a = fma(x, x, a); }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+      if (lane == 0) nrm[j] = a;
+    }
+    __syncthreads();
+    if (warp == 0) {                                   // argmax (smallest index on ties)
+      double best = -1.0; int bj = 0;
+      for (int j = lane; j < n; j += 32) if (nrm[j] > best) { best = nrm[j]; bj = j; }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+        if (ob > best || (ob == best && oj < bj)) { best = ob; bj = oj; }
+      }
+      if (lane == 0) {
+        if (step == 0) s_n0 = best;
+        s_jp = bj;
+        s_stop = !(best > 0.0) || best <= rtol * rtol * s_n0;
+        if (!s_stop) {
+          const double x0 = W[(long long)bj * m + step], nx = sqrt(best);
+          const double al = x0 >= 0.0 ? -nx : nx;
+          v[0] = x0 - al;
+          s_tau = 1.0 / (nx * (nx + fabs(x0)));           // 2 / (v^T v)
+        }
+      }
+    }
+    __syncthreads();
+    if (s_stop) break;
+    const int jp = s_jp;
+    for (int i = step + 1 + t; i < m; i += DN_BIG) v[i - step] = W[(long long)jp * m + i];
+    __syncthreads();
+    const double tau = s_tau;
+    for (int j = warp; j < n; j += nw) {               // W[step:, j] -= tau v (v^T W[step:, j])
+      double* wc = W + (long long)j * m + step;
+      double a = 0.0;
+      for (int i = lane; i < m - step; i += 32) a = fma(v[i], wc[i], a);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+      a *= tau;
+      for (int i = lane; i < m - step; i += 32) wc[i] = fma(-a, v[i], wc[i]);
+    }
+    __syncthreads();
+    k = step + 1;
+  }
+  for (long long e = t; e < (long long)n * k; e += DN_BIG) {
+    const int j = (int)(e % n), i = (int)(e / n);
+    AT[(long long)i * n + j] = W[(long long)j * m + i];
+  }
+  if (t == 0) *kout = k;
+}
+
 // Newton sign iteration update (one CTA):  with mu = scaling,
 //   A <- (mu A + Ainv/mu)/2,  B <- (mu B + Binv/mu)/2,  C <- (mu C + (Ainv C Binv)/mu)/2 where
 //   T = Ainv C Binv is given; out[0] = ||A_new - A_old||_1-ish change measure.
@@ -573,7 +642,7 @@ extern "C" int fde2d_step(int nx, int ny, double alpha1, double alpha2, double h
   (void)hsum;
   if (resid_out) *resid_out = rel;
   if (iters_out) *iters_out = std::min(it, ek_maxit);
-  // ---- truncation: Y Z = W Sigma (one-sided Jacobi), X = (U W Sigma)(V Z)^T, keep sigma > tol sigma_1
+  // ---- truncation: X = U_s Y V_s^T with Y = sum sigma_i u_i w_i^T, keep sigma > tol sigma_1
   const int sa = sx.s, sbb = sy.s;
   const bool dbg2 = getenv("FDE_DEBUG2D") != nullptr;
   if (dbg2) {                                       // stored A U vs a fresh product, both sides
@@ -595,20 +664,35 @@ extern "C" int fde2d_step(int nx, int ny, double alpha1, double alpha2, double h
     }
   }
   if (dbg2) CU(cudaMemcpyAsync(w.M3, Ym, (size_t)sa * sbb * 8, cudaMemcpyDeviceToDevice, s));
-  { PROF("k_osj_svd"); k_osj_svd<<<1, DN_BIG, dn_smem((long long)sa * sbb, sbb + 2), s>>>(sa, sbb, Ym, sa, Zm, sig, 60); }
-  if ((rc = dn_check("k_osj_svd")) != FDE_OK) return fail(rc);
-  CU(cudaMemcpyAsync(hs.data(), sig, sbb * sizeof(double), cudaMemcpyDeviceToHost, s));
-  CU(cudaStreamSynchronize(s));
-  if (getenv("FDE_DEBUG2D")) {                      // orthogonality of the right singular vectors
-    std::vector<double> g((size_t)sbb * sbb);
-    if ((rc = ts_tn(s, sbb, sbb, sbb, 1.0, Zm, sbb, Zm, sbb, 0.0, w.G, sbb)) != FDE_OK) return fail(rc);
+  // Y (sa x sbb) is numerically low-rank: rank-revealing QR with column pivoting first
+  // (Q_k^T Y, k ~ final rank), then the one-sided Jacobi SVD of (Q_k^T Y)^T (sbb x k) gives Y's
+  // right singular vectors W and sigma; the left factor is Y W (exact product, no Q_k needed).
+  // (A Jacobi SVD of the whole sa x sbb Y cost ~50 ms per step at cfg5.)
+  int kq = 0;
+  {
+    int* kdev = reinterpret_cast<int*>(w.dv + 32);
+    CU(cudaMemcpyAsync(w.M4, Ym, (size_t)sa * sbb * 8, cudaMemcpyDeviceToDevice, s));
+    { PROF("k_qrcp_rows"); k_qrcp_rows<<<1, DN_BIG, 0, s>>>(sa, sbb, w.M4, 1e-2 * tol, w.V, kdev); }
+    if ((rc = dn_check("k_qrcp_rows")) != FDE_OK) return fail(rc);
+    CU(cudaMemcpyAsync(&kq, kdev, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+  }
+  if (kq > 0) {
+    { PROF("k_osj_svd"); k_osj_svd<<<1, DN_BIG, dn_smem((long long)sbb * kq, kq + 2), s>>>(sbb, kq, w.V, sbb, Zm, sig, 60); }
+    if ((rc = dn_check("k_osj_svd")) != FDE_OK) return fail(rc);
+    CU(cudaMemcpyAsync(hs.data(), sig, kq * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+  }
+  if (getenv("FDE_DEBUG2D") && kq > 0) {            // orthogonality of the Jacobi rotations
+    std::vector<double> g((size_t)kq * kq);
+    if ((rc = ts_tn(s, kq, kq, kq, 1.0, Zm, kq, Zm, kq, 0.0, w.G, kq)) != FDE_OK) return fail(rc);
     CU(cudaMemcpy(g.data(), w.G, g.size() * 8, cudaMemcpyDeviceToHost));
     double e = 0.0;
-    for (int i = 0; i < sbb; ++i) for (int j = 0; j < sbb; ++j) e = std::max(e, std::fabs(g[(size_t)i * sbb + j] - (i == j)));
-    fprintf(stderr, "fde2d svd: sa %d sb %d |Z^T Z - I|max %.3e sig1 %.3e\n", sa, sbb, e, hs[0]);
+    for (int i = 0; i < kq; ++i) for (int j = 0; j < kq; ++j) e = std::max(e, std::fabs(g[(size_t)i * kq + j] - (i == j)));
+    fprintf(stderr, "fde2d svd: sa %d sb %d qr rank %d |Z^T Z - I|max %.3e sig1 %.3e\n", sa, sbb, kq, e, hs[0]);
   }
-  ord.assign(sbb, 0);
-  for (int i = 0; i < sbb; ++i) ord[i] = i;
+  ord.assign(kq, 0);
+  for (int i = 0; i < kq; ++i) ord[i] = i;
   std::sort(ord.begin(), ord.end(), [&](int a, int c) { return hs[a] > hs[c] || (hs[a] == hs[c] && a < c); });
   keep.clear();
   for (int i : ord) if (hs[i] > tol * hs[ord[0]] && hs[i] > 0.0) keep.push_back(i);
@@ -616,15 +700,16 @@ extern "C" int fde2d_step(int nx, int ny, double alpha1, double alpha2, double h
   if (rk > rmax) { fail(FDE_OK); return set_err(FDE_EDIM, "solution rank %d exceeds rmax=%d", rk, rmax); }
   if (rk > 0) {
     CU(cudaMemcpyAsync(w.idx, keep.data(), rk * sizeof(int), cudaMemcpyHostToDevice, s));
-    { PROF("k_gather_cols"); k_gather_cols<<<(sa * rk + 255) / 256, 256, 0, s>>>(sa, rk, Ym, sa, w.idx, nullptr, w.M5, sa); }
-    { PROF("k_gather_cols"); k_gather_cols<<<(sbb * rk + 255) / 256, 256, 0, s>>>(sbb, rk, Zm, sbb, w.idx, nullptr, w.M6, sbb); }
+    // right vectors M6 = (AT Z)[:, keep] / sigma, left factor M5 = Y M6 (= U_k Sigma_k)
+    { PROF("k_gather_cols"); k_gather_cols<<<(sbb * rk + 255) / 256, 256, 0, s>>>(sbb, rk, w.V, sbb, w.idx, sig, w.M6, sbb); }
     if ((rc = dn_check("k_gather_cols")) != FDE_OK) return fail(rc);
+    if ((rc = ts_nn(s, sa, rk, sbb, 1.0, Ym, sa, w.M6, sbb, 0.0, w.M5, sa)) != FDE_OK) return fail(rc);
     if (dbg2) {                                     // |M5 M6^T - Y| / |Y|: the truncated assembly
       if ((rc = transpose(s, sbb, rk, w.M6, sbb, w.G, rk)) != FDE_OK) return fail(rc);
       if ((rc = ts_nn(s, sa, sbb, rk, 1.0, w.M5, sa, w.G, rk, -1.0, w.M3, sa)) != FDE_OK) return fail(rc);
       double d2 = 0.0, y2 = 0.0;
       if ((rc = sumsq(s, sa, sbb, w.M3, sa, w.dv + 8, &d2)) != FDE_OK) return fail(rc);
-      for (int i = 0; i < sbb; ++i) y2 += hs[i] * hs[i];
+      for (int i = 0; i < kq; ++i) y2 += hs[i] * hs[i];
       fprintf(stderr, "fde2d assembly: rk %d of %d, |M5 M6^T - Y|/|Y| %.3e, |Y| %.6e sig max %.3e min kept %.3e\n", rk, sbb,
               std::sqrt(d2 / y2), std::sqrt(y2), hs[ord[0]], hs[keep[rk - 1]]);
     }
