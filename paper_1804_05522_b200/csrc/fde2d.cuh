@@ -84,6 +84,15 @@ static int dn_attrs() {
   CU(cudaFuncSetAttribute(k_sym_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, DN_SMEM_MAX + 4096));
   CU(cudaFuncSetAttribute(k_osj_svd, cudaFuncAttributeMaxDynamicSharedMemorySize, DN_SMEM_MAX + 4096));
   CU(cudaFuncSetAttribute(k_gj_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, DN_SMEM_MAX + 4096));
+  // the per-step workspace comes from the device's default stream-ordered pool: keep freed
+  // blocks mapped across synchronisations (release threshold 0 would unmap and re-map ~50 MB
+  // every fde2d_step)
+  int dev = 0;
+  cudaMemPool_t pool;
+  CU(cudaGetDevice(&dev));
+  CU(cudaDeviceGetDefaultMemPool(&pool, dev));
+  unsigned long long keep_bytes = 1ULL << 30;
+  CU(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep_bytes));
   g_dn_attr = true;
   return FDE_OK;
 }
