@@ -388,12 +388,13 @@ k_gj_inverse(const InvJob* __restrict__ jobs, DevStatus* st) {
     __syncthreads();
     // Gauss-Jordan update: row k scaled, other rows eliminated; column k becomes -a_ik / p
     // (pivot row and column are read from the shared snapshots: no read-write race)
-    for (long long e = t; e < (long long)s * s; e += DN_BIG) {
-      const int i = (int)(e % s), j = (int)(e / s);
+    // (warp per column, lane per row: no 64-bit index division in the per-pivot sweep)
+    for (int j = warp; j < s; j += DN_BIG / 32) {
       if (j == k) continue;
       const double akj = rowk[j];
-      if (i == k) A[(long long)j * lda + i] = akj * rp;
-      else A[(long long)j * lda + i] = fma(-colk[i] * rp, akj, A[(long long)j * lda + i]);
+      double* Aj = A + (long long)j * lda;
+      for (int i = lane; i < s; i += 32)
+        Aj[i] = (i == k) ? akj * rp : fma(-colk[i] * rp, akj, Aj[i]);
     }
     __syncthreads();
     for (int i = t; i < s; i += DN_BIG) A[(long long)k * lda + i] = (i == k) ? rp : -colk[i] * rp;
