@@ -908,7 +908,7 @@ static int solve_impl(fde_hodlr* H, const double* b, const double* f, double* y,
   SaArgs sa{};
   sa.tree = H->tree; sa.Ainv = H->d_LU; sa.lustride = H->lustride; sa.b = b; sa.f = f; sa.dt = H->dt;
   sa.y = y; sa.nrhs = nrhs; sa.ld = ld;
-  { PROF("k_leaf_apply"); k_leaf_apply<<<dim3(H->nleaf, B), SA_THREADS, 0, s>>>(sa); }
+  { PROF("k_leaf_apply"); k_leaf_apply<<<dim3(H->nleaf, B, std::max(1, std::min((nrhs + SA_COLS - 1) / SA_COLS, 16))), SA_THREADS, 0, s>>>(sa); }
   LAUNCHED();
   SlArgs sl{};
   sl.tree = H->tree; sl.Lf = H->d_Lf; sl.lf_stride = H->lf_stride; sl.rank = H->d_rank;
@@ -916,7 +916,7 @@ static int solve_impl(fde_hodlr* H, const double* b, const double* f, double* y,
   sl.Y = y; sl.nrhs = nrhs; sl.ld = ld;
   for (int l = L - 1; l >= 0; --l) {
     sl.level = l; sl.k = H->kl[l]; sl.xcol = H->xcol[l]; sl.kofs = H->kofs[l];
-    { PROF("k_solve_level"); k_solve_level<<<dim3(1 << l, B), SL_THREADS, 0, s>>>(sl); }
+    { PROF("k_solve_level"); k_solve_level<<<dim3(1 << l, B, std::max(1, std::min(nrhs, 32))), SL_THREADS, 0, s>>>(sl); }
     LAUNCHED();
   }
   return FDE_OK;

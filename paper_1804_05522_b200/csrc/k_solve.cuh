@@ -32,7 +32,7 @@ k_leaf_apply(const SaArgs a) {
   const double* Ai = a.Ainv + (long long)inst * a.lustride + (long long)leaf * LEAF_MAX * LEAF_MAX;
   const long long ib = (long long)inst * a.ld * a.nrhs + r0;
   const int i = t % 128, h = t / 128;            // row, half of the j range
-  for (int c0 = 0; c0 < a.nrhs; c0 += SA_COLS) {
+  for (int c0 = blockIdx.z * SA_COLS; c0 < a.nrhs; c0 += gridDim.z * SA_COLS) {   // (column groups over grid.z)
     const int nc = min(SA_COLS, a.nrhs - c0);
     for (int e = t; e < s * nc; e += SA_THREADS) {
       const int j = e % s, cc = e / s;
@@ -83,7 +83,7 @@ k_solve_level(const SlArgs a) {
   const double* Ll = a.Lf + (long long)inst * a.lf_stride + tr.lev_lofs[l];
   const double* Kn = a.Kst + (long long)inst * a.kstride_inst + a.kofs + (long long)j * 3 * k * k;
   const double* W = a.X + (long long)inst * a.xstride + (long long)a.xcol * n;
-  for (int c = 0; c < a.nrhs; ++c) {
+  for (int c = blockIdx.z; c < a.nrhs; c += gridDim.z) {   // (right-hand sides over grid.z)
     double* y = a.Y + (long long)inst * a.ld * a.nrhs + (long long)c * a.ld;
     // a_q = V12[:, q]^T y2 (child 2 rows), b_q = V21[:, q]^T y1 (child 1 rows)
     for (int w = warp; w < 2 * k; w += SL_THREADS / 32) {
