@@ -70,7 +70,7 @@ struct SlArgs {
   double* Y; int nrhs, ld;
 };
 
-__global__ void __launch_bounds__(SL_THREADS, 3)   // (3 CTAs per SM: the right-hand-side loop over grid.z must not raise the register count)
+__global__ void __launch_bounds__(SL_THREADS, 4)   // (4 CTAs per SM: the right-hand-side loop over grid.z must not raise the register count)
 k_solve_level(const SlArgs a) {
   __shared__ double z[2 * KCAP];                 // [a (k) | b (k)]
   __shared__ double sv[2 * KCAP];                // [top (k) | y_v (k)]
