@@ -58,7 +58,7 @@ def test_bound_golden():
     with open(os.path.join(GOLDEN, "rank_bounds.txt")) as fh:
         rows = [l.split("#")[0].split() for l in fh if l.split("#")[0].strip()]
     for kind, N, eps, val in rows:
-        f = bound_B if kind == "B" else qsrank_bound_T
+        f = {"B": bound_B, "QT": qsrank_bound_T, "QA": qsrank_bound_A}[kind]
         assert f(int(N), float(eps)) == int(val)
 
 
