@@ -188,7 +188,7 @@ def run_reference(args, world, rank):
     wl = W.cfg3(K=2)
     steps = max(1, min(args.steps, 3))
     warm = max(0, min(args.warmup, 1))
-    base = cpu_oracle_baseline(wl, n_sample=4096, reps=warm + steps) if True else None
+    base = cpu_oracle_baseline(wl, n_sample=4096, reps=warm + steps)
     line = {"impl": "reference", "metric": METRIC, "value": base["value"], "unit": "time-steps/s",
             "n_gpus": args.gpus, "steps": steps, "warmup": warm,
             "ms_per_step": 1e3 / base["value"], "higher_is_better": True, "scaling": "weak",
@@ -335,33 +335,15 @@ def measure_small(dev, name, reps=3):
             "ranks": ranks, "timing": "CUDA events around one fde1d_run of all K steps, best of %d" % reps}
 
 
-def task_profile(st, wl, DPK, DMK, F, U0, K=16):
-    """Per-task durations inside k_run (untimed diagnostic run with FDE_TRACE_RUN): mean us per
-    task and SM-us per step / 148 for the leaf tasks A, B, B' and the tree levels."""
-    import collections
-    import tempfile
-    import torch
-    path = os.path.join(tempfile.gettempdir(), "fde_run_trace_%d.txt" % os.getpid())
-    os.environ["FDE_TRACE_RUN"] = path
-    try:
-        st.run(wl.dt, DPK[:K], DMK[:K], F, U0)
-        torch.cuda.synchronize()
-    finally:
-        del os.environ["FDE_TRACE_RUN"]
-    rows = [tuple(int(x) for x in ln.split()) for ln in open(path)]
-    os.remove(path)
-    names = {100: "A", 101: "B", 102: "B'", 103: "final"}
-    by = collections.defaultdict(list)
-    t0, t1 = min(r[0] for r in rows), max(r[1] for r in rows)
-    nsm = len(set(r[3] for r in rows))
-    for s_, e_, code, sm in rows:
-        kind = code % 1000
-        by[names.get(kind, "L%d" % kind)].append((e_ - s_) / 1e3)
-    busy = sum(sum(v) for v in by.values())
-    return {"steps": K, "us_per_step": (t1 - t0) / 1e3 / K, "sm_busy": busy / ((t1 - t0) / 1e3 * nsm),
-            "tasks": {k: {"n": len(v), "mean_us": sum(v) / len(v), "sm_us_per_step_per_sm": sum(v) / nsm / K}
-                      for k, v in sorted(by.items())},
-            "note": "diagnostic run with per-task globaltimer stamps (not the timed run)"}
+def task_profile(K=16):
+    """Per-task durations inside k_run: tools/task_profile.py in a subprocess against the
+    diagnostics library (libfdehodlr_dbg.so; the product library has no trace switches)."""
+    env = dict(os.environ, FDE_LIB_DEBUG="1")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "task_profile.py"), str(K)],
+                       env=env, capture_output=True, text=True, timeout=300)
+    if r.returncode != 0:
+        return {"error": (r.stderr or r.stdout)[-300:]}
+    return json.loads(r.stdout.strip().splitlines()[-1])
 
 
 def run_ours(args, world, rank, local):
@@ -556,7 +538,7 @@ def run_ours(args, world, rank, local):
             "other_variant": other}
     if not args.no_extra:
         try:
-            line["task_profile"] = task_profile(st, wl, DPK, DMK, F, U0)
+            line["task_profile"] = task_profile()
         except Exception as e:
             line["task_profile"] = {"error": str(e)[:200]}
         extra = {}

@@ -103,9 +103,11 @@ int hodlr_solve(fde_hodlr_t H, const double* b, double* x, int nrhs, int ld,
 int hodlr_matvec(fde_hodlr_t H, const double* x, double* y, int nrhs, int ld,
                  unsigned flags, void* stream);
 
-/* Device-side status latched by the kernels (call after synchronising the stream):
+/* Device-side status latched by the kernels (synchronises the handle's last stream):
  * returns FDE_OK / FDE_ESINGULAR / FDE_ENOCONV; *where (may be NULL) gets the instance*
- * 65536 + leaf-or-node index of the first failure. */
+ * 65536 + index of the first failure (leaf LU pivot: the leaf index; SMW capacitance
+ * pivot: 32768 + the node index 2^l - 1 + j; compression: the level).  A latched failure is reported once: returning it here
+ * (or from any call given FDE_SYNC) clears the word, so later calls on the handle start clean. */
 int hodlr_status(fde_hodlr_t H, int* where);
 
 /* Per-level compressed ranks of instance `inst` (host copy; synchronises the handle's

@@ -6,7 +6,9 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfdehodlr.so")
+# the diagnostics build (trace / experiment switches read from the environment) only on request
+LIB_PATH = os.path.join(HERE, "libfdehodlr_dbg.so" if os.environ.get("FDE_LIB_DEBUG") == "1"
+                        else "libfdehodlr.so")
 
 FDE_OK, FDE_EDOMAIN, FDE_EDIM, FDE_ESINGULAR, FDE_ENOCONV, FDE_ECUDA, FDE_ENOMEM = range(7)
 FDE_SYNC, FDE_CHECK, FDE_HOST_PTRS, FDE_NO_KEEP, FDE_RECOMPRESS, FDE_COMPRESS_ONLY = 1, 2, 4, 8, 16, 32
@@ -52,8 +54,8 @@ def load():
     if _lib is not None:
         return _lib
     if not os.path.exists(LIB_PATH):
-        raise FdeError(FDE_ECUDA, "libfdehodlr.so not built (run __graft_entry__.build() or "
-                                  "python paper_1804_05522_b200/build.py)")
+        raise FdeError(FDE_ECUDA, "%s not built (run __graft_entry__.build() or "
+                                  "python paper_1804_05522_b200/build.py)" % os.path.basename(LIB_PATH))
     lib = ctypes.CDLL(LIB_PATH)
     for name, (res, args) in SIGNATURES.items():
         fn = getattr(lib, name)

@@ -343,7 +343,7 @@ static int proj_sylvester(cudaStream_t s, const DenseWs& w, int sa, int sb, doub
     TRY(dn_check("k_sign_update"));
     CU(cudaMemcpyAsync(hout, w.dv, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
-    if (getenv("FDE_DEBUG2D") && getenv("FDE_DEBUG2D")[0] == '2')
+    if (fde_dbg_env("FDE_DEBUG2D") && fde_dbg_env("FDE_DEBUG2D")[0] == '2')
       fprintf(stderr, "  sign it %d change %.3e mu %.3e\n", it, hout[0], hout[1]);
     if (hout[0] < 1e-14) { ++it; break; }
   }
@@ -603,7 +603,7 @@ extern "C" int fde2d_step(int nx, int ny, double alpha1, double alpha2, double h
     double rp2 = 0.0;
     if ((rc = sumsq(s, sa, sbb, w.M1, sa, w.dv + 8, &rp2)) != FDE_OK) return rc;
     rel = std::sqrt((ra2 + rb2 + rp2) / cnorm2);
-    if (getenv("FDE_DEBUG2D")) {
+    if (fde_dbg_env("FDE_DEBUG2D")) {
       double oe[2] = {0.0, 0.0};
       for (int side = 0; side < 2; ++side) {
         const int ss = side ? sbb : sa, nn2 = side ? ny : nx;
@@ -653,7 +653,7 @@ extern "C" int fde2d_step(int nx, int ny, double alpha1, double alpha2, double h
   if (iters_out) *iters_out = std::min(it, ek_maxit);
   // ---- truncation: X = U_s Y V_s^T with Y = sum sigma_i u_i w_i^T, keep sigma > tol sigma_1
   const int sa = sx.s, sbb = sy.s;
-  const bool dbg2 = getenv("FDE_DEBUG2D") != nullptr;
+  const bool dbg2 = fde_dbg_env("FDE_DEBUG2D") != nullptr;
   if (dbg2) {                                       // stored A U vs a fresh product, both sides
     for (EkSide* e : {&sx, &sy}) {
       if ((rc = hodlr_mv_cols(e->H, e->U, Wt, e->s, s)) != FDE_OK) return fail(rc);
@@ -692,7 +692,7 @@ extern "C" int fde2d_step(int nx, int ny, double alpha1, double alpha2, double h
     CU(cudaMemcpyAsync(hs.data(), sig, kq * sizeof(double), cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
   }
-  if (getenv("FDE_DEBUG2D") && kq > 0) {            // orthogonality of the Jacobi rotations
+  if (fde_dbg_env("FDE_DEBUG2D") && kq > 0) {            // orthogonality of the Jacobi rotations
     std::vector<double> g((size_t)kq * kq);
     if ((rc = ts_tn(s, kq, kq, kq, 1.0, Zm, kq, Zm, kq, 0.0, w.G, kq)) != FDE_OK) return fail(rc);
     CU(cudaMemcpy(g.data(), w.G, g.size() * 8, cudaMemcpyDeviceToHost));

@@ -6,6 +6,18 @@
 
 #include "../../include/fdehodlr.h"
 
+// ---- diagnostics switches ----------------------------------------------------------------
+// Trace / experiment switches (FDE_TRACE_RUN, FDE_TRACE_STEP, FDE_TRACE_LEVELS, FDE_DEBUG2D,
+// FDE_LEVEL_PASSES, FDE_SPLIT_KERNELS) exist only in the diagnostics build
+// (libfdehodlr_dbg.so, compiled with -DFDE_DEBUG by build.py); the product library never reads
+// the environment, so its behaviour is fixed by the C-ABI arguments alone.
+#ifdef FDE_DEBUG
+#include <cstdlib>
+static inline const char* fde_dbg_env(const char* name) { return getenv(name); }
+#else
+static inline const char* fde_dbg_env(const char*) { return nullptr; }
+#endif
+
 // ---- capacities ---------------------------------------------------------------------
 #define LEAF_MAX   FDE_LEAF_MAX          // leaf held in shared memory (128 x 129 doubles)
 #define RCAP       FDE_RANK_MAX          // max compressed rank per level (T-block)

@@ -159,6 +159,7 @@ struct fde_hodlr {
   double *d_part = nullptr, *d_gram_part = nullptr, *d_gram = nullptr, *d_vkeep = nullptr;
   int *d_task_kr = nullptr, *d_task_rank = nullptr;
   DevStatus* d_status = nullptr;
+  int* d_flag = nullptr;            // FDE_CHECK result word (own allocation, never aliased)
   // staging for FDE_HOST_PTRS
   double *d_in = nullptr;   // 4 * batch * n
   double* d_rhs = nullptr;  // batch * n (solve-only rhs)
@@ -374,8 +375,6 @@ static int set_attrs() {
   CU(cudaFuncSetAttribute(k_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           LEAF_SMEM));
   CU(cudaFuncSetAttribute(k_lvl_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_REDUCE));
-  CU(cudaFuncSetAttribute(k_lvl_node, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_NODE));
-  CU(cudaFuncSetAttribute(k_lvl_update, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_UPDATE));
   CU(cudaFuncSetAttribute(k_mv_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_LEAF_SMEM));
   CU(cudaFuncSetAttribute(k_mv_update, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MV_UPDATE));
   CU(cudaFuncSetAttribute(k_levels<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, LV_SMEM_MAX));
@@ -407,7 +406,7 @@ __global__ void k_check_nonneg(const double* __restrict__ a, long long cnt, int*
 }
 
 static int check_nonneg(fde_hodlr* H, const double* dp, const double* dm, cudaStream_t s) {
-  int* bad = (int*)H->d_in;  // scratch (first 4 bytes of the staging area)
+  int* bad = H->d_flag;
   CU(cudaMemsetAsync(bad, 0, sizeof(int), s));
   const long long cnt = (long long)H->batch * H->n;
   { PROF("k_check_nonneg"); k_check_nonneg<<<(unsigned)((cnt + 255) / 256), 256, 0, s>>>(dp, cnt, bad); }
@@ -421,10 +420,20 @@ static int check_nonneg(fde_hodlr* H, const double* dp, const double* dm, cudaSt
   return FDE_OK;
 }
 
+// Read the latched device status after a synchronisation.  A failure is reported once: the
+// word is cleared when it is returned, so a later call on the same handle starts clean.
+static int read_status(fde_hodlr* H, DevStatus* out) {
+  DevStatus st{};
+  CU(cudaMemcpy(&st, H->d_status, sizeof(st), cudaMemcpyDeviceToHost));
+  if (st.code != FDE_OK) CU(cudaMemset(H->d_status, 0, sizeof(DevStatus)));
+  *out = st;
+  return FDE_OK;
+}
+
 static int sync_and_status(fde_hodlr* H, cudaStream_t s) {
   CU(cudaStreamSynchronize(s));
   DevStatus st{};
-  CU(cudaMemcpy(&st, H->d_status, sizeof(st), cudaMemcpyDeviceToHost));
+  TRY(read_status(H, &st));
   if (st.code != FDE_OK)
     return set_err(st.code, "device status %d at instance %d index %d", st.code, st.where / 65536,
                    st.where % 65536);
@@ -736,7 +745,7 @@ static int launch_levels(fde_hodlr* H, int mode, int nf, double* Y, int ld, int 
 
 // debug tracing buffer (FDE_TRACE_LEVELS): cleared before every leaf launch
 static int trace_reset(cudaStream_t s) {
-  if (!getenv("FDE_TRACE_LEVELS")) { g_trace = nullptr; return FDE_OK; }
+  if (!fde_dbg_env("FDE_TRACE_LEVELS")) { g_trace = nullptr; return FDE_OK; }
   if (!g_trace) CU(cudaMalloc(&g_trace, 8192 * sizeof(unsigned long long)));
   CU(cudaMemsetAsync(g_trace, 0, 8192 * sizeof(unsigned long long), s));
   return FDE_OK;
@@ -787,7 +796,8 @@ static int build_impl(int batch, int n, const double* alpha, double h, double dt
       (rc = dalloc(H, &H->d_vkeep, std::max<size_t>(1, ntask) * KRAW * RCAP)) ||
       (rc = dalloc(H, &H->d_task_kr, std::max<size_t>(1, ntask))) ||
       (rc = dalloc(H, &H->d_task_rank, std::max<size_t>(1, ntask))) ||
-      (rc = dalloc(H, &H->d_status, 1)) || (rc = dalloc(H, &H->d_in, 5 * B * n + 8)))
+      (rc = dalloc(H, &H->d_status, 1)) || (rc = dalloc(H, &H->d_flag, 1)) ||
+      (rc = dalloc(H, &H->d_in, 5 * B * n + 8)))
     return fail(rc);
   H->d_rhs = H->d_in + 4 * B * n;
   if (cudaMemcpy(H->d_alpha, alpha, B * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess ||
@@ -839,12 +849,12 @@ static int factor_impl(fde_hodlr* H, const double* dp, const double* dm, int nf,
   la.keep = keep; la.nf = nf; la.u_prev = u_prev; la.f = f; la.st = H->d_status;
   TRY(trace_reset(s));
   la.trace = g_trace;
-  const bool tree = nf == 1 && !keep && H->tree_ok && !getenv("FDE_LEVEL_PASSES");
+  const bool tree = nf == 1 && !keep && H->tree_ok && !fde_dbg_env("FDE_LEVEL_PASSES");
   if (tree) {
     la.Q = H->d_Q + H->qlev[L]; la.qinst = H->qinst;
     la.qstride = (long long)(H->xcol[L] - 1) * H->xcol[L];
   }
-  if (tree && !getenv("FDE_SPLIT_KERNELS")) {
+  if (tree && !fde_dbg_env("FDE_SPLIT_KERNELS")) {
     // one persistent dataflow launch: leaves -> tree levels -> u = X v (k_step.cuh)
     StepArgs sa{};
     sa.la = la;
@@ -853,8 +863,6 @@ static int factor_impl(fde_hodlr* H, const double* dp, const double* dm, int nf,
     a.L = L; a.NC = H->xcol[L]; a.nleaf = H->nleaf; a.batch = H->batch; a.kmaxc = H->kmax;
     for (int l = 0; l <= L; ++l) a.xc[l] = H->xcol[l];
     for (int m = 0; m < L; ++m) { a.rc[m] = H->trc[m]; a.slev[m] = H->slev[m]; }
-    if (const char* e = getenv("FDE_STEP_RC"))       // experiment: cap the row chunks per node
-      for (int m = 0; m < L; ++m) a.rc[m] = std::min(a.rc[m], std::max(1, atoi(e)));
     for (int m = 1; m <= L; ++m) a.qlev[m] = H->qlev[m];
     a.qinst = H->qinst; a.sinst = H->sinst;
     a.Qleaf = H->d_Q + H->qlev[L]; a.Q = H->d_Q; a.Sst = H->d_S;
@@ -866,7 +874,7 @@ static int factor_impl(fde_hodlr* H, const double* dp, const double* dm, int nf,
     for (int l = 0; l <= L; ++l) sa.dofs[l] = H->dofs[l];
     sa.lofs = H->lofs;
     static unsigned long long* step_trace = nullptr;
-    if (getenv("FDE_TRACE_STEP")) {
+    if (fde_dbg_env("FDE_TRACE_STEP")) {
       if (!step_trace) CU(cudaMalloc(&step_trace, 16384 * sizeof(unsigned long long)));
       CU(cudaMemsetAsync(step_trace, 0, 16384 * sizeof(unsigned long long), s));
       sa.trace = step_trace;
@@ -879,7 +887,7 @@ static int factor_impl(fde_hodlr* H, const double* dp, const double* dm, int nf,
       std::vector<unsigned long long> h(16384);
       CU(cudaStreamSynchronize(s));
       CU(cudaMemcpy(h.data(), sa.trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-      FILE* fo = fopen(getenv("FDE_TRACE_STEP"), "w");
+      FILE* fo = fopen(fde_dbg_env("FDE_TRACE_STEP"), "w");
       if (fo) {
         for (int i = 0; i < 4000; ++i)
           if (h[4 * i + 1]) fprintf(fo, "%d %llu %llu %llu %llu\n", i, h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3]);
@@ -951,6 +959,161 @@ static int matvec_impl(fde_hodlr* H, const double* x, double* y, int nrhs, int l
 
 // ---------------------------------------------------------------------------------------
 // C-ABI
+// One k_run launch of K <= RUN_KMAX pipelined steps: u_out[m] = A_m^{-1}(u^(m-1) + dt f^(m)),
+// u^(-1) = u0 (the caller's chunk base pointers).
+static int run_chunk(fde_hodlr* H, int K, double dt, const double* d_plus, const double* d_minus,
+                     long long coef_stride, const double* f, long long f_stride, const double* u0,
+                     double* u_out, cudaStream_t s) {
+  const size_t cnt = (size_t)H->batch * H->n;
+  const int L = H->L, B = H->batch;
+  // second buffer set + stored leaf LUs (allocated once per handle)
+  if (!H->d_X2) {
+    TRY(dalloc(H, &H->d_X2, (size_t)B * H->xstride));
+    TRY(dalloc(H, &H->d_Q2, (size_t)B * H->qinst));
+    TRY(dalloc(H, &H->d_S2, (size_t)B * H->sinst));
+    TRY(dalloc(H, &H->d_LUr[0], (size_t)B * H->lustride));
+    TRY(dalloc(H, &H->d_LUr[1], (size_t)B * H->lustride));
+  }
+  // per-step counters: A done [n_leaf], B' done [n_leaf], pair counters [B 2^(L-1)], per
+  // level m: chunk completions [B 2^m] and completed children [B 2^m]; ready queue: one slot
+  // per tree unit of the run
+  const long long n_leaf = (long long)B * H->nleaf;
+  RunArgs ra{};
+  long long o = 0, units = 0;
+  ra.o_A = o; o += n_leaf;
+  ra.o_R = o; o += n_leaf;
+  ra.o_pair = o; o += (long long)B << (L - 1);
+  for (int m = 0; m < L; ++m) {
+    ra.o_lvl[m] = o; o += (long long)B << m;
+    ra.o_kid[m] = o; o += (long long)B << m;
+    units += ((long long)B << m) * H->trc[m];
+  }
+  ra.per_step = o;
+  const long long need = 4 + (long long)K * o;
+  if (need > H->runctr_cap) {
+    if (H->d_runctr) { cudaStreamSynchronize(s); cudaFree(H->d_runctr); H->allocs.erase(std::find(H->allocs.begin(), H->allocs.end(), (void*)H->d_runctr)); }
+    TRY(dalloc(H, &H->d_runctr, (size_t)need));
+    H->runctr_cap = need;
+  }
+  const long long nrq = (long long)K * units;
+  if (nrq > H->runrq_cap) {
+    if (H->d_runrq) { cudaStreamSynchronize(s); cudaFree(H->d_runrq); H->allocs.erase(std::find(H->allocs.begin(), H->allocs.end(), (void*)H->d_runrq)); }
+    TRY(dalloc(H, &H->d_runrq, (size_t)nrq));
+    H->runrq_cap = nrq;
+  }
+  CU(cudaMemsetAsync(H->d_runctr, 0, need * sizeof(int), s));
+  CU(cudaMemsetAsync(H->d_runrq, 0, nrq * sizeof(unsigned long long), s));
+  ra.heads = reinterpret_cast<unsigned*>(H->d_runctr);
+  ra.done = H->d_runctr + 4;
+  ra.rq = H->d_runrq;
+  ra.rq_cap = nrq;
+  ra.use_rq = 0;
+  // per-step argument blocks (k_run.cuh RunArgs), copied to the device once per call
+  LeafArgs la{};
+  la.tree = H->tree; la.mode = 0; la.shift = H->shift; la.cfac = H->d_cfac; la.dt = dt;
+  la.g = H->d_g; la.gstride = H->gstride;
+  la.Lf = H->d_Lf; la.lf_stride = H->lf_stride; la.rank = H->d_rank;
+  for (int l = 0; l < L; ++l) { la.kl[l] = H->kl[l]; la.xcol[l] = H->xcol[l]; }
+  la.xcol[L] = H->xcol[L];
+  la.xstride = H->xstride; la.lustride = H->lustride; la.keep = 0; la.st = H->d_status;
+  la.qinst = H->qinst; la.qstride = (long long)(H->xcol[L] - 1) * H->xcol[L];
+  la.trace = nullptr; la.nf = 0; la.store_lu = 1;
+  TrArgs a = H->tr_geo;
+  a.L = L; a.NC = H->xcol[L]; a.nleaf = H->nleaf; a.batch = B; a.kmaxc = H->kmax;
+  for (int l = 0; l <= L; ++l) a.xc[l] = H->xcol[l];
+  for (int m = 0; m < L; ++m) { a.rc[m] = H->trc[m]; a.slev[m] = H->slev[m]; }
+  for (int m = 1; m <= L; ++m) a.qlev[m] = H->qlev[m];
+  a.qinst = H->qinst; a.sinst = H->sinst;
+  a.n = H->n; a.xstride = H->xstride;
+  a.leaf_r0 = H->tree.leaf_r0; a.leaf_n = H->tree.leaf_n;
+  a.bar = H->d_bar; a.st = H->d_status; a.trace = nullptr;
+  double* Xp[2] = {H->d_X, H->d_X2};
+  double* Qp[2] = {H->d_Q, H->d_Q2};
+  double* Sp[2] = {H->d_S, H->d_S2};
+  H->run_las.resize(K);
+  H->run_tas.resize(K);
+  for (int m = 0; m < K; ++m) {
+    const int p = m & 1;
+    LeafArgs& lm = H->run_las[m];
+    lm = la;
+    lm.dp = d_plus + m * coef_stride; lm.dm = d_minus + m * coef_stride; lm.f = f + m * f_stride;
+    lm.u_prev = m == 0 ? u0 : u_out + (m - 1) * cnt;
+    lm.X = Xp[p]; lm.LU = H->d_LUr[p]; lm.Q = Qp[p] + H->qlev[L];
+    TrArgs& tm = H->run_tas[m];
+    tm = a;
+    // one unit per node in the pipelined run: the row-chunk split that shortens k_step's exposed
+    // tree chain would put the extra chunks in the ready queue, where they wait for a CTA to
+    // come free from leaf work; measured 630 vs 663 us/step at cfg3
+    for (int l = 0; l < L; ++l) tm.rc[l] = 1;
+    tm.Q = Qp[p]; tm.Qleaf = Qp[p] + H->qlev[L]; tm.Sst = Sp[p]; tm.X = Xp[p];
+    tm.u = u_out + m * cnt;
+  }
+  static unsigned long long* run_trace = nullptr;
+  const long long run_trace_len = 4 + 4 * 262144;
+  if (fde_dbg_env("FDE_TRACE_RUN")) {
+    if (!run_trace) CU(cudaMalloc(&run_trace, run_trace_len * sizeof(unsigned long long)));
+    CU(cudaMemsetAsync(run_trace, 0, run_trace_len * sizeof(unsigned long long), s));
+    ra.trace = run_trace; ra.trace_cap = 262144;
+    static unsigned long long* run_prof = nullptr;
+    if (!run_prof) CU(cudaMalloc(&run_prof, 1200 * sizeof(unsigned long long)));
+    CU(cudaMemsetAsync(run_prof, 0, 1200 * sizeof(unsigned long long), s));
+    ra.prof = run_prof;
+    for (int m = 0; m < K; ++m) { H->run_las[m].prof = run_prof + 16; H->run_tas[m].trace = run_prof; }
+  }
+  const size_t args_bytes = (size_t)K * (sizeof(LeafArgs) + sizeof(TrArgs));
+  if (args_bytes > H->run_args_cap) {
+    if (H->d_run_args) { cudaStreamSynchronize(s); cudaFree(H->d_run_args); H->allocs.erase(std::find(H->allocs.begin(), H->allocs.end(), H->d_run_args)); }
+    H->d_run_args = nullptr;
+    CU(cudaMalloc(&H->d_run_args, args_bytes));
+    H->allocs.push_back(H->d_run_args);
+    H->run_args_cap = args_bytes;
+  }
+  // (host blocks are owned by the handle: they stay valid while the asynchronous copy reads them)
+  CU(cudaMemcpyAsync(H->d_run_args, H->run_las.data(), K * sizeof(LeafArgs), cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync((char*)H->d_run_args + K * sizeof(LeafArgs), H->run_tas.data(), K * sizeof(TrArgs),
+                     cudaMemcpyHostToDevice, s));
+  ra.las = reinterpret_cast<const LeafArgs*>(H->d_run_args);
+  ra.tas = reinterpret_cast<const TrArgs*>((char*)H->d_run_args + K * sizeof(LeafArgs));
+  ra.K = K;
+  ra.smem_doubles = (int)(H->step_smem / sizeof(double));
+  CU(cudaFuncSetAttribute(k_run, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)H->step_smem));
+  void* args[] = {&ra};
+  { PROF("k_run"); CU(cudaLaunchCooperativeKernel((void*)k_run, dim3(H->step_grid), dim3(TR_THREADS), args, H->step_smem, s)); }
+  LAUNCHED();
+  if (ra.trace) {                                 // FDE_TRACE_RUN=<file>: task timeline
+    std::vector<unsigned long long> h(run_trace_len);
+    CU(cudaStreamSynchronize(s));
+    CU(cudaMemcpy(h.data(), ra.trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    std::vector<unsigned long long> pf(1200);
+    CU(cudaMemcpy(pf.data(), ra.prof, 1200 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    for (int g = 0; g < 2; ++g) {
+      const unsigned long long* q = pf.data() + 1100 + 8 * g;
+      const double c = (double)std::max(1ULL, q[7]) * 1965.0;
+      fprintf(stderr, "k_run tree %s units (%llu): stage %.2f sc+T %.2f gj %.2f S %.2f Qupd %.2f (issue %.2f wait %.2f) us\n",
+              g ? "upper" : "bottom", q[7], q[0] / c, q[1] / c, q[2] / c, q[3] / c, q[4] / c, q[5] / c, q[6] / c);
+    }
+    {
+      const double c = (double)K * B * H->nleaf * 1965.0;
+      fprintf(stderr, "k_run A phases (us avg per leaf): build+gj0 %.2f lu+store %.2f panel %.2f\n",
+              pf[16] / c, pf[17] / c, pf[20] / c);
+    }
+    for (int g = 0; g < 2; ++g) {
+      const double c = (double)std::max(1ULL, pf[8 * g + 7]);
+      fprintf(stderr, "k_run %s phases (us avg over %llu): issue %.2f S %.2f v %.2f Xv %.2f LUwait %.2f solve %.2f\n",
+              g ? "final-only" : "B'", pf[8 * g + 7], pf[8 * g + 6] / c / 1965.0, pf[8 * g + 1] / c / 1965.0, pf[8 * g + 2] / c / 1965.0,
+              pf[8 * g + 3] / c / 1965.0, pf[8 * g + 4] / c / 1965.0, pf[8 * g + 5] / c / 1965.0);
+    }
+    FILE* fo = fopen(fde_dbg_env("FDE_TRACE_RUN"), "w");
+    if (fo) {
+      const long long ne = std::min<long long>((long long)h[0], ra.trace_cap);
+      for (long long e = 0; e < ne; ++e)
+        fprintf(fo, "%llu %llu %llu %llu\n", h[4 + 4 * e], h[5 + 4 * e], h[6 + 4 * e], h[7 + 4 * e]);
+      fclose(fo);
+    }
+  }
+  return FDE_OK;
+}
+
 extern "C" {
 
 const char* fde_last_error(void) { return g_last_error.c_str(); }
@@ -1065,7 +1228,7 @@ int hodlr_status(fde_hodlr_t H, int* where) {
   if (!H) return set_err(FDE_EDOMAIN, "handle is NULL");
   DevStatus st{};
   CU(cudaStreamSynchronize(H->last_stream));
-  CU(cudaMemcpy(&st, H->d_status, sizeof(st), cudaMemcpyDeviceToHost));
+  TRY(read_status(H, &st));
   if (where) *where = st.where;
   return st.code;
 }
@@ -1175,153 +1338,16 @@ int fde1d_run(int batch, int n, const double* alpha, double h, double dt, int K,
     return rc;
   }
   if (H->dt != dt) TRY(set_dt(H, dt, s));
-  const int L = H->L, B = H->batch;
-  // second buffer set + stored leaf LUs (allocated once per handle)
-  if (!H->d_X2) {
-    TRY(dalloc(H, &H->d_X2, (size_t)B * H->xstride));
-    TRY(dalloc(H, &H->d_Q2, (size_t)B * H->qinst));
-    TRY(dalloc(H, &H->d_S2, (size_t)B * H->sinst));
-    TRY(dalloc(H, &H->d_LUr[0], (size_t)B * H->lustride));
-    TRY(dalloc(H, &H->d_LUr[1], (size_t)B * H->lustride));
+  // chunks of at most RUN_KMAX steps per launch (the step index is a 16-bit field of the tree
+  // task ids, k_run.cuh rn_tid; the counters and argument blocks are sized per chunk); chunk c
+  // starts from the last solution of chunk c-1
+  for (int m0 = 0; m0 < K && rc == FDE_OK; m0 += RUN_KMAX) {
+    const int Kc = std::min(RUN_KMAX, K - m0);
+    rc = run_chunk(H, Kc, dt, d_plus + m0 * coef_stride, d_minus + m0 * coef_stride, coef_stride,
+                   f + m0 * f_stride, f_stride, m0 == 0 ? u0 : u_out + (size_t)(m0 - 1) * cnt,
+                   u_out + (size_t)m0 * cnt, s);
   }
-  // per-step counters: A done [n_leaf], B' done [n_leaf], pair counters [B 2^(L-1)], per
-  // level m: chunk completions [B 2^m] and completed children [B 2^m]; ready queue: one slot
-  // per tree unit of the run
-  const long long n_leaf = (long long)B * H->nleaf;
-  RunArgs ra{};
-  long long o = 0, units = 0;
-  ra.o_A = o; o += n_leaf;
-  ra.o_R = o; o += n_leaf;
-  ra.o_pair = o; o += (long long)B << (L - 1);
-  for (int m = 0; m < L; ++m) {
-    ra.o_lvl[m] = o; o += (long long)B << m;
-    ra.o_kid[m] = o; o += (long long)B << m;
-    units += ((long long)B << m) * H->trc[m];
-  }
-  ra.per_step = o;
-  const long long need = 4 + (long long)K * o;
-  if (need > H->runctr_cap) {
-    if (H->d_runctr) { cudaStreamSynchronize(s); cudaFree(H->d_runctr); H->allocs.erase(std::find(H->allocs.begin(), H->allocs.end(), (void*)H->d_runctr)); }
-    TRY(dalloc(H, &H->d_runctr, (size_t)need));
-    H->runctr_cap = need;
-  }
-  const long long nrq = (long long)K * units;
-  if (nrq > H->runrq_cap) {
-    if (H->d_runrq) { cudaStreamSynchronize(s); cudaFree(H->d_runrq); H->allocs.erase(std::find(H->allocs.begin(), H->allocs.end(), (void*)H->d_runrq)); }
-    TRY(dalloc(H, &H->d_runrq, (size_t)nrq));
-    H->runrq_cap = nrq;
-  }
-  CU(cudaMemsetAsync(H->d_runctr, 0, need * sizeof(int), s));
-  CU(cudaMemsetAsync(H->d_runrq, 0, nrq * sizeof(unsigned long long), s));
-  ra.heads = reinterpret_cast<unsigned*>(H->d_runctr);
-  ra.done = H->d_runctr + 4;
-  ra.rq = H->d_runrq;
-  ra.rq_cap = nrq;
-  ra.use_rq = 0;
-  // per-step argument blocks (k_run.cuh RunArgs), copied to the device once per call
-  LeafArgs la{};
-  la.tree = H->tree; la.mode = 0; la.shift = H->shift; la.cfac = H->d_cfac; la.dt = dt;
-  la.g = H->d_g; la.gstride = H->gstride;
-  la.Lf = H->d_Lf; la.lf_stride = H->lf_stride; la.rank = H->d_rank;
-  for (int l = 0; l < L; ++l) { la.kl[l] = H->kl[l]; la.xcol[l] = H->xcol[l]; }
-  la.xcol[L] = H->xcol[L];
-  la.xstride = H->xstride; la.lustride = H->lustride; la.keep = 0; la.st = H->d_status;
-  la.qinst = H->qinst; la.qstride = (long long)(H->xcol[L] - 1) * H->xcol[L];
-  la.trace = nullptr; la.nf = 0; la.store_lu = 1;
-  TrArgs a = H->tr_geo;
-  a.L = L; a.NC = H->xcol[L]; a.nleaf = H->nleaf; a.batch = B; a.kmaxc = H->kmax;
-  for (int l = 0; l <= L; ++l) a.xc[l] = H->xcol[l];
-  for (int m = 0; m < L; ++m) { a.rc[m] = H->trc[m]; a.slev[m] = H->slev[m]; }
-  for (int m = 1; m <= L; ++m) a.qlev[m] = H->qlev[m];
-  a.qinst = H->qinst; a.sinst = H->sinst;
-  a.n = H->n; a.xstride = H->xstride;
-  a.leaf_r0 = H->tree.leaf_r0; a.leaf_n = H->tree.leaf_n;
-  a.bar = H->d_bar; a.st = H->d_status; a.trace = nullptr;
-  double* Xp[2] = {H->d_X, H->d_X2};
-  double* Qp[2] = {H->d_Q, H->d_Q2};
-  double* Sp[2] = {H->d_S, H->d_S2};
-  H->run_las.resize(K);
-  H->run_tas.resize(K);
-  for (int m = 0; m < K; ++m) {
-    const int p = m & 1;
-    LeafArgs& lm = H->run_las[m];
-    lm = la;
-    lm.dp = d_plus + m * coef_stride; lm.dm = d_minus + m * coef_stride; lm.f = f + m * f_stride;
-    lm.u_prev = m == 0 ? u0 : u_out + (m - 1) * cnt;
-    lm.X = Xp[p]; lm.LU = H->d_LUr[p]; lm.Q = Qp[p] + H->qlev[L];
-    TrArgs& tm = H->run_tas[m];
-    tm = a;
-    // one unit per node in the pipelined run: the row-chunk split that shortens k_step's exposed
-    // tree chain would put the extra chunks in the ready queue, where they wait for a CTA to
-    // come free from leaf work; measured 630 vs 663 us/step at cfg3 (FDE_RUN_RC overrides)
-    const int rcap = getenv("FDE_RUN_RC") ? std::max(1, atoi(getenv("FDE_RUN_RC"))) : 1;
-    for (int l = 0; l < L; ++l) { tm.rc[l] = std::min(tm.rc[l], rcap); if (tm.rc[l] > 1) ra.use_rq = 1; }
-    tm.Q = Qp[p]; tm.Qleaf = Qp[p] + H->qlev[L]; tm.Sst = Sp[p]; tm.X = Xp[p];
-    tm.u = u_out + m * cnt;
-  }
-  static unsigned long long* run_trace = nullptr;
-  const long long run_trace_len = 4 + 4 * 262144;
-  if (getenv("FDE_TRACE_RUN")) {
-    if (!run_trace) CU(cudaMalloc(&run_trace, run_trace_len * sizeof(unsigned long long)));
-    CU(cudaMemsetAsync(run_trace, 0, run_trace_len * sizeof(unsigned long long), s));
-    ra.trace = run_trace; ra.trace_cap = 262144;
-    static unsigned long long* run_prof = nullptr;
-    if (!run_prof) CU(cudaMalloc(&run_prof, 1200 * sizeof(unsigned long long)));
-    CU(cudaMemsetAsync(run_prof, 0, 1200 * sizeof(unsigned long long), s));
-    ra.prof = run_prof;
-    for (int m = 0; m < K; ++m) { H->run_las[m].prof = run_prof + 16; H->run_tas[m].trace = run_prof; }
-  }
-  const size_t args_bytes = (size_t)K * (sizeof(LeafArgs) + sizeof(TrArgs));
-  if (args_bytes > H->run_args_cap) {
-    if (H->d_run_args) { cudaStreamSynchronize(s); cudaFree(H->d_run_args); H->allocs.erase(std::find(H->allocs.begin(), H->allocs.end(), H->d_run_args)); }
-    H->d_run_args = nullptr;
-    CU(cudaMalloc(&H->d_run_args, args_bytes));
-    H->allocs.push_back(H->d_run_args);
-    H->run_args_cap = args_bytes;
-  }
-  // (host blocks are owned by the handle: they stay valid while the asynchronous copy reads them)
-  CU(cudaMemcpyAsync(H->d_run_args, H->run_las.data(), K * sizeof(LeafArgs), cudaMemcpyHostToDevice, s));
-  CU(cudaMemcpyAsync((char*)H->d_run_args + K * sizeof(LeafArgs), H->run_tas.data(), K * sizeof(TrArgs),
-                     cudaMemcpyHostToDevice, s));
-  ra.las = reinterpret_cast<const LeafArgs*>(H->d_run_args);
-  ra.tas = reinterpret_cast<const TrArgs*>((char*)H->d_run_args + K * sizeof(LeafArgs));
-  ra.K = K;
-  ra.smem_doubles = (int)(H->step_smem / sizeof(double));
-  CU(cudaFuncSetAttribute(k_run, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)H->step_smem));
-  void* args[] = {&ra};
-  { PROF("k_run"); CU(cudaLaunchCooperativeKernel((void*)k_run, dim3(H->step_grid), dim3(TR_THREADS), args, H->step_smem, s)); }
-  LAUNCHED();
-  if (ra.trace) {                                 // FDE_TRACE_RUN=<file>: task timeline
-    std::vector<unsigned long long> h(run_trace_len);
-    CU(cudaStreamSynchronize(s));
-    CU(cudaMemcpy(h.data(), ra.trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-    std::vector<unsigned long long> pf(1200);
-    CU(cudaMemcpy(pf.data(), ra.prof, 1200 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-    for (int g = 0; g < 2; ++g) {
-      const unsigned long long* q = pf.data() + 1100 + 8 * g;
-      const double c = (double)std::max(1ULL, q[7]) * 1965.0;
-      fprintf(stderr, "k_run tree %s units (%llu): stage %.2f sc+T %.2f gj %.2f S %.2f Qupd %.2f (issue %.2f wait %.2f) us\n",
-              g ? "upper" : "bottom", q[7], q[0] / c, q[1] / c, q[2] / c, q[3] / c, q[4] / c, q[5] / c, q[6] / c);
-    }
-    {
-      const double c = (double)K * B * H->nleaf * 1965.0;
-      fprintf(stderr, "k_run A phases (us avg per leaf): build+gj0 %.2f lu+store %.2f panel %.2f\n",
-              pf[16] / c, pf[17] / c, pf[20] / c);
-    }
-    for (int g = 0; g < 2; ++g) {
-      const double c = (double)std::max(1ULL, pf[8 * g + 7]);
-      fprintf(stderr, "k_run %s phases (us avg over %llu): issue %.2f S %.2f v %.2f Xv %.2f LUwait %.2f solve %.2f\n",
-              g ? "final-only" : "B'", pf[8 * g + 7], pf[8 * g + 6] / c / 1965.0, pf[8 * g + 1] / c / 1965.0, pf[8 * g + 2] / c / 1965.0,
-              pf[8 * g + 3] / c / 1965.0, pf[8 * g + 4] / c / 1965.0, pf[8 * g + 5] / c / 1965.0);
-    }
-    FILE* fo = fopen(getenv("FDE_TRACE_RUN"), "w");
-    if (fo) {
-      const long long ne = std::min<long long>((long long)h[0], ra.trace_cap);
-      for (long long e = 0; e < ne; ++e)
-        fprintf(fo, "%llu %llu %llu %llu\n", h[4 + 4 * e], h[5 + 4 * e], h[6 + 4 * e], h[7 + 4 * e]);
-      fclose(fo);
-    }
-  }
+  if (rc != FDE_OK) { if (!cache) hodlr_destroy(H); return rc; }
   H->last_stream = s;
   H->factored = false;
   if ((flags & FDE_SYNC) || !cache) rc = sync_and_status(H, s);

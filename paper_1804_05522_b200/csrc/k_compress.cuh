@@ -16,7 +16,7 @@
 //   (2) recompression: eigen-decomposition of the small Gram L^T L = V diag(lam) V^T by
 //       cyclic Jacobi, keep lam >= tau (the eigenvalues of L L^T), L <- L V_keep.
 // The block error is <= 2 tau; the kept rank equals the truncated-SVD rank of the oracle
-// in every tested case (tests/test_parity_compress.py).
+// in every tested case (tests/test_parity_1d.py::test_ranks_equal_truncated_svd, tests/test_rank_study.py).
 //
 // (1) runs as one cooperative launch: each (instance, level) task is cut into chunks of
 // PC_ROWS rows, one CTA per chunk with its rows of L resident in shared memory; the CTAs

@@ -32,6 +32,10 @@
 #include "k_step.cuh"   // (k_final.cuh: leaf_rhs_final, rn_copy)
 
 
+// Steps per k_run launch: the step index is the 16-bit field of the tree task ids (rn_tid, kept
+// non-negative); fde1d_run splits longer runs into launches of at most RUN_KMAX steps.
+#define RUN_KMAX 8192
+
 struct RunArgs {
   // per-step argument blocks in device memory (host-filled): step m's d+-, f, u^(m-1), u^(m)
   // and the parity-(m & 1) buffer set (X, stored leaf LU, Q, S).  Read by reference from
@@ -71,6 +75,7 @@ __device__ __forceinline__ bool rn_leaf_ready(const RunArgs& ra, long long n_lea
 
 // Tree task ids: step (16 bits) | level m (8) | chunk (8) | node jj = inst 2^m + j (32).
 __device__ __forceinline__ long long rn_tid(int step, int m, int chunk, long long jj) {
+  // step < RUN_KMAX < 2^15, m < 2^8, chunk < 2^8, jj < 2^32: the id stays non-negative
   return ((long long)step << 48) | ((long long)m << 40) | ((long long)chunk << 32) | jj;
 }
 

@@ -110,8 +110,35 @@ def cfg4(batch=512, n=8192, K=16):
     # BASELINE configs[3] states no truncation tolerance.  Reading R18: tol 1e-13,
     # because at 1e-12 even the truncated-SVD definition of the compression (oracle) leaves a
     # forward error of 1.6e-8 > 1e-8 on the stiffest instance (alpha = 1.899); 1e-13 gives 7.7e-10.
-    return Workload1D("cfg4", batch, n, h, alpha, K, dt, 128, 1e-13, True,
-                      np.zeros((batch, n)), d, d.copy(), f, x)
+    wl = Workload1D("cfg4", batch, n, h, alpha, K, dt, 128, 1e-13, True,
+                    np.zeros((batch, n)), d, d.copy(), f, x)
+    wl.a, wl.b = a, b                # the per-instance coefficient parameters (d = a + b x)
+    return wl
+
+
+def cfg4_checked_instances(wl):
+    """The 16 cfg4 instances with a dense-oracle trajectory: the argmax /
+    argmin of alpha_i and of a_i + b_i (stiffest and mildest cases), then 12 drawn with
+    rng(40).choice from the rest."""
+    ext = [int(np.argmax(wl.alpha)), int(np.argmin(wl.alpha)),
+           int(np.argmax(wl.a + wl.b)), int(np.argmin(wl.a + wl.b))]
+    ext = list(dict.fromkeys(ext))
+    rest = np.setdiff1d(np.arange(wl.batch), ext)
+    picks = np.random.default_rng(40).choice(rest, 16 - len(ext), replace=False)
+    return ext + [int(i) for i in picks]
+
+
+def lowrank_state(nx, ny, r=27, seed=16, smax=1.0, smin=1e-10):
+    """A seeded rank-r 2D state U = Su Sv^T with the shape of a cfg5 solution: smooth columns
+    (8-mode sine series) and singular-value scales log-spaced from smax to smin (SURVEY.md
+    Appendix A6: the solution rank at tol 1e-12 is ~27 with singular values spanning ~1e-10
+    relative).  Used as the shared input of a late-step parity check."""
+    rng = np.random.default_rng(seed)
+    x = np.arange(1, nx + 1) / (nx + 1.0)
+    y = np.arange(1, ny + 1) / (ny + 1.0)
+    Su = _sine_series(x, rng.standard_normal((r, 8))).T * np.logspace(np.log10(smax), np.log10(smin), r)
+    Sv = _sine_series(y, rng.standard_normal((r, 8))).T
+    return Su, Sv
 
 
 def make_1d(n, alpha, leaf, tol, K=4, dt=None, kind="smooth", seed=7, batch=1):
