@@ -56,10 +56,14 @@ extern "C" {
 #define FDE_RECOMPRESS 16u /* fde1d_step: recompute S1 (GL weights) and S2 (compression of T)
                              even when the cached handle already holds them */
 
-/* Compile-time capacities of this build (see DESIGN.md). */
 #define FDE_COMPRESS_ONLY 32u /* hodlr_build: stop after S1-S2 (GL weights + compression); the handle
                                  serves hodlr_ranks / hodlr_status / hodlr_destroy only (rank
                                  studies beyond the factorisation's width limits) */
+#define FDE_COEFFS_CHANGED 64u /* fde2d_step: the coefficient arrays were rewritten in place since the
+                                 operators were factorised: refactorise them (the cache otherwise
+                                 refactorises only when dt or the coefficient pointers change) */
+
+/* Compile-time capacities of this build (see DESIGN.md). */
 #define FDE_LEAF_MAX  128 /* largest leaf (dense diagonal block) held in shared memory */
 #define FDE_RANK_MAX  47  /* largest compressed rank of one level's T-block */
 
@@ -153,12 +157,18 @@ int fde1d_run(int batch, int n, const double* alpha, double h, double dt, int K,
 /* One step of the 2D scheme as a Sylvester equation (Eq. 4.3, reading R11):
  *     A1 X + X A2^T = Uu Uv^T + dt Fu Fv^T,
  *     A1 = 1/2 I + (dt/hx^alpha1)(D1+ T1 + D1- T1^T),  A2 likewise in y,
- * solved by the extended Krylov method on the HODLR factors of A1 and A2.
+ * solved by the extended Krylov method on the HODLR factors of A1 and A2; the
+ * right-hand side is compressed by Householder QR of both factors + an SVD and the
+ * solution truncated at tol relative to its largest singular value.
  *   d1p, d1m [dev, nx]; d2p, d2m [dev, ny]; Fu [dev, nx*rf], Fv [dev, ny*rf];
  *   Uu [dev, nx*ru], Uv [dev, ny*ru] (ru may be 0); Xu [dev, nx*rmax], Xv [dev, ny*rmax].
- *   *rx receives the rank of X = Xu Xv^T; resid_out (host, may be NULL) the relative true
- *   residual; iters_out (host, may be NULL) the EK iterations.  cache[2] holds the two
- *   operator handles (built on first use, reused while the arguments match).
+ *   *rx receives the rank of X = Xu Xv^T; resid_out (host, may be NULL) the relative residual
+ *   ||A1 X + X A2^T - C||_F / ||C||_F of the RETURNED (truncated) X against the input C, with
+ *   A1, A2 the HODLR operators; iters_out (host, may be NULL) the EK iterations.  cache[2]
+ *   holds the two operator handles: built and factorised on first use, rebuilt when (n, alpha,
+ *   h, tol, leaf) change, refactorised when dt or the coefficient pointers change or flags has
+ *   FDE_COEFFS_CHANGED.  Device-side failures of either operator are reported (and cleared).
+ *   Synchronous: the EK iteration reads back the small quantities that steer it.
  *   Returns FDE_ENOCONV with the best iterate if ek_maxit is reached, FDE_EDIM if the
  *   truncated rank exceeds rmax. */
 int fde2d_step(int nx, int ny, double alpha1, double alpha2, double hx, double hy, double dt,
@@ -169,6 +179,30 @@ int fde2d_step(int nx, int ny, double alpha1, double alpha2, double hx, double h
                double tol, double ek_tol, int ek_maxit, int leaf,
                fde_hodlr_t* cache, double* resid_out, int* iters_out,
                unsigned flags, void* stream);
+
+/* The x/y split of the 2D step over two processes (the two extended block
+ * Arnoldi processes are independent): rank 0 owns A1, its Krylov basis and Xu; rank 1
+ * owns A2, its basis and Xv.  The sides couple only through four small exchanges per projected
+ * solve (the right-hand side's R factors, the projected matrices, the basis sizes, the residual
+ * parts), which the library hands to `gather`:
+ *   gather(ctx, send, recv, count, stream): all-gather `count` doubles of every rank's `send`
+ *   (device) into `recv` (device, world * count, rank order) ordered on `stream`; returns 0 on
+ *   success.  (The Python binding implements it with torch.distributed over NCCL.)
+ * The small dense work is repeated on both ranks on identical data, so both take the same
+ * decisions and return the same rank, residual and status.  world = 1 is fde2d_step (both sides
+ * local, the exchanges local copies; gather may be NULL).  Arguments as fde2d_step; a rank reads
+ * only its own side's arrays (d1p, d1m, Fu, Uu, Xu on rank 0; d2p, d2m, Fv, Uv, Xv on rank 1) and
+ * builds only its own operator in cache. */
+typedef int (*fde_allgather_fn)(void* ctx, const double* send, double* recv, long long count, void* stream);
+int fde2d_step_split(int world, int rank, fde_allgather_fn gather, void* ctx,
+                     int nx, int ny, double alpha1, double alpha2, double hx, double hy, double dt,
+                     const double* d1p, const double* d1m, const double* d2p, const double* d2m,
+                     const double* Fu, const double* Fv, int rf,
+                     const double* Uu, const double* Uv, int ru,
+                     double* Xu, double* Xv, int rmax, int* rx,
+                     double tol, double ek_tol, int ek_maxit, int leaf,
+                     fde_hodlr_t* cache, double* resid_out, int* iters_out,
+                     unsigned flags, void* stream);
 
 /* Thread-local description of the last error returned on this thread ("" if none). */
 const char* fde_last_error(void);

@@ -12,6 +12,7 @@ LIB_PATH = os.path.join(HERE, "libfdehodlr_dbg.so" if os.environ.get("FDE_LIB_DE
 
 FDE_OK, FDE_EDOMAIN, FDE_EDIM, FDE_ESINGULAR, FDE_ENOCONV, FDE_ECUDA, FDE_ENOMEM = range(7)
 FDE_SYNC, FDE_CHECK, FDE_HOST_PTRS, FDE_NO_KEEP, FDE_RECOMPRESS, FDE_COMPRESS_ONLY = 1, 2, 4, 8, 16, 32
+FDE_COEFFS_CHANGED = 64
 FDE_LEAF_MAX, FDE_RANK_MAX = 128, 47
 
 # every symbol the header declares, with its ctypes signature
@@ -33,11 +34,17 @@ SIGNATURES = {
                        _d, _i, _u, _ph, _p]),
     "fde2d_step": (_i, [_i, _i, _d, _d, _d, _d, _d, _p, _p, _p, _p, _p, _p, _i, _p, _p, _i,
                         _p, _p, _i, _pi, _d, _d, _i, _i, _ph, _pd, _pi, _u, _p]),
+    "fde2d_step_split": (_i, [_i, _i, _p, _p, _i, _i, _d, _d, _d, _d, _d, _p, _p, _p, _p, _p, _p, _i, _p, _p, _i,
+                              _p, _p, _i, _pi, _d, _d, _i, _i, _ph, _pd, _pi, _u, _p]),
     "fde_last_error": (ctypes.c_char_p, []),
     "fde_launch_count": (ctypes.c_longlong, []),
     "fde_profile_enable": (None, [_i]),
     "fde_profile_dump": (_i, [ctypes.c_char_p, _i]),
 }
+
+# all-gather callback of fde2d_step_split: (ctx, send, recv, count, stream) -> 0
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                ctypes.c_longlong, ctypes.c_void_p)
 
 _lib = None
 

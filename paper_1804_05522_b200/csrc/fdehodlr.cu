@@ -164,6 +164,7 @@ struct fde_hodlr {
   double *d_in = nullptr;   // 4 * batch * n
   double* d_rhs = nullptr;  // batch * n (solve-only rhs)
   bool factored = false;
+  const double *src_dp = nullptr, *src_dm = nullptr;   // fde2d_step: coefficient arrays factorised
   cudaStream_t last_stream = nullptr;
 };
 
@@ -367,9 +368,13 @@ static int set_dt(fde_hodlr* H, double dt, cudaStream_t s) {
   return FDE_OK;
 }
 
-static bool g_attr_done = false;
+// cudaFuncSetAttribute applies to the current device: one bit per device that has them
+static std::atomic<unsigned long long> g_attr_mask{0};
 static int set_attrs() {
-  if (g_attr_done) return FDE_OK;
+  int dev = 0;
+  CU(cudaGetDevice(&dev));
+  const unsigned long long bit = 1ULL << (dev & 63);
+  if (g_attr_mask.load() & bit) return FDE_OK;
   CU(cudaFuncSetAttribute(k_pchol, cudaFuncAttributeMaxDynamicSharedMemorySize, KRAW * PC_ROWS * 8));
   CU(cudaFuncSetAttribute(k_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * KRAW * KRAW * 8));
   CU(cudaFuncSetAttribute(k_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -380,7 +385,7 @@ static int set_attrs() {
   CU(cudaFuncSetAttribute(k_levels<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, LV_SMEM_MAX));
   CU(cudaFuncSetAttribute(k_levels<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, LV_SMEM_MAX));
   CU(cudaFuncSetAttribute(k_levels<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, LV_SMEM_MAX));
-  g_attr_done = true;
+  g_attr_mask.fetch_or(bit);
   return FDE_OK;
 }
 

@@ -139,10 +139,9 @@ k_pchol(const PcTask* __restrict__ tasks, const PcChunk* __restrict__ chunks,
   double d = valid ? gi[2 + 2 * i] : 0.0;            // diag of H_m: g_{2+2i}
   int k = 0;
   unsigned step = 0;
-  // Stopping threshold of the pivoted Cholesky: tau * PC_STOP (floored at the rounding level
-  // of the residual trace).  Stopping well below tau lets the optimal recompression below
-  // reproduce the truncated-SVD approximant (same rank, same accuracy; tests/ and DESIGN.md).
-  double stop_tau = tk.tau;
+  // Stopping threshold of the pivoted Cholesky (s_total below): tau * PC_STOP, floored at the
+  // rounding level of the residual trace.  Stopping well below tau lets the optimal
+  // recompression reproduce the truncated-SVD approximant (same rank; tests/ and DESIGN.md).
   for (;;) {
     // ---- local partials of the residual diagonal
     double s = block_sum(d, redv);
@@ -181,7 +180,6 @@ k_pchol(const PcTask* __restrict__ tasks, const PcChunk* __restrict__ chunks,
       }
     }
     __syncthreads();
-    stop_tau = s_total;
     if (s_stop) break;
     const int p = s_p;
     const double sp = sqrt(s_pmax);

@@ -193,8 +193,6 @@ __device__ void tr_unit(const TrArgs& a, double* sm, int inst, int m, int j, int
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31, gid = lane >> 2, tig = lane & 3;
   const int xm = a.xc[m], k = a.xc[m + 1] - xm, ncol1 = a.xc[m + 1];   // child Q: (ncol1-1) x ncol1
   const int lds = a.lds, ldk = a.ldk;
-  double* Bs = sm + a.off_B;      // k x k   (ld ldk)
-  double* Cs = sm + a.off_C;
   double* Ms = sm + a.off_M;      // Sc, then Sc^{-1} (Gauss-Jordan ping-pong with M2)
   double* M2 = sm + a.off_M2;
   double* Ss = sm + a.off_S;      // rows 0..k-1: S_top; rows k..2k-1: T, then S_bot (ld lds)

@@ -9,7 +9,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import check, FDE_SYNC, FDE_CHECK, FDE_HOST_PTRS, FDE_NO_KEEP, FDE_RECOMPRESS, FDE_COMPRESS_ONLY  # noqa: F401
+from ._lib import (check, FDE_SYNC, FDE_CHECK, FDE_HOST_PTRS, FDE_NO_KEEP, FDE_RECOMPRESS,  # noqa: F401
+                   FDE_COMPRESS_ONLY, FDE_COEFFS_CHANGED)
 
 
 def _stream(stream=None):
@@ -183,7 +184,7 @@ class Fde2dStepper:
         self.tol, self.ek_tol, self.ek_maxit, self.leaf, self.rmax = tol, ek_tol, ek_maxit, leaf, rmax
         self._cache = (ctypes.c_void_p * 2)()
 
-    def step(self, Fu, Fv, Uu=None, Uv=None, stream=None):
+    def step(self, Fu, Fv, Uu=None, Uv=None, flags=0, stream=None):
         """Fu (rf, nx), Fv (rf, ny), Uu (ru, nx), Uv (ru, ny): CUDA float64, one factor column per row."""
         dev = Fu.device
         rf = Fu.shape[0]
@@ -200,7 +201,7 @@ class Fde2dStepper:
             _dev(Uu, "Uu", ru * self.nx) if ru else nul, _dev(Uv, "Uv", ru * self.ny) if ru else nul, ru,
             _dev(Xu, "Xu"), _dev(Xv, "Xv"), self.rmax, ctypes.byref(rx), self.tol, self.ek_tol,
             self.ek_maxit, self.leaf, ctypes.cast(self._cache, ctypes.POINTER(ctypes.c_void_p)),
-            ctypes.byref(res), ctypes.byref(its), 0, _stream(stream)))
+            ctypes.byref(res), ctypes.byref(its), flags, _stream(stream)))
         r = rx.value
         return Xu[:r].contiguous(), Xv[:r].contiguous(), res.value, its.value
 

@@ -23,6 +23,7 @@ def lib():
 def header_functions():
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    src = re.sub(r"^\s*typedef[^;]*;", "", src, flags=re.M | re.S)      # (function-pointer typedefs)
     return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z_ ]+\*?\s*\b([a-z0-9_]+)\s*\(", src, flags=re.M)))
 
 
