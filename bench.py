@@ -188,7 +188,7 @@ def run_reference(args, world, rank):
     wl = W.cfg3(K=2)
     steps = max(1, min(args.steps, 3))
     warm = max(0, min(args.warmup, 1))
-    base = cpu_oracle_baseline(wl, n_sample=4096, reps=warm + steps)
+    base = cpu_oracle_baseline(wl, n_sample=8192, reps=warm + steps)      # (the same sample as our arm's)
     line = {"impl": "reference", "metric": METRIC, "value": base["value"], "unit": "time-steps/s",
             "n_gpus": args.gpus, "steps": steps, "warmup": warm,
             "ms_per_step": 1e3 / base["value"], "higher_is_better": True, "scaling": "weak",
@@ -204,10 +204,24 @@ def run_reference(args, world, rank):
 
 
 # ---------------------------------------------------------------------------------------
+def _max_over_ranks(dev, world, x):
+    if world > 1:
+        import torch
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+    return x
+
+
 def measure_cfg4(dev, world, rank, steps=16):
-    """BASELINE configs[3]: 512 independent n = 8192 problems, time-invariant d+- (factor
-    once), 16 steps; instances sharded over the ranks (shard.py), no collective in the
-    timed region.  Returns instance-steps/s over all ranks (max-over-ranks time)."""
+    """BASELINE configs[3]: 512 independent n = 8192 problems, time-invariant d+- (P:1333), 16
+    steps; instances sharded over the ranks (shard.py), no collective in the timed region.
+    Reported (instance-steps/s over all ranks, max-over-ranks device time):
+      value_factor_once        -- ONE figure for the whole run: the factorisation (fused with the
+                                  first step's solve) + the 15 further solves with the kept factor,
+                                  i.e. SURVEY §8(d)'s "factor once" protocol (its roofline: ~2.7e5);
+      value_solve_only         -- the 16 steps with an already kept factor (solve phase alone);
+      value_refactor_every_step / _pipelined_run -- d+- treated as new every step."""
     import torch
     from paper_1804_05522_b200 import workloads as W
     from paper_1804_05522_b200.hodlr import Fde1dStepper, FDE_NO_KEEP
@@ -220,90 +234,109 @@ def measure_cfg4(dev, world, rank, steps=16):
     DP, DM, F = t(dp[sl]), t(dm[sl]), t(wl.source(1)[sl])
     u = [t(wl.u0[sl]), torch.empty_like(t(wl.u0[sl]))]
     st = Fde1dStepper(wl.n, wl.alpha[sl], wl.h, wl.tol, wl.leaf, batch=run.count)
-    st.step(wl.dt, DP, DM, F, u[0], u_next=u[1], coeffs_changed=True)     # build + factor
+    st.step(wl.dt, DP, DM, F, u[0], u_next=u[1], coeffs_changed=True)     # build (S1-S2) + factor
     torch.cuda.synchronize()
 
-    def go(refactor):
+    def timed(fn):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
         a.record()
-        for k in range(steps):
-            # refactor: the fused factor + solve step (k_step, FDE_NO_KEEP) every step
-            st.step(wl.dt, DP, DM, F, u[k % 2], u_next=u[(k + 1) % 2], coeffs_changed=refactor,
-                    flags=FDE_NO_KEEP if refactor else 0)
+        fn()
         b.record()
         torch.cuda.synchronize()
-        ms = a.elapsed_time(b)
-        if world > 1:
-            x = torch.tensor([ms], device=dev, dtype=torch.float64)
-            torch.distributed.all_reduce(x, op=torch.distributed.ReduceOp.MAX)
-            ms = float(x.item())
+        ms = _max_over_ranks(dev, world, a.elapsed_time(b))
         return wl.batch * steps / (ms / 1e3), ms
-    go(False)
-    v_reuse, ms_reuse = go(False)
-    v_ref, ms_ref = go(True)
 
-    def go_run():                                   # refactor every step, K steps in one k_run
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        if world > 1:
-            torch.distributed.barrier()
-        torch.cuda.synchronize()
-        a.record()
-        st.run(wl.dt, DP[None], DM[None], F[None], u[0], K=steps)
-        b.record()
-        torch.cuda.synchronize()
-        ms = a.elapsed_time(b)
-        if world > 1:
-            x = torch.tensor([ms], device=dev, dtype=torch.float64)
-            torch.distributed.all_reduce(x, op=torch.distributed.ReduceOp.MAX)
-            ms = float(x.item())
-        return wl.batch * steps / (ms / 1e3), ms
+    def factor_once():                               # factor (fused with step 1) + 15 solves
+        for k in range(steps):
+            st.step(wl.dt, DP, DM, F, u[k % 2], u_next=u[(k + 1) % 2], coeffs_changed=(k == 0))
+
+    def solve_only():
+        for k in range(steps):
+            st.step(wl.dt, DP, DM, F, u[k % 2], u_next=u[(k + 1) % 2], coeffs_changed=False)
+
+    def refactor():
+        for k in range(steps):
+            st.step(wl.dt, DP, DM, F, u[k % 2], u_next=u[(k + 1) % 2], coeffs_changed=True, flags=FDE_NO_KEEP)
+    factor_once()
+    v_once, ms_once = timed(factor_once)
+    factor_once()                                    # (re-keep the factor for the solve-only pass)
+    v_solve, ms_solve = timed(solve_only)
+    v_ref, ms_ref = timed(refactor)
     try:
-        go_run()
-        v_run, ms_run = go_run()
+        st.run(wl.dt, DP[None], DM[None], F[None], u[0], K=steps)
+        v_run, ms_run = timed(lambda: st.run(wl.dt, DP[None], DM[None], F[None], u[0], K=steps))
     except Exception as e:                          # (memory for the second buffer set)
         v_run, ms_run = None, str(e)[:120]
     st.close()
     return {"workload": "cfg4: 512 x n=8192, alpha_i~U(1.1,1.9), 16 steps, leaf 128, tol 1e-13 (R18)",
-            "metric": "instance-steps/s", "value_factor_once": v_reuse, "ms_16_steps_factor_once": ms_reuse,
+            "metric": "instance-steps/s",
+            "value_factor_once": v_once, "ms_16_steps_factor_once": ms_once,
+            "value_solve_only": v_solve, "ms_16_steps_solve_only": ms_solve,
             "value_refactor_every_step": v_ref, "ms_16_steps_refactor": ms_ref,
             "value_refactor_pipelined_run": v_run, "ms_16_steps_refactor_pipelined_run": ms_run,
+            "survey_roofline_factor_once": 2.7e5,
             "sharding": "%d instances per rank (shard.py), no data-path collective" % run.count}
 
 
-def measure_cfg5(dev, steps=4):
-    """BASELINE configs[4]: 2D Sylvester step (fde2d_step), nx = ny = 2048, first `steps`
-    steps of the trajectory (coefficients time-invariant: operators factored once)."""
+def measure_cfg5(dev, world, rank, steps=16):
+    """BASELINE configs[4]: the 2D Sylvester step, nx = ny = 2048, all 16 steps of the trajectory
+    (operators factorised once: the coefficients are time-invariant).  world = 1: fde2d_step.
+    world >= 2: the x/y split (split2d.py, fde2d_step_split) on rank pairs; pairs beyond the first
+    solve their own replica of the problem (value = all pairs' steps / max time)."""
     import torch
     from paper_1804_05522_b200 import workloads as W
     from paper_1804_05522_b200.hodlr import Fde2dStepper
     wl = W.cfg5()
     t = lambda a: torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device=dev)
-    st = Fde2dStepper(wl.nx, wl.ny, wl.alpha1, wl.alpha2, wl.hx, wl.hy, wl.dt, t(wl.d1p), t(wl.d1m),
-                      t(wl.d2p), t(wl.d2m), wl.tol, ek_tol=wl.ek_tol, leaf=wl.leaf)
     Fs = [tuple(t(f.T) for f in wl.source_factors(m)) for m in range(1, steps + 1)]
-    Xu, Xv, _, _ = st.step(*Fs[0])                     # builds + factors the two operators
+    args = (wl.nx, wl.ny, wl.alpha1, wl.alpha2, wl.hx, wl.hy, wl.dt, t(wl.d1p), t(wl.d1m), t(wl.d2p), t(wl.d2m), wl.tol)
+    if world == 1:
+        st = Fde2dStepper(*args, ek_tol=wl.ek_tol, leaf=wl.leaf)
+        stepf = lambda m, X: st.step(*Fs[m]) if X is None else st.step(*Fs[m], *X)
+        own = lambda out: (out[0], out[1])
+        pairs, psize = 1, 1
+    else:
+        from paper_1804_05522_b200.split2d import SplitSylvesterStepper, pair_group
+        g, prank, psize = pair_group(world, rank)
+        st = SplitSylvesterStepper(*args, ek_tol=wl.ek_tol, leaf=wl.leaf, group=g, world=psize, rank=prank)
+        pairs = world // 2
+
+        def stepf(m, X):
+            Fu, Fv = Fs[m]
+            if psize == 1:
+                return st.step(Fu, Fv, *(X if X is not None else (None, None)))
+            if prank == 0:
+                return st.step(Fu, None, X, None)
+            return st.step(None, Fv, None, X)
+        own = lambda out: out[0]
+    X = own(stepf(0, None))                             # builds + factors the operator(s)
     torch.cuda.synchronize()
-    el = None
-    for rep in range(3):                               # host-timed: best of 3 (host jitter)
-        t0 = time.perf_counter()
-        Xu = Xv = None
-        its = []
+
+    def trajectory():
+        X, its = None, []
         for m in range(steps):
-            if Xu is None:
-                Xu, Xv, res, it = st.step(*Fs[m])
-            else:
-                Xu, Xv, res, it = st.step(*Fs[m], Xu, Xv)
-            its.append(it)
-        torch.cuda.synchronize()
-        e = time.perf_counter() - t0
-        el = e if el is None else min(el, e)
+            out = stepf(m, X)
+            X = own(out)
+            its.append(out[-1])
+        return X, its
+    trajectory()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    X, its = trajectory()
+    torch.cuda.synchronize()
+    el = _max_over_ranks(dev, world, time.perf_counter() - t0)
     st.close()
-    return {"workload": "cfg5: 2D nx=ny=2048, alpha=(1.3,1.7), rank-4 source, ek_tol 1e-11, tol 1e-12",
-            "metric": "time-steps/s", "value": steps / el, "steps": steps, "ek_iterations": its,
-            "final_rank": int(Xu.shape[0]), "timing": "host wall clock around synchronous fde2d_step calls, best of 3 runs"}
+    return {"workload": "cfg5: 2D nx=ny=2048, alpha=(1.3,1.7), rank-4 source, ek_tol 1e-11, tol 1e-12, all %d steps" % steps,
+            "metric": "time-steps/s", "value": max(1, pairs) * steps / el, "ms_per_step": 1e3 * el / steps,
+            "steps": steps, "ek_iterations": its,
+            "parallelism": "single GPU" if world == 1 else "x/y split over rank pairs (%d pair(s) of %d)" % (pairs, psize),
+            "timing": "host wall clock around the synchronous fde2d_step calls of the whole trajectory "
+                      "(max over ranks); the step reads back the small quantities that steer EK"}
 
 
 def measure_small(dev, name, reps=3):
@@ -551,11 +584,10 @@ def run_ours(args, world, rank, local):
             extra["cfg4"] = measure_cfg4(dev, world, rank)
         except Exception as e:                              # reported, not fatal for the headline
             extra["cfg4"] = {"error": str(e)[:200]}
-        if world == 1:
-            try:
-                extra["cfg5"] = measure_cfg5(dev)
-            except Exception as e:
-                extra["cfg5"] = {"error": str(e)[:200]}
+        try:
+            extra["cfg5"] = measure_cfg5(dev, world, rank)
+        except Exception as e:
+            extra["cfg5"] = {"error": str(e)[:200]}
         line["other_configs"] = extra
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_oracle_baseline(wl)
