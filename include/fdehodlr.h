@@ -69,6 +69,12 @@ extern "C" {
 
 typedef struct fde_hodlr* fde_hodlr_t;   /* opaque; one per (operator family, batch) */
 
+/* All-gather callback of the split entry points (fde1d_step_split, fde2d_step_split):
+ * gather(ctx, send, recv, count, stream) gathers `count` doubles of every rank's `send` (device)
+ * into `recv` (device, world * count, rank order), ordered on `stream`; returns 0 on success.
+ * The Python binding implements it with torch.distributed (NCCL over NVLink on the GPU box). */
+typedef int (*fde_allgather_fn)(void* ctx, const double* send, double* recv, long long count, void* stream);
+
 /* Build the HODLR representation of `batch` operators
  *     A_b = shift*I + (dt/h^alpha_b)(D+_b T_{alpha_b} + D-_b T_{alpha_b}^T),  b < batch,
  * i.e. steps S1 (GL weights) and S2 (per-level compression of the Toeplitz
@@ -135,6 +141,25 @@ int fde1d_step(int batch, int n, const double* alpha, double h, double dt,
                const double* u_prev, double* u_next, double tol, int leaf,
                int coeffs_changed, unsigned flags, fde_hodlr_t* cache, void* stream);
 
+/* One implicit-Euler step of ONE problem (batch 1) split over `world` ranks at the top of the HODLR
+ * tree (every lower off-diagonal block is a sub-block of
+ * the top-level ones).  world = 2^p; rank g owns the leaves [g, g+1) * nleaf/world, i.e. the rows
+ * [g, g+1) * n/world, and runs the leaf work (assembly, LU, panel, projection) and the SMW levels
+ * p .. L-1 of its subtree; the parts then exchange the level-p projected matrices of their subtree
+ * roots ((xc_p - 1) x xc_p doubles each), every rank runs the top levels 0 .. p-1 on the same data
+ * and the finals u = X v of its own leaves, and u_next's row blocks are all-gathered, so every rank
+ * returns the full u_next.  Same arithmetic as fde1d_step with FDE_NO_KEEP (d+- new every step).
+ *   gather: as fde2d_step_split (all-gather of `count` doubles per rank, rank order) -- NULL only
+ *   at world 1; rank = -1: run every part in this process, one launch after the other (the
+ *   launches of a world-rank split, for checking and per-part timing).
+ *   Needs the tree path with L >= p and equal leaves (n = number of leaves x leaf size): FDE_EDIM
+ *   otherwise.  u_next must not alias u_prev.  d_plus_m, d_minus_m, f_m, u_prev [dev, n] on every
+ *   rank (each reads its rows); cache as fde1d_step. */
+int fde1d_step_split(int world, int rank, fde_allgather_fn gather, void* ctx, int n, double alpha, double h,
+                     double dt, const double* d_plus_m, const double* d_minus_m, const double* f_m,
+                     const double* u_prev, double* u_next, double tol, int leaf, unsigned flags,
+                     fde_hodlr_t* cache, void* stream);
+
 /* K implicit-Euler steps of Eq. (2.5) in one pipelined launch (fused factor + solve every step,
  * P:1310-1315):  u^(m) = A_m^{-1}(u^(m-1) + dt f^(m)),  m = 1..K.  The coefficient-dependent
  * leaf work of step m+1 (LU, U columns of the panel, their projection) overlaps the tree levels
@@ -193,7 +218,6 @@ int fde2d_step(int nx, int ny, double alpha1, double alpha2, double hx, double h
  * local, the exchanges local copies; gather may be NULL).  Arguments as fde2d_step; a rank reads
  * only its own side's arrays (d1p, d1m, Fu, Uu, Xu on rank 0; d2p, d2m, Fv, Uv, Xv on rank 1) and
  * builds only its own operator in cache. */
-typedef int (*fde_allgather_fn)(void* ctx, const double* send, double* recv, long long count, void* stream);
 int fde2d_step_split(int world, int rank, fde_allgather_fn gather, void* ctx,
                      int nx, int ny, double alpha1, double alpha2, double hx, double hy, double dt,
                      const double* d1p, const double* d1m, const double* d2p, const double* d2m,

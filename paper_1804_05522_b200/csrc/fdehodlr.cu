@@ -165,6 +165,7 @@ struct fde_hodlr {
   double* d_rhs = nullptr;  // batch * n (solve-only rhs)
   bool factored = false;
   const double *src_dp = nullptr, *src_dm = nullptr;   // fde2d_step: coefficient arrays factorised
+  double* d_split = nullptr;        // fde1d_step_split: send staging (n doubles)
   cudaStream_t last_stream = nullptr;
 };
 
@@ -839,6 +840,56 @@ static int build_impl(int batch, int n, const double* alpha, double h, double dt
   return FDE_OK;
 }
 
+// One k_step launch over a part of the step (StepArgs in k_step.cuh): leaves [lf0, lf1), tree
+// levels [mlo, mhi) (restricted to the part's nodes or all), leaf tasks and/or finals.
+struct StepPart { int lf0, lf1, mlo, mhi, restrict_nodes, do_leaf, do_final; };
+
+static int launch_step(fde_hodlr* H, const LeafArgs& la, const StepPart& pt, double* u_next, cudaStream_t s,
+                       const char* prof_name = "k_step") {
+  const int L = H->L;
+  StepArgs sa{};
+  sa.la = la;
+  TrArgs& a = sa.ta;
+  a = H->tr_geo;
+  a.L = L; a.NC = H->xcol[L]; a.nleaf = H->nleaf; a.batch = H->batch; a.kmaxc = H->kmax;
+  for (int l = 0; l <= L; ++l) a.xc[l] = H->xcol[l];
+  for (int m = 0; m < L; ++m) { a.rc[m] = H->trc[m]; a.slev[m] = H->slev[m]; }
+  for (int m = 1; m <= L; ++m) a.qlev[m] = H->qlev[m];
+  a.qinst = H->qinst; a.sinst = H->sinst;
+  a.Qleaf = H->d_Q + H->qlev[L]; a.Q = H->d_Q; a.Sst = H->d_S;
+  a.X = H->d_X; a.xstride = H->xstride; a.n = H->n;
+  a.leaf_r0 = H->tree.leaf_r0; a.leaf_n = H->tree.leaf_n;
+  a.u = u_next; a.bar = H->d_bar; a.st = H->d_status; a.trace = nullptr;
+  sa.ctr = reinterpret_cast<unsigned*>(H->d_done);
+  sa.done = H->d_done;
+  for (int l = 0; l <= L; ++l) sa.dofs[l] = H->dofs[l];
+  sa.lofs = H->lofs;
+  sa.lf0 = pt.lf0; sa.lf1 = pt.lf1; sa.mlo = pt.mlo; sa.mhi = pt.mhi;
+  sa.restrict_nodes = pt.restrict_nodes; sa.do_leaf = pt.do_leaf; sa.do_final = pt.do_final;
+  static unsigned long long* step_trace = nullptr;
+  if (fde_dbg_env("FDE_TRACE_STEP")) {
+    if (!step_trace) CU(cudaMalloc(&step_trace, 16384 * sizeof(unsigned long long)));
+    CU(cudaMemsetAsync(step_trace, 0, 16384 * sizeof(unsigned long long), s));
+    sa.trace = step_trace;
+  }
+  CU(cudaMemsetAsync(H->d_done, 0, H->ndone * sizeof(int), s));
+  void* args[] = {&sa};
+  { PROF(prof_name); CU(cudaLaunchCooperativeKernel((void*)k_step, dim3(H->step_grid), dim3(TR_THREADS), args, H->step_smem, s)); }
+  LAUNCHED();
+  if (sa.trace) {
+    std::vector<unsigned long long> h(16384);
+    CU(cudaStreamSynchronize(s));
+    CU(cudaMemcpy(h.data(), sa.trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    FILE* fo = fopen(fde_dbg_env("FDE_TRACE_STEP"), "w");
+    if (fo) {
+      for (int i = 0; i < 4000; ++i)
+        if (h[4 * i + 1]) fprintf(fo, "%d %llu %llu %llu %llu\n", i, h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3]);
+      fclose(fo);
+    }
+  }
+  return FDE_OK;
+}
+
 // factor (nf = 0) or fused factor + solve of one rhs column (nf = 1: b = u + dt f -> u_next)
 static int factor_impl(fde_hodlr* H, const double* dp, const double* dm, int nf, const double* u_prev,
                        const double* f, double* u_next, int keep, cudaStream_t s) {
@@ -861,45 +912,8 @@ static int factor_impl(fde_hodlr* H, const double* dp, const double* dm, int nf,
   }
   if (tree && !fde_dbg_env("FDE_SPLIT_KERNELS")) {
     // one persistent dataflow launch: leaves -> tree levels -> u = X v (k_step.cuh)
-    StepArgs sa{};
-    sa.la = la;
-    TrArgs& a = sa.ta;
-    a = H->tr_geo;
-    a.L = L; a.NC = H->xcol[L]; a.nleaf = H->nleaf; a.batch = H->batch; a.kmaxc = H->kmax;
-    for (int l = 0; l <= L; ++l) a.xc[l] = H->xcol[l];
-    for (int m = 0; m < L; ++m) { a.rc[m] = H->trc[m]; a.slev[m] = H->slev[m]; }
-    for (int m = 1; m <= L; ++m) a.qlev[m] = H->qlev[m];
-    a.qinst = H->qinst; a.sinst = H->sinst;
-    a.Qleaf = H->d_Q + H->qlev[L]; a.Q = H->d_Q; a.Sst = H->d_S;
-    a.X = H->d_X; a.xstride = H->xstride; a.n = H->n;
-    a.leaf_r0 = H->tree.leaf_r0; a.leaf_n = H->tree.leaf_n;
-    a.u = u_next; a.bar = H->d_bar; a.st = H->d_status; a.trace = nullptr;
-    sa.ctr = reinterpret_cast<unsigned*>(H->d_done);
-    sa.done = H->d_done;
-    for (int l = 0; l <= L; ++l) sa.dofs[l] = H->dofs[l];
-    sa.lofs = H->lofs;
-    static unsigned long long* step_trace = nullptr;
-    if (fde_dbg_env("FDE_TRACE_STEP")) {
-      if (!step_trace) CU(cudaMalloc(&step_trace, 16384 * sizeof(unsigned long long)));
-      CU(cudaMemsetAsync(step_trace, 0, 16384 * sizeof(unsigned long long), s));
-      sa.trace = step_trace;
-    }
-    CU(cudaMemsetAsync(H->d_done, 0, H->ndone * sizeof(int), s));
-    void* args[] = {&sa};
-    { PROF("k_step"); CU(cudaLaunchCooperativeKernel((void*)k_step, dim3(H->step_grid), dim3(TR_THREADS), args, H->step_smem, s)); }
-    LAUNCHED();
-    if (sa.trace) {
-      std::vector<unsigned long long> h(16384);
-      CU(cudaStreamSynchronize(s));
-      CU(cudaMemcpy(h.data(), sa.trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-      FILE* fo = fopen(fde_dbg_env("FDE_TRACE_STEP"), "w");
-      if (fo) {
-        for (int i = 0; i < 4000; ++i)
-          if (h[4 * i + 1]) fprintf(fo, "%d %llu %llu %llu %llu\n", i, h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3]);
-        fclose(fo);
-      }
-    }
-    return FDE_OK;
+    StepPart whole{0, H->nleaf, 0, L, 0, 1, 1};
+    return launch_step(H, la, whole, u_next, s);
   }
   { PROF("k_leaf"); k_leaf<<<dim3(H->nleaf, B), LEAF_THREADS, LEAF_SMEM, s>>>(la); }
   LAUNCHED();
@@ -1309,6 +1323,90 @@ int fde1d_step(int batch, int n, const double* alpha, double h, double dt, const
   if ((flags & FDE_SYNC) || !cache || (flags & FDE_HOST_PTRS)) rc = sync_and_status(H, s);
   if (!cache) hodlr_destroy(H);
   return rc;
+}
+
+int fde1d_step_split(int world, int rank, fde_allgather_fn gather, void* ctx, int n, double alpha, double h,
+                     double dt, const double* d_plus_m, const double* d_minus_m, const double* f_m,
+                     const double* u_prev, double* u_next, double tol, int leaf, unsigned flags,
+                     fde_hodlr_t* cache, void* stream) {
+  g_last_error.clear();
+  TRY(check_common(1, n, &alpha, h, dt, tol, leaf));
+  if (world < 1 || (world & (world - 1))) return set_err(FDE_EDOMAIN, "world=%d must be a power of two", world);
+  if (rank < -1 || rank >= world) return set_err(FDE_EDOMAIN, "rank=%d outside [-1, %d)", rank, world);
+  if (rank >= 0 && world > 1 && !gather) return set_err(FDE_EDOMAIN, "world > 1 needs an all-gather callback");
+  if (!d_plus_m || !d_minus_m || !f_m || !u_prev || !u_next) return set_err(FDE_EDOMAIN, "NULL array argument");
+  if (u_next == u_prev) return set_err(FDE_EDOMAIN, "u_next must not alias u_prev");
+  cudaStream_t s = (cudaStream_t)stream;
+  fde_hodlr* H = cache ? *cache : nullptr;
+  if (H) {
+    const bool same = H->batch == 1 && H->n == n && H->h == h && H->leaf == leaf && H->tol == tol &&
+                      H->shift == 1.0 && H->alpha[0] == alpha && !H->compress_only;
+    if (!same) { hodlr_destroy(H); H = nullptr; if (cache) *cache = nullptr; }
+  }
+  if (!H) {
+    TRY(build_impl(1, n, &alpha, h, dt, nullptr, nullptr, 1.0, tol, leaf, 0, s, &H));
+    if (cache) *cache = H;
+  }
+  auto out = [&](int rc) { if (!cache) hodlr_destroy(H); return rc; };
+  int p = 0;
+  while ((1 << p) < world) ++p;
+  const int L = H->L, NL = H->nleaf;
+  if (!H->tree_ok || L < p || NL % world != 0)
+    return out(set_err(FDE_EDIM, "the split needs the tree path with L >= log2(world) (L=%d, world=%d)", L, world));
+  for (int i = 1; i < NL; ++i)
+    if (H->leaf_n[i] != H->leaf_n[0]) return out(set_err(FDE_EDIM, "the split needs equal leaves (n = leaves x leaf)"));
+  if (H->dt != dt) { const int rc = set_dt(H, dt, s); if (rc) return out(rc); }
+  LeafArgs la{};
+  la.tree = H->tree; la.mode = 0; la.shift = H->shift; la.cfac = H->d_cfac; la.dt = dt;
+  la.g = H->d_g; la.gstride = H->gstride; la.dp = d_plus_m; la.dm = d_minus_m;
+  la.Lf = H->d_Lf; la.lf_stride = H->lf_stride; la.rank = H->d_rank;
+  for (int l = 0; l < L; ++l) { la.kl[l] = H->kl[l]; la.xcol[l] = H->xcol[l]; }
+  la.xcol[L] = H->xcol[L];
+  la.X = H->d_X; la.xstride = H->xstride; la.LU = H->d_LU; la.lustride = H->lustride;
+  la.keep = 0; la.nf = 1; la.u_prev = u_prev; la.f = f_m; la.st = H->d_status;
+  la.Q = H->d_Q + H->qlev[L]; la.qinst = H->qinst; la.qstride = (long long)(H->xcol[L] - 1) * H->xcol[L];
+  const int per = NL / world;
+  int rc = FDE_OK;
+  if (rank < 0) {
+    // every part in this process, one after the other (no part waits on another's launch):
+    // the same launches the ranks of a world-sized split run, for checking and per-part timing
+    for (int g = 0; g < world && rc == FDE_OK; ++g)
+      rc = launch_step(H, la, StepPart{g * per, (g + 1) * per, p, L, 1, 1, 0}, nullptr, s, "k_step_part");
+    if (rc == FDE_OK) rc = launch_step(H, la, StepPart{0, NL, 0, p, 0, 0, 1}, u_next, s, "k_step_top");
+  } else {
+    if (!H->d_split) {
+      const long long qs = (long long)(H->xcol[p] - 1) * H->xcol[p];
+      rc = dalloc(H, &H->d_split, (size_t)std::max<long long>(qs, n));
+    }
+    // 1. the part's leaves and its subtree (levels p .. L-1)
+    if (rc == FDE_OK) rc = launch_step(H, la, StepPart{rank * per, (rank + 1) * per, p, L, 1, 1, 0}, nullptr, s, "k_step_part");
+    // 2. the level-p projected matrices of the subtree roots, node g from rank g (P:1169-1177:
+    //    every lower block is a sub-block of the top-level ones; the top levels couple the parts
+    //    only through these (xc_p - 1) x xc_p matrices)
+    if (rc == FDE_OK && world > 1) {
+      const long long qs = (long long)(H->xcol[p] - 1) * H->xcol[p];
+      double* Qp = H->d_Q + H->qlev[p];
+      if (cudaMemcpyAsync(H->d_split, Qp + rank * qs, qs * sizeof(double), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+        rc = set_err(FDE_ECUDA, "split staging copy failed");
+      else if (gather(ctx, H->d_split, Qp, qs, s) != 0)
+        rc = set_err(FDE_ECUDA, "split exchange callback failed");
+    }
+    // 3. the top levels 0 .. p-1 (every rank, same data: same S) and the part's finals
+    if (rc == FDE_OK) rc = launch_step(H, la, StepPart{rank * per, (rank + 1) * per, 0, p, 0, 0, 1}, u_next, s, "k_step_top");
+    // 4. u_next rows of every part
+    if (rc == FDE_OK && world > 1) {
+      const long long rows = (long long)n / world;
+      if (cudaMemcpyAsync(H->d_split, u_next + rank * rows, rows * sizeof(double), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+        rc = set_err(FDE_ECUDA, "split staging copy failed");
+      else if (gather(ctx, H->d_split, u_next, rows, s) != 0)
+        rc = set_err(FDE_ECUDA, "split exchange callback failed");
+    }
+  }
+  if (rc != FDE_OK) return out(rc);
+  H->last_stream = s;
+  H->factored = false;
+  if ((flags & FDE_SYNC) || !cache) rc = sync_and_status(H, s);
+  return out(rc);
 }
 
 int fde1d_run(int batch, int n, const double* alpha, double h, double dt, int K, const double* d_plus,

@@ -21,6 +21,12 @@ struct StepArgs {
                                  // dofs[L]: [inst][level L-1 node] count of projected leaves
   long long lofs;                // [inst][leaf] panel-done flags
   unsigned long long* trace;     // optional: [task][start, end, kind, sm] (FDE_TRACE_STEP)
+  // part of the step (the top-level split of one problem over ranks; batch 1):
+  //   leaf tasks and finals for leaves [lf0, lf1); tree levels m in [mlo, mhi); restrict = 1:
+  //   only the nodes of level m above [lf0, lf1); level mhi - 1's children (level mhi) were
+  //   completed by an earlier launch when mhi < L (no wait).  Whole step: lf0 = 0, lf1 = nleaf,
+  //   mlo = 0, mhi = L, restrict = 0, do_leaf = do_final = 1.
+  int lf0, lf1, mlo, mhi, restrict_nodes, do_leaf, do_final;
 };
 
 __device__ __forceinline__ int st_ld_acquire(const int* p) {
@@ -49,11 +55,21 @@ k_step(const StepArgs sa) {
   __shared__ int task;
   const TrArgs& a = sa.ta;
   const int B = a.batch, L = a.L, nleaf = a.nleaf;
-  const long long n_leaf = (long long)B * nleaf;
+  // leaves of the part (per instance) and the nodes of each processed level
+  const int lcnt = sa.lf1 - sa.lf0;
+  const long long n_leaf = sa.do_leaf ? (long long)B * lcnt : 0;
   long long n_lvl[LMAX];
+  int j0[LMAX], jn[LMAX];
   long long total = 2 * n_leaf;                    // panel tasks, then projection tasks
-  for (int m = L - 1; m >= 0; --m) { n_lvl[m] = (long long)B * (1LL << m) * a.rc[m]; total += n_lvl[m]; }
-  const long long n_fin = (n_leaf + TR_NL - 1) / TR_NL;
+  for (int m = L - 1; m >= 0; --m) {
+    const bool on = m >= sa.mlo && m < sa.mhi;
+    j0[m] = sa.restrict_nodes ? (sa.lf0 >> (L - m)) : 0;
+    jn[m] = !on ? 0 : (sa.restrict_nodes ? (lcnt >> (L - m)) : (1 << m));
+    n_lvl[m] = (long long)B * jn[m] * a.rc[m];
+    total += n_lvl[m];
+  }
+  const long long n_fin_leaves = sa.do_final ? (long long)B * lcnt : 0;
+  const long long n_fin = (n_fin_leaves + TR_NL - 1) / TR_NL;
   total += n_fin;
   while (true) {
     __syncthreads();                               // (task of the previous iteration consumed)
@@ -74,16 +90,18 @@ k_step(const StepArgs sa) {
       }
     };
     if (tk < n_leaf) {                             // ---- leaf: build, LU, panel X
-      const int inst = (int)(tk / nleaf), leaf = (int)(tk % nleaf);
+      const int inst = (int)(tk / lcnt), leaf = sa.lf0 + (int)(tk % lcnt);
+      const long long gl = (long long)inst * nleaf + leaf;
       leaf_task(sa.la, smem, leaf, inst, false);
-      st_signal(sa.done + sa.lofs + tk);
+      st_signal(sa.done + sa.lofs + gl);
       rec(100);
       continue;
     }
     tk -= n_leaf;
     if (tk < n_leaf) {                             // ---- leaf: projection Q = V^T X
-      const int inst = (int)(tk / nleaf), leaf = (int)(tk % nleaf);
-      st_wait(sa.done + sa.lofs + tk, 1);
+      const int inst = (int)(tk / lcnt), leaf = sa.lf0 + (int)(tk % lcnt);
+      const long long gl = (long long)inst * nleaf + leaf;
+      st_wait(sa.done + sa.lofs + gl, 1);
       leaf_proj_task(sa.la, smem, leaf, inst);
       st_signal(sa.done + sa.dofs[L] + (long long)inst * (1 << (L - 1)) + (leaf >> 1));
       rec(101);
@@ -93,27 +111,35 @@ k_step(const StepArgs sa) {
     int m = L - 1;
     while (m >= 0 && tk >= n_lvl[m]) { tk -= n_lvl[m]; --m; }
     if (m >= 0) {                                  // ---- SMW unit of level m
-      const long long per_inst = (1LL << m) * a.rc[m];
+      const long long per_inst = (long long)jn[m] * a.rc[m];
       const int inst = (int)(tk / per_inst), w = (int)(tk % per_inst);
-      const int j = w / a.rc[m], chunk = w % a.rc[m];
+      const int j = j0[m] + w / a.rc[m], chunk = w % a.rc[m];
       if (m == L - 1) {
         st_wait(sa.done + sa.dofs[L] + (long long)inst * (1 << (L - 1)) + j, 2);
-      } else {
+      } else if (m + 1 < sa.mhi) {
         const int* c = sa.done + sa.dofs[m + 1] + (long long)inst * (1 << (m + 1)) + 2 * j;
         st_wait(c, a.rc[m + 1]);
         st_wait(c + 1, a.rc[m + 1]);
-      }
+      }                                            // (else: children from an earlier launch)
       tr_unit(a, smem, inst, m, j, chunk);
       st_signal(sa.done + sa.dofs[m] + (long long)inst * (1 << m) + j);
       rec(m);
       continue;
     }
-    // ---- final group: u = X v for TR_NL leaves (needs every ancestor's S: the root's done)
+    // ---- final group: u = X v for TR_NL leaves of the part (needs every ancestor's S: the
+    //      root's done -- in this launch if it holds level 0, else from an earlier launch)
     const long long lu0 = tk * TR_NL;
-    const int nl = (int)min((long long)TR_NL, n_leaf - lu0);
-    const int i0 = (int)(lu0 / nleaf), i1 = (int)((lu0 + nl - 1) / nleaf);
-    for (int inst = i0; inst <= i1; ++inst) st_wait(sa.done + sa.dofs[0] + inst, a.rc[0]);
-    tr_final(a, smem, (int)lu0, nl);
+    const int nl = (int)min((long long)TR_NL, n_fin_leaves - lu0);
+    const int i0 = (int)(lu0 / lcnt), i1 = (int)((lu0 + nl - 1) / lcnt);
+    if (sa.mlo == 0 && sa.mhi > 0)
+      for (int inst = i0; inst <= i1; ++inst) st_wait(sa.done + sa.dofs[0] + inst, a.rc[0]);
+    for (int q = 0; q < nl; ) {                    // (contiguous runs of one instance)
+      const long long g = lu0 + q;
+      const int inst = (int)(g / lcnt), l = (int)(g % lcnt);
+      const int run = min(nl - q, lcnt - l);
+      tr_final(a, smem, inst * nleaf + sa.lf0 + l, run);
+      q += run;
+    }
     rec(200);
   }
 }
