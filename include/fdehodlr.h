@@ -228,6 +228,44 @@ int fde2d_step_split(int world, int rank, fde_allgather_fn gather, void* ctx,
                      fde_hodlr_t* cache, double* resid_out, int* iters_out,
                      unsigned flags, void* stream);
 
+/* The 2D step with a multi-shift rational Krylov projection: the same
+ * Galerkin framework as fde2d_step with the bases grown by rounds of `npole`
+ * independent shifted solves per side -- W_j = (A1 + p_j I)^{-1} Cu, (A2 + q_j I)^{-1} Cv, each
+ * shifted operator its own HODLR factorisation (shift 1/2 + p_j), kept in cache -- until the
+ * residual is below rk_tol or `rounds` rounds are used.  poles [host, 2 * npole * rounds]: side 0
+ * (A1) then side 1, round-major, all > 0; NULL = automatic (log-spaced in the other operator's
+ * spectral range [1/2, 1/2 + c 2^alpha (max|d+| + max|d-|)], round r offset).  The shifted solves of
+ * a round are independent: with pw > 1, rank pr solves poles j = pr mod pw and the blocks are
+ * all-gathered through `gather` (as fde2d_step_split); the rest runs on every rank.
+ *   cache [2 + 2 * npole * rounds]: the two operators, then the shifted factorisations (required).
+ *   *rounds_out (host, may be NULL): rounds used.  Other arguments, outputs and errors as fde2d_step
+ *   (FDE_ENOCONV when rk_tol is not reached).  npole in 1..16, rounds in 1..6. */
+int fde2d_step_rk(int pw, int pr, fde_allgather_fn gather, void* ctx,
+                  int nx, int ny, double alpha1, double alpha2, double hx, double hy, double dt,
+                  const double* d1p, const double* d1m, const double* d2p, const double* d2m,
+                  const double* Fu, const double* Fv, int rf,
+                  const double* Uu, const double* Uv, int ru,
+                  double* Xu, double* Xv, int rmax, int* rx,
+                  double tol, double rk_tol, int npole, int rounds, const double* poles, int leaf,
+                  fde_hodlr_t* cache, double* resid_out, int* rounds_out, unsigned flags, void* stream);
+
+/* The paper's 1D comparison method: GMRES (full, x0 = 0)
+ * for A_m x = b, left-preconditioned by a tridiagonal structure-preserving preconditioner of [DMS]
+ * -- A_m with T_{alpha,N} replaced by T_{1,N} (precond = 1, P1: Eq. 2.6 at alpha = 1) or by
+ * tridiag(-1, 2, -1) = T_{2,N} (precond = 2, P2); precond = 0: no preconditioner -- with the exact
+ * operator applied by FFT circulant embedding.  Stops when the preconditioned relative
+ * residual ||P^{-1}(b - A x)|| / ||P^{-1} b|| <= tol (*relres, host) or after maxit (1..127)
+ * iterations (*iters, host; FDE_ENOCONV with the best iterate).  d_plus, d_minus, b, x [dev, n];
+ * n <= 2^19.  Synchronous (one read-back per iteration). */
+int fde1d_pgmres(int n, double alpha, double h, double dt, const double* d_plus, const double* d_minus,
+                 const double* b, double* x, int precond, double tol, int maxit, int* iters,
+                 double* relres, unsigned flags, void* stream);
+
+/* y = A_m x with the exact (uncompressed) operator of Eq. (2.5) (shift 1), T x and T^T x by FFT
+ * circulant embedding; for residual checks.  [dev, n] arrays; y must not alias x. */
+int fde1d_apply_exact(int n, double alpha, double h, double dt, const double* d_plus, const double* d_minus,
+                      const double* x, double* y, void* stream);
+
 /* Thread-local description of the last error returned on this thread ("" if none). */
 const char* fde_last_error(void);
 

@@ -405,8 +405,8 @@ static int ek_grow(cudaStream_t s, const Ws2d& w, EkSide& e, double* Wtmp, doubl
 
 // ---- the two operators (built and factorised once, reused while the arguments match)
 static int build_op_2d(int n, double alpha, double h, double dt, const double* dp, const double* dm, double tol,
-                       int leaf, cudaStream_t s, fde_hodlr** out) {
-  TRY(build_impl(1, n, &alpha, h, dt, dp, dm, 0.5, tol, leaf, 0, s, out));
+                       int leaf, cudaStream_t s, fde_hodlr** out, double shift = 0.5) {
+  TRY(build_impl(1, n, &alpha, h, dt, dp, dm, shift, tol, leaf, 0, s, out));
   fde_hodlr* H = *out;
   const int rc = factor_impl(H, H->d_dp, H->d_dm, 0, nullptr, nullptr, nullptr, 1, s);
   if (rc != FDE_OK) { free_handle(H); *out = nullptr; return rc; }
@@ -420,14 +420,14 @@ static int build_op_2d(int n, double alpha, double h, double dt, const double* d
 // rebuild when (n, alpha, h, tol, leaf) differ; re-copy the coefficients, set dt and refactorise
 // when only dt, the coefficient pointers or FDE_COEFFS_CHANGED differ (compression reused).
 static int ensure_op_2d(fde_hodlr** op, int n, double alpha, double h, double dt, const double* dp,
-                        const double* dm, double tol, int leaf, unsigned flags, cudaStream_t s) {
+                        const double* dm, double tol, int leaf, unsigned flags, cudaStream_t s, double shift = 0.5) {
   fde_hodlr* H = *op;
   const bool same = H && H->batch == 1 && H->n == n && H->alpha[0] == alpha && H->h == h && H->tol == tol &&
-                    H->leaf == leaf && H->shift == 0.5 && !H->compress_only;
+                    H->leaf == leaf && H->shift == shift && !H->compress_only;
   if (!same) {
     if (H) hodlr_destroy(H);
     *op = nullptr;
-    return build_op_2d(n, alpha, h, dt, dp, dm, tol, leaf, s, op);
+    return build_op_2d(n, alpha, h, dt, dp, dm, tol, leaf, s, op, shift);
   }
   if (H->factored && H->dt == dt && H->src_dp == dp && H->src_dm == dm && !(flags & FDE_COEFFS_CHANGED))
     return FDE_OK;
@@ -440,6 +440,42 @@ static int ensure_op_2d(fde_hodlr** op, int n, double alpha, double h, double dt
   H->src_dp = dp; H->src_dm = dm;
   H->last_stream = s;
   return FDE_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// Multi-shift rational Krylov mode (the paper's projection framework,
+// P:1519-1550, with rational instead of extended Krylov bases).  The bases grow by rounds of
+// npole independent shifted solves per side, W_j = (A1 + p_j I)^{-1} Cu and (A2 + q_j I)^{-1} Cv,
+// each shifted operator an independent HODLR factorisation (hodlr_build with shift 1/2 + p_j).
+// Poles: the A1 side takes p_j in the spectral range of A2 and the A2 side q_j in that of A1 (the
+// poles of the solution X = int e^{-t A1} C e^{-t A2^T} dt seen from either side), log-spaced in
+// [1/2, 1/2 + c 2^alpha (max d+ + max d-)] (reading R7's norm bound), round r offset by phi_r;
+// or given.  The poles of a round are independent: with pw > 1 ranks, pole j is solved by rank
+// j mod pw and the blocks are all-gathered (one exchange per round and side); everything else
+// runs on every rank on the same data.
+struct RkSpec {
+  int npole;                    // poles per round and side
+  int rounds;                   // maximum number of rounds
+  const double* poles;          // host [2 * npole * rounds] (side 0 then side 1, round-major) or NULL
+  int pw, pr;                   // pole sharding: world, rank
+  fde_allgather_fn gather; void* ctx;
+  fde_hodlr** shifted;          // cache [2 * npole * rounds] of the shifted factorisations
+};
+
+__global__ void k_absmax2(int n, const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ out) {
+  __shared__ double red[2][1024];
+  double ma = 0.0, mb = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) { ma = fmax(ma, fabs(a[i])); mb = fmax(mb, fabs(b[i])); }
+  red[0][threadIdx.x] = ma; red[1][threadIdx.x] = mb;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      red[0][threadIdx.x] = fmax(red[0][threadIdx.x], red[0][threadIdx.x + w]);
+      red[1][threadIdx.x] = fmax(red[1][threadIdx.x], red[1][threadIdx.x + w]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { out[0] = red[0][0]; out[1] = red[1][0]; }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -480,7 +516,7 @@ static int step_2d_impl(Xchg& xc, int nx, int ny, double alpha1, double alpha2, 
                         const double* Fu, const double* Fv, int rf, const double* Uu, const double* Uv,
                         int ru, double* Xu, double* Xv, int rmax, int* rx, double tol, double ek_tol,
                         int ek_maxit, int leaf, fde_hodlr_t* cache, double* resid_out, int* iters_out,
-                        unsigned flags, cudaStream_t s) {
+                        unsigned flags, cudaStream_t s, const RkSpec* rk = nullptr) {
   const bool own0 = xc.own(0), own1 = xc.own(1);
   TRY(check_common(1, nx, &alpha1, hx, dt, tol, leaf));
   TRY(check_common(1, ny, &alpha2, hy, dt, tol, leaf));
@@ -520,11 +556,18 @@ static int step_2d_impl(Xchg& xc, int nx, int ny, double alpha1, double alpha2, 
   const size_t oDv = carve(64), oIv = carve(EK_SMAX), oJobs = carve(64), oAm = carve(sm2), oBm = carve(sm2);
   const size_t oCm = carve(sm2), oYm = carve(sm2), oZm = carve(sm2), oSig = carve(EK_SMAX), oLc = carve(sm2), oRc = carve(sm2);
   const size_t oSg = carve(NRHS_MAX), oXs = carve(2 * SS), oXr = carve((size_t)xc.world * 2 * SS);
+  const int rk_np = rk ? rk->npole : 0, rk_pw = rk ? std::max(1, rk->pw) : 1;
+  const size_t rk_cnt = (size_t)((rk_np + rk_pw - 1) / rk_pw) * nmax * NRHS_MAX;     // blocks per rank
+  const size_t oWs = carve(rk ? rk_cnt : 0), oWr = carve(rk && rk_pw > 1 ? rk_pw * rk_cnt : 0);
   double* base = nullptr;
   if (cudaMallocAsync(reinterpret_cast<void**>(&base), o * sizeof(double), s) != cudaSuccess) {
     cudaGetLastError(); cleanup(); return set_err(FDE_ENOMEM, "fde2d workspace allocation failed (%zu MB)", o * 8 >> 20);
   }
-  auto fail = [&](int code) { cudaFreeAsync(base, s); cudaStreamSynchronize(s); cleanup(); return code; };
+  bool failed = false;                             // (fail() may be reached twice: inner + outer)
+  auto fail = [&](int code) {
+    if (!failed) { failed = true; cudaFreeAsync(base, s); cudaStreamSynchronize(s); cleanup(); }
+    return code;
+  };
 #define CK(call) do { cudaError_t e_ = (call); if (e_ != cudaSuccess) return fail(set_err(FDE_ECUDA, "%s: %s", #call, cudaGetErrorString(e_))); } while (0)
 #define TK(call) do { const int r_ = (call); if (r_ != FDE_OK) return fail(r_); } while (0)
   double *Ux = base + oUx, *AUx = base + oAUx, *Vy = base + oVy, *AVy = base + oAVy, *Wt = base + oWt;
@@ -611,8 +654,74 @@ static int step_2d_impl(Xchg& xc, int nx, int ny, double alpha1, double alpha2, 
   EkSide sx{ops[0], nx, Ux, AUx, 0, 0, 0, 0, 0}, sy{ops[1], ny, Vy, AVy, 0, 0, 0, 0, 0};
   EkSide* sides[2] = {&sx, &sy};
   const double dtol = 1e-11;
+  // ---- rational Krylov mode: poles, and one round of shifted solves + orthogonalisation
+  std::vector<double> poles;
+  int rk_round = 0;
+  if (rk) {
+    const int K = rk->npole, R = rk->rounds;
+    poles.assign((size_t)2 * K * R, 0.0);
+    if (rk->poles) std::copy(rk->poles, rk->poles + 2 * K * R, poles.begin());
+    else {
+      // spectral range of A_d (real parts in [1/2, 1/2 + c_d 2^alpha_d (max|d+| + max|d-|)])
+      double hm[4] = {0, 0, 0, 0};
+      { PROF("k_absmax2"); k_absmax2<<<1, 1024, 0, s>>>(nx, d1p, d1m, w.dv + 20); }
+      { PROF("k_absmax2"); k_absmax2<<<1, 1024, 0, s>>>(ny, d2p, d2m, w.dv + 22); }
+      TK(dn_check("k_absmax2"));
+      CK(cudaMemcpyAsync(hm, w.dv + 20, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      const double hi[2] = {0.5 + dt / std::pow(hx, alpha1) * std::exp2(alpha1) * (hm[0] + hm[1]),
+                            0.5 + dt / std::pow(hy, alpha2) * std::exp2(alpha2) * (hm[2] + hm[3])};
+      const double phi[6] = {0.5, 0.0, 1.0, 0.25, 0.75, 0.125};
+      for (int d = 0; d < 2; ++d)
+        for (int r = 0; r < R; ++r)
+          for (int j = 0; j < K; ++j) {
+            const double e = (j + phi[r % 6]) / K, lo = 0.5, h_ = hi[1 - d];   // the other side's range
+            poles[((size_t)d * R + r) * K + j] = lo * std::pow(h_ / lo, e);
+          }
+    }
+  }
+  auto rk_grow = [&](int r) -> int {
+    const int K = rk->npole, R = rk->rounds, pw = rk_pw, pr = rk->pr;
+    for (int d = 0; d < 2; ++d) {
+      EkSide* e = sides[d];
+      const double* Cs = d == 0 ? Cu : Cv;
+      const long long blk = (long long)e->n * rcr;
+      double* Ws = base + oWs;
+      for (int j = pr; j < K; j += pw) {                // this rank's poles of the round
+        const size_t idx = ((size_t)d * R + r) * K + j;
+        const double pole = poles[idx];
+        TRY(ensure_op_2d(&rk->shifted[idx], e->n, d == 0 ? alpha1 : alpha2, d == 0 ? hx : hy, dt,
+                         d == 0 ? d1p : d2p, d == 0 ? d1m : d2m, tol, leaf, flags, s, 0.5 + pole));
+        TRY(hodlr_solve_cols(rk->shifted[idx], Cs, Ws + (size_t)(j / pw) * blk, rcr, s));
+      }
+      const double* Wall = Ws;
+      const long long cnt = (long long)((K + pw - 1) / pw) * blk;
+      if (pw > 1) {                                     // blocks of every rank (rank-major)
+        double* Wr = base + oWr;
+        if (rk->gather(rk->ctx, Ws, Wr, cnt, s) != 0) return set_err(FDE_ECUDA, "pole exchange callback failed");
+        Wall = Wr;
+      }
+      for (int j = 0; j < K; ++j) {                     // orthogonalise in pole order (every rank)
+        const double* Wj = Wall + (size_t)(j % pw) * cnt + (size_t)(j / pw) * blk;
+        CK(cudaMemcpyAsync(Wt, Wj, (size_t)blk * 8, cudaMemcpyDeviceToDevice, s));
+        int nb = 0;
+        TRY(orth_append(s, w, e->n, Wt, rcr, e->U, e->s, EK_SMAX, dtol, &nb));
+        if (nb) TRY(hodlr_mv_cols(e->H, e->U + (size_t)e->s * e->n, e->AU + (size_t)e->s * e->n, nb, s));
+        e->s += nb;
+      }
+    }
+    return FDE_OK;
+  };
   for (int d = 0; d < 2; ++d) {
     if (!xc.own(d)) continue;
+    if (rk) {                                           // first block C_s; then round 0 of the poles
+      EkSide* e = sides[d];
+      const double* Cs = d == 0 ? Cu : Cv;
+      CK(cudaMemcpyAsync(e->U, Cs, (size_t)e->n * rcr * 8, cudaMemcpyDeviceToDevice, s));
+      TK(hodlr_mv_cols(e->H, e->U, e->AU, rcr, s));
+      e->s = rcr;
+      continue;
+    }
     EkSide* e = sides[d];
     const double* Cs = d == 0 ? Cu : Cv;
     CK(cudaMemcpyAsync(e->U, Cs, (size_t)e->n * rcr * 8, cudaMemcpyDeviceToDevice, s));   // orthonormal
@@ -638,6 +747,7 @@ static int step_2d_impl(Xchg& xc, int nx, int ny, double alpha1, double alpha2, 
     *sa_out = (int)v0; *sb_out = (int)v1;
     return FDE_OK;
   };
+  if (rk) { TK(rk_grow(0)); rk_round = 1; }
   int sa = 0, sbb = 0;
   TK(sizes(&sa, &sbb));
   // ---- S10: projected solves until the residual is below ek_tol (relative to ||C||_F)
@@ -724,8 +834,15 @@ static int step_2d_impl(Xchg& xc, int nx, int ny, double alpha1, double alpha2, 
     }
     if (it == ek_maxit) break;
     const int s0x = sa, s0y = sbb;
-    if (own0) TK(ek_grow(s, w, sx, Wt, dtol));
-    if (own1) TK(ek_grow(s, w, sy, Wt, dtol));
+    if (rk) {
+      if (rk_round >= rk->rounds) break;
+      TK(rk_grow(rk_round));
+      ++rk_round;
+      solve_now = true;
+    } else {
+      if (own0) TK(ek_grow(s, w, sx, Wt, dtol));
+      if (own1) TK(ek_grow(s, w, sy, Wt, dtol));
+    }
     TK(sizes(&sa, &sbb));
     if (sa == s0x && sbb == s0y) break;              // no new directions (EK_SMAX or exhausted)
   }
@@ -733,7 +850,7 @@ static int step_2d_impl(Xchg& xc, int nx, int ny, double alpha1, double alpha2, 
     TK(solve_and_check());
     conv = rel <= 10.0 * ek_tol;
   }
-  if (iters_out) *iters_out = std::min(it, ek_maxit);
+  if (iters_out) *iters_out = rk ? rk_round : std::min(it, ek_maxit);
   // ---- truncation: X = U_s Y V_s^T with Y = sum sigma_i u_i w_i^T, keep sigma > tol sigma_1.
   // Rank-revealing QR of Y first (Q_k^T Y, k ~ final rank), then the one-sided Jacobi SVD of
   // (Q_k^T Y)^T (sbb x k): right singular vectors W and sigma; the left factor is Y W.
@@ -756,31 +873,37 @@ static int step_2d_impl(Xchg& xc, int nx, int ny, double alpha1, double alpha2, 
   std::sort(ord.begin(), ord.end(), [&](int a, int c) { return hs[a] > hs[c] || (hs[a] == hs[c] && a < c); });
   keep.clear();
   for (int i : ord) if (hs[i] > tol * hs[ord[0]] && hs[i] > 0.0) keep.push_back(i);
-  const int rk = (int)keep.size();
-  if (rk > rmax) { fail(FDE_OK); return set_err(FDE_EDIM, "solution rank %d exceeds rmax=%d", rk, rmax); }
+  const int rkt = (int)keep.size();
+  if (rkt > rmax) { fail(FDE_OK); return set_err(FDE_EDIM, "solution rank %d exceeds rmax=%d", rkt, rmax); }
   double rel_t = rel;
-  if (rk > 0) {
-    CK(cudaMemcpyAsync(w.iv, keep.data(), rk * sizeof(int), cudaMemcpyHostToDevice, s));
+  if (rkt > 0) {
+    CK(cudaMemcpyAsync(w.iv, keep.data(), rkt * sizeof(int), cudaMemcpyHostToDevice, s));
     // right vectors M6 = (AT Z)[:, keep] / sigma, left factor M5 = Y M6 (= U_k Sigma_k)
-    { PROF("k_gather_cols"); k_gather_cols<<<(sbb * rk + 255) / 256, 256, 0, s>>>(sbb, rk, w.M3, sbb, w.iv, sig, w.M6, sbb); }
+    { PROF("k_gather_cols"); k_gather_cols<<<(sbb * rkt + 255) / 256, 256, 0, s>>>(sbb, rkt, w.M3, sbb, w.iv, sig, w.M6, sbb); }
     TK(dn_check("k_gather_cols"));
-    TK(ts_nn(s, sa, rk, sbb, 1.0, Ym, sa, w.M6, sbb, 0.0, w.M5, sa));
+    TK(ts_nn(s, sa, rkt, sbb, 1.0, Ym, sa, w.M6, sbb, 0.0, w.M5, sa));
     // the returned X's residual: the splitting at Yt = M5 M6^T (plus the dropped part of C)
     double* Yt = w.M4;
-    TK(transpose(s, sbb, rk, w.M6, sbb, w.S, rk));
-    TK(ts_nn(s, sa, sbb, rk, 1.0, w.M5, sa, w.S, rk, 0.0, Yt, sa));
+    TK(transpose(s, sbb, rkt, w.M6, sbb, w.S, rkt));
+    TK(ts_nn(s, sa, sbb, rkt, 1.0, w.M5, sa, w.S, rkt, 0.0, Yt, sa));
     double r3[3];
     TK(resid_at(Yt, r3));
     rel_t = std::sqrt((r3[0] + r3[1] + r3[2] + cdrop2) / cnorm2);
-    if (own0) TK(ts_nn(s, nx, rk, sa, 1.0, Ux, nx, w.M5, sa, 0.0, Xu, nx));
-    if (own1) TK(ts_nn(s, ny, rk, sbb, 1.0, Vy, ny, w.M6, sbb, 0.0, Xv, ny));
+    if (own0) TK(ts_nn(s, nx, rkt, sa, 1.0, Ux, nx, w.M5, sa, 0.0, Xu, nx));
+    if (own1) TK(ts_nn(s, ny, rkt, sbb, 1.0, Vy, ny, w.M6, sbb, 0.0, Xv, ny));
   }
   if (resid_out) *resid_out = rel_t;
-  *rx = rk;
+  *rx = rkt;
   // device status of the owned operators; exchanged so that both ranks report a failure
   CK(cudaStreamSynchronize(s));
   DevStatus dd[2] = {{0, 0}, {0, 0}};
   for (int d = 0; d < 2; ++d) if (xc.own(d)) TK(read_status(ops[d], &dd[d]));
+  if (rk)
+    for (int d = 0; d < 2; ++d)
+      for (int i = 0; i < rk->npole * rk->rounds && dd[d].code == FDE_OK; ++i) {
+        fde_hodlr* Hs = rk->shifted[(size_t)d * rk->npole * rk->rounds + i];
+        if (Hs) TK(read_status(Hs, &dd[d]));
+      }
   std::vector<double> hst(2);
   for (int d = 0; d < 2; ++d) {
     hst[d] = (double)dd[d].code * 4294967296.0 + (double)(unsigned)dd[d].where;
@@ -832,4 +955,26 @@ extern "C" int fde2d_step_split(int world, int rank, fde_allgather_fn gather, vo
   Xchg xc{world, rank, gather, ctx, nullptr, nullptr};
   return step_2d_impl(xc, nx, ny, alpha1, alpha2, hx, hy, dt, d1p, d1m, d2p, d2m, Fu, Fv, rf, Uu, Uv, ru, Xu, Xv,
                       rmax, rx, tol, ek_tol, ek_maxit, leaf, cache, resid_out, iters_out, flags, (cudaStream_t)stream);
+}
+
+extern "C" int fde2d_step_rk(int pw, int pr, fde_allgather_fn gather, void* ctx, int nx, int ny, double alpha1,
+                             double alpha2, double hx, double hy, double dt, const double* d1p, const double* d1m,
+                             const double* d2p, const double* d2m, const double* Fu, const double* Fv, int rf,
+                             const double* Uu, const double* Uv, int ru, double* Xu, double* Xv, int rmax, int* rx,
+                             double tol, double rk_tol, int npole, int rounds, const double* poles, int leaf,
+                             fde_hodlr_t* cache, double* resid_out, int* rounds_out, unsigned flags, void* stream) {
+  g_last_error.clear();
+  if (npole < 1 || npole > 16 || rounds < 1 || rounds > 6)
+    return set_err(FDE_EDOMAIN, "npole=%d (1..16), rounds=%d (1..6)", npole, rounds);
+  if (pw < 1 || pr < 0 || pr >= pw) return set_err(FDE_EDOMAIN, "pole sharding pw=%d pr=%d", pw, pr);
+  if (pw > 1 && !gather) return set_err(FDE_EDOMAIN, "pw > 1 needs an all-gather callback");
+  if (!cache) return set_err(FDE_EDOMAIN, "cache is required (2 + 2 npole rounds handles)");
+  if (poles)
+    for (int i = 0; i < 2 * npole * rounds; ++i)
+      if (!(poles[i] > 0.0) || !std::isfinite(poles[i])) return set_err(FDE_EDOMAIN, "poles[%d]=%g must be > 0", i, poles[i]);
+  RkSpec rk{npole, rounds, poles, pw, pr, gather, ctx, reinterpret_cast<fde_hodlr**>(cache) + 2};
+  Xchg xc{1, 0, nullptr, nullptr, nullptr, nullptr};
+  return step_2d_impl(xc, nx, ny, alpha1, alpha2, hx, hy, dt, d1p, d1m, d2p, d2m, Fu, Fv, rf, Uu, Uv, ru, Xu, Xv,
+                      rmax, rx, tol, rk_tol, rounds + 1, leaf, cache, resid_out, rounds_out, flags,
+                      (cudaStream_t)stream, &rk);
 }

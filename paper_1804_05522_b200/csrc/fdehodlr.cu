@@ -1461,3 +1461,198 @@ int fde1d_run(int batch, int n, const double* alpha, double h, double dt, int K,
 }  // extern "C"
 
 #include "fde2d.cuh"
+
+// ---------------------------------------------------------------------------------------
+// PGMRES with the tridiagonal preconditioners P1 / P2 (k_pgmres.cuh)
+#include "k_pgmres.cuh"
+
+namespace {
+struct FftPlan { int M1, M2, lg1, lg2; long long M; };
+FftPlan fft_plan(long long Mmin) {
+  int lg = 4;
+  while ((1LL << lg) < Mmin) ++lg;
+  FftPlan p;
+  p.lg1 = (lg + 1) / 2; p.lg2 = lg - p.lg1;
+  p.M1 = 1 << p.lg1; p.M2 = 1 << p.lg2; p.M = 1LL << lg;
+  return p;
+}
+int fft(const FftPlan& p, const double2* x, double2* tmp, double2* X, double sign, double scale, cudaStream_t s) {
+  { PROF("k_fft_cols"); k_fft_cols<<<p.M1 / FFT_G, FFT_T, (size_t)FFT_G * p.M2 * 16, s>>>(x, tmp, p.M1, p.M2, p.lg2, sign); }
+  LAUNCHED();
+  { PROF("k_fft_rows"); k_fft_rows<<<p.M2 / FFT_G, FFT_T, (size_t)FFT_G * p.M1 * 16, s>>>(tmp, X, p.M1, p.lg1, p.M2, sign, scale); }
+  LAUNCHED();
+  return FDE_OK;
+}
+}  // namespace
+
+extern "C" int fde1d_pgmres(int n, double alpha, double h, double dt, const double* d_plus, const double* d_minus,
+                            const double* b, double* x, int precond, double tol, int maxit, int* iters,
+                            double* relres, unsigned flags, void* stream) {
+  g_last_error.clear();
+  TRY(check_common(1, n, &alpha, h, dt, 0.5, 2));
+  if (!d_plus || !d_minus || !b || !x) return set_err(FDE_EDOMAIN, "NULL array argument");
+  if (precond < 0 || precond > 2) return set_err(FDE_EDOMAIN, "precond=%d (0 none, 1 P1, 2 P2)", precond);
+  if (!(tol > 0.0 && tol < 1.0) || maxit < 1 || maxit > 127) return set_err(FDE_EDOMAIN, "tol / maxit (1..127) out of range");
+  if (n > (1 << 19)) return set_err(FDE_EDIM, "n=%d exceeds the FFT plan (2^19)", n);
+  cudaStream_t s = (cudaStream_t)stream;
+  {
+    int dev = 0;
+    CU(cudaGetDevice(&dev));
+    static std::atomic<unsigned long long> mask{0};
+    if (!(mask.load() & (1ULL << (dev & 63)))) {
+      CU(cudaFuncSetAttribute(k_fft_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, FFT_G * 1024 * 16));
+      CU(cudaFuncSetAttribute(k_fft_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, FFT_G * 1024 * 16));
+      mask.fetch_or(1ULL << (dev & 63));
+    }
+  }
+  const FftPlan fp = fft_plan(2LL * n);
+  const long long M = fp.M;
+  const int nb = (n + TD_M - 1) / TD_M, nparts = std::min(148, std::max(1, n / 1024));
+  const int K = maxit;
+  // workspace
+  size_t o = 0;
+  auto carve = [&](size_t d) { const size_t r = o; o += (d + 31) & ~(size_t)31; return r; };
+  const size_t oG = carve(n + 2), oST = carve(2 * M), oSTt = carve(2 * M), oZ = carve(2 * M), oZ1 = carve(2 * M),
+               oZ2 = carve(2 * M), oTmp = carve(2 * M), oV = carve((size_t)n * (K + 1)), oW = carve(n), oR = carve(n),
+               oLo = carve(n), oDi = carve(n), oUp = carve(n), oCp = carve(n), oDd = carve(n), oSv = carve(n),
+               oSw = carve(n), oY = carve(n), oAb = carve(2 * nb), oRw = carve(6 * nb), oH = carve(128 * 129),
+               oGs = carve(3 * 128), oHp = carve(128), oPart = carve(128 * (size_t)nparts), oSc = carve(8), oYv = carve(128),
+               oA = carve(1);
+  double* base = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&base), o * sizeof(double), s) != cudaSuccess) {
+    cudaGetLastError(); return set_err(FDE_ENOMEM, "pgmres workspace allocation failed");
+  }
+  auto D = [&](size_t off) { return base + off; };
+  auto Z = [&](size_t off) { return reinterpret_cast<double2*>(base + off); };
+  int rc = FDE_OK;
+  auto fin = [&](int code) { cudaFreeAsync(base, s); cudaStreamSynchronize(s); return code; };
+#define PG(call) do { const int r_ = (call); if (r_ != FDE_OK) return fin(r_); } while (0)
+#define PK(call) do { call; const cudaError_t e_ = cudaGetLastError(); g_launches++; if (e_ != cudaSuccess) return fin(set_err(FDE_ECUDA, "%s", cudaGetErrorString(e_))); } while (0)
+  const double c = dt / std::pow(h, alpha);
+  const unsigned gb = (unsigned)((M + 255) / 256), gn = (unsigned)((n + 255) / 256);
+  // GL weights (S1) and the spectra of the two circulant embeddings
+  double* d_alpha = D(oA);
+  CU(cudaMemcpyAsync(d_alpha, &alpha, sizeof(double), cudaMemcpyHostToDevice, s));
+  PK((k_gl_weights<<<1, GL_THREADS, 0, s>>>(d_alpha, n + 2, D(oG), n + 2)));
+  PK((k_embed_T<<<gb, 256, 0, s>>>(D(oG), n, M, Z(oZ1), Z(oZ2))));
+  PG(fft(fp, Z(oZ1), Z(oTmp), Z(oST), -1.0, 1.0, s));
+  PG(fft(fp, Z(oZ2), Z(oTmp), Z(oSTt), -1.0, 1.0, s));
+  // preconditioner factors
+  if (precond) {
+    PK((k_prec_coeffs<<<gn, 256, 0, s>>>(n, precond, c, d_plus, d_minus, D(oLo), D(oDi), D(oUp))));
+    PK((k_td_block_setup<<<(nb + 127) / 128, 128, 0, s>>>(n, D(oLo), D(oDi), D(oUp), D(oCp), D(oDd), D(oSv), D(oSw))));
+  }
+  auto apply_A = [&](const double* xin, double* yout) -> int {
+    PK((k_pad_complex<<<gb, 256, 0, s>>>(xin, n, M, Z(oZ))));
+    TRY(fft(fp, Z(oZ), Z(oTmp), Z(oZ), -1.0, 1.0, s));
+    PK((k_spec_mul<<<gb, 256, 0, s>>>(Z(oZ), Z(oST), Z(oSTt), M, Z(oZ1), Z(oZ2))));
+    TRY(fft(fp, Z(oZ1), Z(oTmp), Z(oZ1), 1.0, 1.0 / (double)M, s));
+    TRY(fft(fp, Z(oZ2), Z(oTmp), Z(oZ2), 1.0, 1.0 / (double)M, s));
+    PK((k_apply_combine<<<gn, 256, 0, s>>>(n, xin, Z(oZ1), Z(oZ2), d_plus, d_minus, c, yout)));
+    return FDE_OK;
+  };
+  auto apply_Pinv = [&](const double* r, double* out) -> int {
+    if (!precond) { CU(cudaMemcpyAsync(out, r, (size_t)n * 8, cudaMemcpyDeviceToDevice, s)); return FDE_OK; }
+    PK((k_td_block_solve<<<(nb + 127) / 128, 128, 0, s>>>(n, D(oLo), D(oCp), D(oDd), r, D(oY))));
+    PK((k_td_reduced<<<1, 32, 0, s>>>(n, nb, D(oSv), D(oSw), D(oY), D(oAb), D(oRw))));
+    PK((k_td_reconstruct<<<gn, 256, 0, s>>>(n, nb, D(oY), D(oSv), D(oSw), D(oAb), out)));
+    return FDE_OK;
+  };
+  auto nrm = [&](const double* v, double* out) -> int {     // out = ||v||
+    PK((k_gm_dots<<<nparts, GM_T, 0, s>>>(n, 1, v, v, D(oPart))));
+    PK((k_gm_sum<<<1, 128, 0, s>>>(1, nparts, D(oPart), out)));
+    PK((k_sqrt1<<<1, 1, 0, s>>>(out)));
+    return FDE_OK;
+  };
+  double* V = D(oV);
+  double* H = D(oH);
+  // r0 = P^{-1} b (x0 = 0), beta, v_0
+  PG(apply_Pinv(b, D(oR)));
+  PG(nrm(D(oR), D(oSc)));
+  PK((k_gm_scale<<<gn, 256, 0, s>>>(n, D(oR), D(oSc), V)));
+  PK((k_gm_setg<<<1, 1, 0, s>>>(D(oGs), D(oSc))));
+  CU(cudaMemsetAsync(H, 0, 128 * 129 * sizeof(double), s));
+  double beta = 0.0, res = 1.0;
+  CU(cudaMemcpyAsync(&beta, D(oSc), sizeof(double), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  int k = 0;
+  if (beta > 0.0) {
+    for (k = 0; k < K; ++k) {
+      PG(apply_A(V + (size_t)k * n, D(oR)));
+      PG(apply_Pinv(D(oR), D(oW)));
+      // classical Gram-Schmidt twice: h = V^T w, w -= V h (x2), H[:, k] = h1 + h2
+      double* Hc = H + (size_t)k * 128;
+      for (int pass = 0; pass < 2; ++pass) {
+        PK((k_gm_dots<<<nparts, GM_T, 0, s>>>(n, k + 1, V, D(oW), D(oPart))));
+        PK((k_gm_sum<<<1, 128, 0, s>>>(k + 1, nparts, D(oPart), D(oHp))));
+        PK((k_gm_axpy<<<gn, 256, 0, s>>>(n, k + 1, V, D(oHp), D(oW))));
+        PK((k_add_vec<<<1, 128, 0, s>>>(k + 1, D(oHp), Hc)));
+      }
+      PG(nrm(D(oW), Hc + k + 1));
+      PK((k_gm_scale<<<gn, 256, 0, s>>>(n, D(oW), Hc + k + 1, V + (size_t)(k + 1) * n)));
+      PK((k_gm_givens<<<1, 1, 0, s>>>(k, Hc, D(oGs), D(oSc) + 1)));
+      CU(cudaMemcpyAsync(&res, D(oSc) + 1, sizeof(double), cudaMemcpyDeviceToHost, s));
+      CU(cudaStreamSynchronize(s));
+      if (res <= tol * beta) { ++k; break; }
+    }
+    if (k > K) k = K;
+    PK((k_gm_backsolve<<<1, 1, 0, s>>>(k, H, D(oGs), D(oYv))));
+    CU(cudaMemsetAsync(x, 0, (size_t)n * 8, s));
+    PK((k_gm_axpy_neg<<<gn, 256, 0, s>>>(n, k, V, D(oYv), x)));
+  } else {
+    CU(cudaMemsetAsync(x, 0, (size_t)n * 8, s));
+  }
+  if (iters) *iters = k;
+  if (relres) *relres = beta > 0.0 ? res / beta : 0.0;
+  rc = fin(FDE_OK);
+  if (rc == FDE_OK && beta > 0.0 && res > tol * beta)
+    return set_err(FDE_ENOCONV, "PGMRES: preconditioned relative residual %.3e > tol %.1e after %d iterations",
+                   res / beta, tol, k);
+  (void)flags;
+#undef PG
+#undef PK
+  return rc;
+}
+
+// y = A_m x with the exact operator (Eq. 2.5, shift I): T x and T^T x by circulant embedding + FFT
+// -- the matrix-free operator of the PGMRES comparison and of residual checks.
+extern "C" int fde1d_apply_exact(int n, double alpha, double h, double dt, const double* d_plus,
+                                 const double* d_minus, const double* x, double* y, void* stream) {
+  g_last_error.clear();
+  TRY(check_common(1, n, &alpha, h, dt, 0.5, 2));
+  if (!d_plus || !d_minus || !x || !y) return set_err(FDE_EDOMAIN, "NULL array argument");
+  if (x == y) return set_err(FDE_EDOMAIN, "y must not alias x");
+  if (n > (1 << 19)) return set_err(FDE_EDIM, "n=%d exceeds the FFT plan (2^19)", n);
+  cudaStream_t s = (cudaStream_t)stream;
+  {
+    int dev = 0;
+    CU(cudaGetDevice(&dev));
+    CU(cudaFuncSetAttribute(k_fft_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, FFT_G * 1024 * 16));
+    CU(cudaFuncSetAttribute(k_fft_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, FFT_G * 1024 * 16));
+  }
+  const FftPlan fp = fft_plan(2LL * n);
+  const long long M = fp.M;
+  size_t o = 0;
+  auto carve = [&](size_t d) { const size_t r = o; o += (d + 31) & ~(size_t)31; return r; };
+  const size_t oG = carve(n + 2), oST = carve(2 * M), oSTt = carve(2 * M), oZ = carve(2 * M), oZ1 = carve(2 * M),
+               oZ2 = carve(2 * M), oTmp = carve(2 * M), oA = carve(1);
+  double* base = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&base), o * sizeof(double), s) != cudaSuccess) {
+    cudaGetLastError(); return set_err(FDE_ENOMEM, "workspace allocation failed");
+  }
+  auto Z = [&](size_t off) { return reinterpret_cast<double2*>(base + off); };
+  const unsigned gb = (unsigned)((M + 255) / 256), gn = (unsigned)((n + 255) / 256);
+  CU(cudaMemcpyAsync(base + oA, &alpha, sizeof(double), cudaMemcpyHostToDevice, s));
+  k_gl_weights<<<1, GL_THREADS, 0, s>>>(base + oA, n + 2, base + oG, n + 2); LAUNCHED();
+  k_embed_T<<<gb, 256, 0, s>>>(base + oG, n, M, Z(oZ1), Z(oZ2)); LAUNCHED();
+  TRY(fft(fp, Z(oZ1), Z(oTmp), Z(oST), -1.0, 1.0, s));
+  TRY(fft(fp, Z(oZ2), Z(oTmp), Z(oSTt), -1.0, 1.0, s));
+  k_pad_complex<<<gb, 256, 0, s>>>(x, n, M, Z(oZ)); LAUNCHED();
+  TRY(fft(fp, Z(oZ), Z(oTmp), Z(oZ), -1.0, 1.0, s));
+  k_spec_mul<<<gb, 256, 0, s>>>(Z(oZ), Z(oST), Z(oSTt), M, Z(oZ1), Z(oZ2)); LAUNCHED();
+  TRY(fft(fp, Z(oZ1), Z(oTmp), Z(oZ1), 1.0, 1.0 / (double)M, s));
+  TRY(fft(fp, Z(oZ2), Z(oTmp), Z(oZ2), 1.0, 1.0 / (double)M, s));
+  k_apply_combine<<<gn, 256, 0, s>>>(n, x, Z(oZ1), Z(oZ2), d_plus, d_minus, dt / std::pow(h, alpha), y); LAUNCHED();
+  CU(cudaFreeAsync(base, s));
+  return FDE_OK;
+}

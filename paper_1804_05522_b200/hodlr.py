@@ -216,3 +216,25 @@ class Fde2dStepper:
             self.close()
         except Exception:
             pass
+
+
+def pgmres(n, alpha, h, dt, d_plus, d_minus, b, precond=2, tol=1e-7, maxit=100, x=None, stream=None):
+    """fde1d_pgmres: GMRES for A_m x = b with the tridiagonal preconditioner P1 (precond=1) or P2
+    (precond=2), or none (0), on the FFT-applied exact operator.  Returns (x, iterations, relres)."""
+    if x is None:
+        x = torch.empty_like(b)
+    its, rel = ctypes.c_int(), ctypes.c_double()
+    check(_lib.load().fde1d_pgmres(n, float(alpha), h, dt, _dev(d_plus, "d_plus", n), _dev(d_minus, "d_minus", n),
+                                   _dev(b, "b", n), _dev(x, "x", n), precond, tol, maxit, ctypes.byref(its),
+                                   ctypes.byref(rel), 0, _stream(stream)))
+    return x, its.value, rel.value
+
+
+def apply_exact(n, alpha, h, dt, d_plus, d_minus, x, y=None, stream=None):
+    """fde1d_apply_exact: y = A_m x with the exact operator (FFT circulant embedding)."""
+    if y is None:
+        y = torch.empty_like(x)
+    check(_lib.load().fde1d_apply_exact(n, float(alpha), h, dt, _dev(d_plus, "d_plus", n),
+                                        _dev(d_minus, "d_minus", n), _dev(x, "x", n), _dev(y, "y", n),
+                                        _stream(stream)))
+    return y

@@ -133,3 +133,71 @@ class SplitSylvesterStepper:
             self.close()
         except Exception:
             pass
+
+
+def pole_block(recv, j, pw, cnt, blk):
+    """Block j of an all-gathered pole exchange (mirrors fde2d.cuh rk_grow): rank j mod pw sent
+    its blocks j = pr, pr + pw, ... packed, so block j sits at (j mod pw) * cnt + (j // pw) * blk."""
+    o = (j % pw) * cnt + (j // pw) * blk
+    return recv[o:o + blk]
+
+
+class RkSylvesterStepper:
+    """fde2d_step_rk: the 2D step with a multi-shift rational Krylov projection (NEXT-1); with
+    pw > 1 the shifted solves of a round are sharded over the ranks of `group` (pole j on rank
+    j mod pw, blocks all-gathered).  step() returns (Xu, Xv, resid, rounds) on every rank."""
+
+    def __init__(self, nx, ny, alpha1, alpha2, hx, hy, dt, d1p, d1m, d2p, d2m, tol, rk_tol=1e-11,
+                 npole=8, rounds=3, poles=None, leaf=128, rmax=256, group=None, pw=1, pr=0):
+        import numpy as np
+        from .hodlr import _dev
+        self.nx, self.ny, self.alpha1, self.alpha2, self.hx, self.hy, self.dt = nx, ny, alpha1, alpha2, hx, hy, dt
+        self.coef = [_dev(d1p, "d1p", nx), _dev(d1m, "d1m", nx), _dev(d2p, "d2p", ny), _dev(d2m, "d2m", ny)]
+        self._keep = (d1p, d1m, d2p, d2m)
+        self.tol, self.rk_tol, self.npole, self.rounds, self.leaf, self.rmax = tol, rk_tol, npole, rounds, leaf, rmax
+        self.poles = None if poles is None else np.ascontiguousarray(poles, dtype=np.float64)
+        self.group, self.pw, self.pr = group, pw, pr
+        self._cache = (ctypes.c_void_p * (2 + 2 * npole * rounds))()
+        self.calls = 0
+        self._cb = _lib.ALLGATHER_FN(self._gather)
+
+    def _gather(self, ctx, send, recv, count, stream):
+        try:
+            gather_into(as_tensor(recv, self.pw * count), as_tensor(send, count), self.group if self.pw > 1 else None)
+            self.calls += 1
+            return 0
+        except Exception:
+            return 1
+
+    def step(self, Fu, Fv, Uu=None, Uv=None, flags=0, stream=None):
+        from .hodlr import _dev, _stream
+        nul = ctypes.c_void_p()
+        rf = Fu.shape[0]
+        ru = 0 if Uu is None else Uu.shape[0]
+        Xu = torch.zeros(self.rmax, self.nx, dtype=torch.float64, device=Fu.device)
+        Xv = torch.zeros(self.rmax, self.ny, dtype=torch.float64, device=Fu.device)
+        rx, res, rnd = ctypes.c_int(), ctypes.c_double(), ctypes.c_int()
+        pp = (self.poles.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if self.poles is not None
+              else ctypes.POINTER(ctypes.c_double)())
+        check(_lib.load().fde2d_step_rk(
+            self.pw, self.pr, ctypes.cast(self._cb, ctypes.c_void_p) if self.pw > 1 else None, None,
+            self.nx, self.ny, self.alpha1, self.alpha2, self.hx, self.hy, self.dt, *self.coef,
+            _dev(Fu, "Fu", rf * self.nx), _dev(Fv, "Fv", rf * self.ny), rf,
+            _dev(Uu, "Uu", ru * self.nx) if ru else nul, _dev(Uv, "Uv", ru * self.ny) if ru else nul, ru,
+            _dev(Xu, "Xu"), _dev(Xv, "Xv"), self.rmax, ctypes.byref(rx), self.tol, self.rk_tol, self.npole,
+            self.rounds, pp, self.leaf, ctypes.cast(self._cache, ctypes.POINTER(ctypes.c_void_p)),
+            ctypes.byref(res), ctypes.byref(rnd), flags, _stream(stream)))
+        r = rx.value
+        return Xu[:r].contiguous(), Xv[:r].contiguous(), res.value, rnd.value
+
+    def close(self):
+        for i in range(len(self._cache)):
+            if self._cache[i]:
+                _lib.load().hodlr_destroy(self._cache[i])
+                self._cache[i] = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,87 @@
+"""PGMRES with the tridiagonal preconditioners P1 / P2 (SPEC
+S:486-504) and the FFT-applied exact operator -- fde1d_pgmres, fde1d_apply_exact (GPU).
+
+Pins: the FFT operator equals the oracle's dense A_m (and its own FFT matvec) to rounding;
+alpha = 2 with P2 (the preconditioner IS the matrix) and dt = 0 (A = I) converge in one
+iteration; the paper's Sec. 3.6 problem (alpha = 1.8, d+ = G(3-a) x^a,
+d- = G(3-a)(2-x)^a on [0, 2], GMRES tol 1e-7) reaches a true relative residual <= 1e-6 (SPEC
+S:486) and its solution matches the dense oracle; P1 / P2 take fewer iterations than no
+preconditioner."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle.fd1d import assemble_A, apply_A_fft
+
+gpu = pytest.mark.gpu
+
+
+def _t(a):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device="cuda")
+
+
+def _sec36(n, alpha):
+    """Sec. 3.6: [L, R] = [0, 2], d+ = G(3-a) x^a, d- = G(3-a)(2-x)^a; grid x_i = i h with
+    h = 2/(n+1) (reading R5 on [0, 2]) and dt = h (the paper takes dt = dx)."""
+    h = 2.0 / (n + 1)
+    x = h * np.arange(1, n + 1)
+    g = math.gamma(3.0 - alpha)
+    return h, h, g * x ** alpha, g * (2.0 - x) ** alpha, x
+
+
+@gpu
+@pytest.mark.parametrize("n,alpha", [(300, 1.3), (1000, 1.8), (4097, 1.5)])
+def test_exact_operator_matches_oracle(n, alpha):
+    from paper_1804_05522_b200.hodlr import apply_exact
+    h, dt, dp, dm, _ = _sec36(n, alpha)
+    u = np.random.default_rng(n).standard_normal(n)
+    y = apply_exact(n, alpha, h, dt, _t(dp), _t(dm), _t(u)).cpu().numpy()
+    want = assemble_A(alpha, n, h, dt, dp, dm) @ u
+    assert np.linalg.norm(y - want) <= 1e-12 * np.linalg.norm(want)
+    np.testing.assert_allclose(y, apply_A_fft(alpha, h, dt, dp, dm, u), rtol=0, atol=1e-11 * np.abs(want).max())
+
+
+@gpu
+def test_one_iteration_special_cases():
+    from paper_1804_05522_b200.hodlr import pgmres
+    n = 777
+    h, dt, dp, dm, x = _sec36(n, 2.0)
+    b = _t(np.sin(3 * x))
+    _, its, rel = pgmres(n, 2.0, h, dt, _t(dp), _t(dm), b, precond=2, tol=1e-10)
+    assert its == 1 and rel <= 1e-10
+    _, its, rel = pgmres(n, 1.5, h, 0.0, _t(dp), _t(dm), b, precond=1, tol=1e-10)    # dt = 0: A = I
+    assert its == 1
+
+
+@gpu
+@pytest.mark.parametrize("precond", [1, 2])
+def test_sec36_problem_residual_and_oracle(precond):
+    from paper_1804_05522_b200.hodlr import pgmres
+    n, alpha = 4096, 1.8
+    h, dt, dp, dm, x = _sec36(n, alpha)
+    b = np.sin(np.pi * x / 2) + 0.3 * x * (2 - x)
+    xs, its, rel = pgmres(n, alpha, h, dt, _t(dp), _t(dm), _t(b), precond=precond, tol=1e-7, maxit=120)
+    xs = xs.cpu().numpy()
+    A = assemble_A(alpha, n, h, dt, dp, dm)
+    assert np.linalg.norm(A @ xs - b) <= 1e-6 * np.linalg.norm(b), (its, rel)
+    xo = np.linalg.solve(A, b)
+    assert np.linalg.norm(xs - xo) <= 1e-4 * np.linalg.norm(xo)
+
+
+@gpu
+def test_preconditioners_reduce_iterations():
+    from paper_1804_05522_b200.hodlr import pgmres
+    from paper_1804_05522_b200._lib import FdeError
+    n, alpha = 1024, 1.5
+    h, dt, dp, dm, x = _sec36(n, alpha)
+    b = _t(np.cos(2 * x))
+    its = {}
+    for p in (0, 1, 2):
+        try:
+            _, its[p], _ = pgmres(n, alpha, h, dt, _t(dp), _t(dm), b, precond=p, tol=1e-7, maxit=127)
+        except FdeError as e:                       # (unpreconditioned: may not converge in 127)
+            assert e.code == 4
+            its[p] = 128
+    assert its[1] < its[0] and its[2] < its[0], its
