@@ -261,6 +261,15 @@ int fde1d_pgmres(int n, double alpha, double h, double dt, const double* d_plus,
                  const double* b, double* x, int precond, double tol, int maxit, int* iters,
                  double* relres, unsigned flags, void* stream);
 
+/* The same solver split into a plan (FFT spectra of T and T^T, the preconditioner's block factors,
+ * the Krylov workspace: built once for time-invariant coefficients) and solves. */
+typedef struct fde_pgmres* fde_pgmres_t;
+int fde1d_pgmres_plan(int n, double alpha, double h, double dt, const double* d_plus, const double* d_minus,
+                      int precond, int maxit, void* stream, fde_pgmres_t* out);
+int fde1d_pgmres_solve(fde_pgmres_t plan, const double* b, double* x, double tol, int* iters, double* relres,
+                       void* stream);
+void fde1d_pgmres_destroy(fde_pgmres_t plan);
+
 /* y = A_m x with the exact (uncompressed) operator of Eq. (2.5) (shift 1), T x and T^T x by FFT
  * circulant embedding; for residual checks.  [dev, n] arrays; y must not alias x. */
 int fde1d_apply_exact(int n, double alpha, double h, double dt, const double* d_plus, const double* d_minus,

@@ -36,6 +36,9 @@ SIGNATURES = {
                         _p, _p, _i, _pi, _d, _d, _i, _i, _ph, _pd, _pi, _u, _p]),
     "fde1d_step_split": (_i, [_i, _i, _p, _p, _i, _d, _d, _d, _p, _p, _p, _p, _p, _d, _i, _u, _ph, _p]),
     "fde1d_pgmres": (_i, [_i, _d, _d, _d, _p, _p, _p, _p, _i, _d, _i, _pi, _pd, _u, _p]),
+    "fde1d_pgmres_plan": (_i, [_i, _d, _d, _d, _p, _p, _i, _i, _p, _ph]),
+    "fde1d_pgmres_solve": (_i, [_p, _p, _p, _d, _pi, _pd, _p]),
+    "fde1d_pgmres_destroy": (None, [_p]),
     "fde1d_apply_exact": (_i, [_i, _d, _d, _d, _p, _p, _p, _p, _p]),
     "fde2d_step_rk": (_i, [_i, _i, _p, _p, _i, _i, _d, _d, _d, _d, _d, _p, _p, _p, _p, _p, _p, _i, _p, _p, _i,
                            _p, _p, _i, _pi, _d, _d, _i, _i, _pd, _i, _ph, _pd, _pi, _u, _p]),

@@ -166,6 +166,8 @@ struct fde_hodlr {
   bool factored = false;
   const double *src_dp = nullptr, *src_dm = nullptr;   // fde2d_step: coefficient arrays factorised
   double* d_split = nullptr;        // fde1d_step_split: send staging (n doubles)
+  double* d_solve_split = nullptr;  // kept-factor solve of large nodes: partials + K-solve results
+  size_t solve_split_cap = 0;
   cudaStream_t last_stream = nullptr;
 };
 
@@ -345,7 +347,7 @@ static int run_compression(fde_hodlr* H, cudaStream_t s) {
     { PROF("k_pchol"); CU(cudaLaunchCooperativeKernel((void*)k_pchol, dim3(c1 - c0), dim3(PC_ROWS), args, smem, s)); }
     LAUNCHED();
   }
-  { PROF("k_eig"); k_eig<<<ntask, EIG_THREADS, 4 * KRAW * KRAW * sizeof(double), s>>>(
+  { PROF("k_eig"); k_eig<<<ntask, EIG_THREADS, 2 * KRAW * KRAW * sizeof(double), s>>>(
       H->d_tasks, H->d_task_kr, H->d_gram, H->d_vkeep, H->d_task_rank, H->d_rank, H->L, H->d_status); }
   LAUNCHED();
   { PROF("k_ltransform"); k_ltransform<<<(int)H->chunks.size(), PC_ROWS, 0, s>>>(
@@ -377,7 +379,7 @@ static int set_attrs() {
   const unsigned long long bit = 1ULL << (dev & 63);
   if (g_attr_mask.load() & bit) return FDE_OK;
   CU(cudaFuncSetAttribute(k_pchol, cudaFuncAttributeMaxDynamicSharedMemorySize, KRAW * PC_ROWS * 8));
-  CU(cudaFuncSetAttribute(k_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * KRAW * KRAW * 8));
+  CU(cudaFuncSetAttribute(k_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * KRAW * KRAW * 8));
   CU(cudaFuncSetAttribute(k_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           LEAF_SMEM));
   CU(cudaFuncSetAttribute(k_lvl_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_REDUCE));
@@ -943,8 +945,37 @@ static int solve_impl(fde_hodlr* H, const double* b, const double* f, double* y,
   sl.Y = y; sl.nrhs = nrhs; sl.ld = ld;
   for (int l = L - 1; l >= 0; --l) {
     sl.level = l; sl.k = H->kl[l]; sl.xcol = H->xcol[l]; sl.kofs = H->kofs[l];
-    { PROF("k_solve_level"); k_solve_level<<<dim3(1 << l, B, std::max(1, std::min(nrhs, 32))), SL_THREADS, 0, s>>>(sl); }
-    LAUNCHED();
+    const long long nodes = (long long)B << l;
+    const int node_rows = H->n >> l;
+    // large nodes (>= 4096 rows) are cut into chunks of ~2048 rows, whatever the batch: an
+    // instance's arithmetic must not depend on how many instances share the launch (the sharded
+    // cfg4 slices are bitwise equal to the full batch, tests/test_parity_full.py)
+    if (node_rows < 4096) {
+      { PROF("k_solve_level"); k_solve_level<<<dim3(1 << l, B, std::max(1, std::min(nrhs, 32))), SL_THREADS, 0, s>>>(sl); }
+      LAUNCHED();
+      continue;
+    }
+    // few large nodes: several CTAs per node (k_solve_dots / _small / _update)
+    SlSplitArgs sp{};
+    sp.a = sl;
+    sp.nch = node_rows / 2048;
+    const size_t need = (size_t)nodes * sp.nch * 2 * KCAP + (size_t)nodes * 2 * KCAP;
+    if (need > H->solve_split_cap) {
+      if (H->d_solve_split) { cudaStreamSynchronize(s); cudaFree(H->d_solve_split); H->allocs.erase(std::find(H->allocs.begin(), H->allocs.end(), (void*)H->d_solve_split)); H->d_solve_split = nullptr; }
+      TRY(dalloc(H, &H->d_solve_split, need));
+      H->solve_split_cap = need;
+    }
+    sp.part = H->d_solve_split;
+    sp.sv = H->d_solve_split + (size_t)nodes * sp.nch * 2 * KCAP;
+    for (int c = 0; c < nrhs; ++c) {
+      sp.c = c;
+      { PROF("k_solve_dots"); k_solve_dots<<<dim3((1 << l) * sp.nch, B), SL_THREADS, 0, s>>>(sp); }
+      LAUNCHED();
+      { PROF("k_solve_small"); k_solve_small<<<dim3(1 << l, B), 32, 0, s>>>(sp); }
+      LAUNCHED();
+      { PROF("k_solve_update"); k_solve_update<<<dim3((1 << l) * sp.nch, B), SL_THREADS, 0, s>>>(sp); }
+      LAUNCHED();
+    }
   }
   return FDE_OK;
 }
@@ -1477,140 +1508,185 @@ FftPlan fft_plan(long long Mmin) {
   return p;
 }
 int fft(const FftPlan& p, const double2* x, double2* tmp, double2* X, double sign, double scale, cudaStream_t s) {
-  { PROF("k_fft_cols"); k_fft_cols<<<p.M1 / FFT_G, FFT_T, (size_t)FFT_G * p.M2 * 16, s>>>(x, tmp, p.M1, p.M2, p.lg2, sign); }
+  { PROF("k_fft_cols"); k_fft_cols<<<p.M1 / FFT_G, FFT_T, (size_t)(FFT_G + 1) * p.M2 * 16, s>>>(x, tmp, p.M1, p.M2, p.lg2, sign); }
   LAUNCHED();
-  { PROF("k_fft_rows"); k_fft_rows<<<p.M2 / FFT_G, FFT_T, (size_t)FFT_G * p.M1 * 16, s>>>(tmp, X, p.M1, p.lg1, p.M2, sign, scale); }
+  { PROF("k_fft_rows"); k_fft_rows<<<p.M2 / FFT_G, FFT_T, (size_t)(FFT_G + 1) * p.M1 * 16, s>>>(tmp, X, p.M1, p.lg1, p.M2, sign, scale); }
   LAUNCHED();
   return FDE_OK;
 }
 }  // namespace
 
-extern "C" int fde1d_pgmres(int n, double alpha, double h, double dt, const double* d_plus, const double* d_minus,
-                            const double* b, double* x, int precond, double tol, int maxit, int* iters,
-                            double* relres, unsigned flags, void* stream) {
+// A PGMRES plan: the operator's FFT spectra, the preconditioner's block factors and the GMRES
+// workspace (Krylov basis of maxit + 1 columns), built once per (alpha, n, h, dt, d+-, precond) and
+// reused by every solve (the coefficients are time-invariant in the paper's comparison).
+struct fde_pgmres {
+  int n = 0, precond = 0, K = 0, nb = 0, nparts = 1;
+  double c = 0;
+  FftPlan fp{};
+  double* base = nullptr;
+  size_t oG, oST, oSTt, oZ, oZ1, oZ2, oTmp, oV, oW, oR, oLo, oDi, oUp, oCp, oDd, oSv, oSw, oY, oAb, oRw, oH, oGs, oHp,
+      oPart, oSc, oYv, oA, oDp, oDm;
+};
+
+extern "C" int fde1d_pgmres_plan(int n, double alpha, double h, double dt, const double* d_plus,
+                                 const double* d_minus, int precond, int maxit, void* stream, fde_pgmres_t* out) {
   g_last_error.clear();
   TRY(check_common(1, n, &alpha, h, dt, 0.5, 2));
-  if (!d_plus || !d_minus || !b || !x) return set_err(FDE_EDOMAIN, "NULL array argument");
+  if (!d_plus || !d_minus || !out) return set_err(FDE_EDOMAIN, "NULL argument");
   if (precond < 0 || precond > 2) return set_err(FDE_EDOMAIN, "precond=%d (0 none, 1 P1, 2 P2)", precond);
-  if (!(tol > 0.0 && tol < 1.0) || maxit < 1 || maxit > 127) return set_err(FDE_EDOMAIN, "tol / maxit (1..127) out of range");
+  if (maxit < 1 || maxit > 127) return set_err(FDE_EDOMAIN, "maxit=%d outside 1..127", maxit);
   if (n > (1 << 19)) return set_err(FDE_EDIM, "n=%d exceeds the FFT plan (2^19)", n);
   cudaStream_t s = (cudaStream_t)stream;
   {
     int dev = 0;
     CU(cudaGetDevice(&dev));
-    static std::atomic<unsigned long long> mask{0};
-    if (!(mask.load() & (1ULL << (dev & 63)))) {
-      CU(cudaFuncSetAttribute(k_fft_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, FFT_G * 1024 * 16));
-      CU(cudaFuncSetAttribute(k_fft_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, FFT_G * 1024 * 16));
-      mask.fetch_or(1ULL << (dev & 63));
-    }
+    CU(cudaFuncSetAttribute(k_fft_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, (FFT_G + 1) * 1024 * 16));
+    CU(cudaFuncSetAttribute(k_fft_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (FFT_G + 1) * 1024 * 16));
   }
-  const FftPlan fp = fft_plan(2LL * n);
-  const long long M = fp.M;
-  const int nb = (n + TD_M - 1) / TD_M, nparts = std::min(148, std::max(1, n / 1024));
-  const int K = maxit;
-  // workspace
+  fde_pgmres* P = new fde_pgmres();
+  P->n = n; P->precond = precond; P->K = maxit; P->c = dt / std::pow(h, alpha);
+  P->fp = fft_plan(2LL * n);
+  P->nb = (n + TD_M - 1) / TD_M;
+  P->nparts = std::min(148, std::max(1, n / 1024));
+  const long long M = P->fp.M;
   size_t o = 0;
   auto carve = [&](size_t d) { const size_t r = o; o += (d + 31) & ~(size_t)31; return r; };
-  const size_t oG = carve(n + 2), oST = carve(2 * M), oSTt = carve(2 * M), oZ = carve(2 * M), oZ1 = carve(2 * M),
-               oZ2 = carve(2 * M), oTmp = carve(2 * M), oV = carve((size_t)n * (K + 1)), oW = carve(n), oR = carve(n),
-               oLo = carve(n), oDi = carve(n), oUp = carve(n), oCp = carve(n), oDd = carve(n), oSv = carve(n),
-               oSw = carve(n), oY = carve(n), oAb = carve(2 * nb), oRw = carve(6 * nb), oH = carve(128 * 129),
-               oGs = carve(3 * 128), oHp = carve(128), oPart = carve(128 * (size_t)nparts), oSc = carve(8), oYv = carve(128),
-               oA = carve(1);
-  double* base = nullptr;
-  if (cudaMallocAsync(reinterpret_cast<void**>(&base), o * sizeof(double), s) != cudaSuccess) {
-    cudaGetLastError(); return set_err(FDE_ENOMEM, "pgmres workspace allocation failed");
+  P->oG = carve(n + 2); P->oST = carve(2 * M); P->oSTt = carve(2 * M); P->oZ = carve(2 * M); P->oZ1 = carve(2 * M);
+  P->oZ2 = carve(2 * M); P->oTmp = carve(2 * M); P->oV = carve((size_t)n * (maxit + 1)); P->oW = carve(n);
+  P->oR = carve(n); P->oLo = carve(n); P->oDi = carve(n); P->oUp = carve(n); P->oCp = carve(n); P->oDd = carve(n);
+  P->oSv = carve(n); P->oSw = carve(n); P->oY = carve(n); P->oAb = carve(2 * P->nb); P->oRw = carve(6 * P->nb);
+  P->oH = carve(128 * 129); P->oGs = carve(3 * 128); P->oHp = carve(128); P->oPart = carve(128 * (size_t)P->nparts);
+  P->oSc = carve(8); P->oYv = carve(128); P->oA = carve(1); P->oDp = carve(n); P->oDm = carve(n);
+  if (cudaMalloc(reinterpret_cast<void**>(&P->base), o * sizeof(double)) != cudaSuccess) {
+    cudaGetLastError(); delete P; return set_err(FDE_ENOMEM, "pgmres workspace allocation failed");
   }
+  double* base = P->base;
   auto D = [&](size_t off) { return base + off; };
   auto Z = [&](size_t off) { return reinterpret_cast<double2*>(base + off); };
-  int rc = FDE_OK;
-  auto fin = [&](int code) { cudaFreeAsync(base, s); cudaStreamSynchronize(s); return code; };
-#define PG(call) do { const int r_ = (call); if (r_ != FDE_OK) return fin(r_); } while (0)
-#define PK(call) do { call; const cudaError_t e_ = cudaGetLastError(); g_launches++; if (e_ != cudaSuccess) return fin(set_err(FDE_ECUDA, "%s", cudaGetErrorString(e_))); } while (0)
-  const double c = dt / std::pow(h, alpha);
+  auto bad = [&](int rc) { cudaFree(P->base); delete P; return rc; };
+#define PK(call) do { call; const cudaError_t e_ = cudaGetLastError(); g_launches++; if (e_ != cudaSuccess) return bad(set_err(FDE_ECUDA, "%s", cudaGetErrorString(e_))); } while (0)
   const unsigned gb = (unsigned)((M + 255) / 256), gn = (unsigned)((n + 255) / 256);
-  // GL weights (S1) and the spectra of the two circulant embeddings
-  double* d_alpha = D(oA);
-  CU(cudaMemcpyAsync(d_alpha, &alpha, sizeof(double), cudaMemcpyHostToDevice, s));
-  PK((k_gl_weights<<<1, GL_THREADS, 0, s>>>(d_alpha, n + 2, D(oG), n + 2)));
-  PK((k_embed_T<<<gb, 256, 0, s>>>(D(oG), n, M, Z(oZ1), Z(oZ2))));
-  PG(fft(fp, Z(oZ1), Z(oTmp), Z(oST), -1.0, 1.0, s));
-  PG(fft(fp, Z(oZ2), Z(oTmp), Z(oSTt), -1.0, 1.0, s));
-  // preconditioner factors
+  if (cudaMemcpyAsync(D(P->oDp), d_plus, (size_t)n * 8, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+      cudaMemcpyAsync(D(P->oDm), d_minus, (size_t)n * 8, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+      cudaMemcpyAsync(D(P->oA), &alpha, sizeof(double), cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return bad(set_err(FDE_ECUDA, "pgmres plan copies failed"));
+  // GL weights (S1) and the spectra of the two circulant embeddings (T and T^T)
+  PK((k_gl_weights<<<1, GL_THREADS, 0, s>>>(D(P->oA), n + 2, D(P->oG), n + 2)));
+  PK((k_embed_T<<<gb, 256, 0, s>>>(D(P->oG), n, M, Z(P->oZ1), Z(P->oZ2))));
+  if (fft(P->fp, Z(P->oZ1), Z(P->oTmp), Z(P->oST), -1.0, 1.0, s) != FDE_OK ||
+      fft(P->fp, Z(P->oZ2), Z(P->oTmp), Z(P->oSTt), -1.0, 1.0, s) != FDE_OK)
+    return bad(FDE_ECUDA);
   if (precond) {
-    PK((k_prec_coeffs<<<gn, 256, 0, s>>>(n, precond, c, d_plus, d_minus, D(oLo), D(oDi), D(oUp))));
-    PK((k_td_block_setup<<<(nb + 127) / 128, 128, 0, s>>>(n, D(oLo), D(oDi), D(oUp), D(oCp), D(oDd), D(oSv), D(oSw))));
+    PK((k_prec_coeffs<<<gn, 256, 0, s>>>(n, precond, P->c, D(P->oDp), D(P->oDm), D(P->oLo), D(P->oDi), D(P->oUp))));
+    PK((k_td_block_setup<<<(P->nb + 127) / 128, 128, 0, s>>>(n, D(P->oLo), D(P->oDi), D(P->oUp), D(P->oCp), D(P->oDd),
+                                                             D(P->oSv), D(P->oSw))));
   }
+#undef PK
+  *out = P;
+  return FDE_OK;
+}
+
+extern "C" void fde1d_pgmres_destroy(fde_pgmres_t P) {
+  if (!P) return;
+  cudaDeviceSynchronize();
+  cudaFree(P->base);
+  delete P;
+}
+
+extern "C" int fde1d_pgmres_solve(fde_pgmres_t P, const double* b, double* x, double tol, int* iters,
+                                  double* relres, void* stream) {
+  g_last_error.clear();
+  if (!P || !b || !x) return set_err(FDE_EDOMAIN, "NULL argument");
+  if (!(tol > 0.0 && tol < 1.0)) return set_err(FDE_EDOMAIN, "tol=%g outside (0, 1)", tol);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int n = P->n, nb = P->nb, nparts = P->nparts, K = P->K, precond = P->precond;
+  const long long M = P->fp.M;
+  const FftPlan& fp = P->fp;
+  double* base = P->base;
+  auto D = [&](size_t off) { return base + off; };
+  auto Z = [&](size_t off) { return reinterpret_cast<double2*>(base + off); };
+#define PK(call) do { call; const cudaError_t e_ = cudaGetLastError(); g_launches++; if (e_ != cudaSuccess) return set_err(FDE_ECUDA, "%s", cudaGetErrorString(e_)); } while (0)
+  const unsigned gb = (unsigned)((M + 255) / 256), gn = (unsigned)((n + 255) / 256);
   auto apply_A = [&](const double* xin, double* yout) -> int {
-    PK((k_pad_complex<<<gb, 256, 0, s>>>(xin, n, M, Z(oZ))));
-    TRY(fft(fp, Z(oZ), Z(oTmp), Z(oZ), -1.0, 1.0, s));
-    PK((k_spec_mul<<<gb, 256, 0, s>>>(Z(oZ), Z(oST), Z(oSTt), M, Z(oZ1), Z(oZ2))));
-    TRY(fft(fp, Z(oZ1), Z(oTmp), Z(oZ1), 1.0, 1.0 / (double)M, s));
-    TRY(fft(fp, Z(oZ2), Z(oTmp), Z(oZ2), 1.0, 1.0 / (double)M, s));
-    PK((k_apply_combine<<<gn, 256, 0, s>>>(n, xin, Z(oZ1), Z(oZ2), d_plus, d_minus, c, yout)));
+    PK((k_pad_complex<<<gb, 256, 0, s>>>(xin, n, M, Z(P->oZ))));
+    TRY(fft(fp, Z(P->oZ), Z(P->oTmp), Z(P->oZ), -1.0, 1.0, s));
+    PK((k_spec_mul<<<gb, 256, 0, s>>>(Z(P->oZ), Z(P->oST), Z(P->oSTt), M, Z(P->oZ1), Z(P->oZ2))));
+    TRY(fft(fp, Z(P->oZ1), Z(P->oTmp), Z(P->oZ1), 1.0, 1.0 / (double)M, s));
+    TRY(fft(fp, Z(P->oZ2), Z(P->oTmp), Z(P->oZ2), 1.0, 1.0 / (double)M, s));
+    PK((k_apply_combine<<<gn, 256, 0, s>>>(n, xin, Z(P->oZ1), Z(P->oZ2), D(P->oDp), D(P->oDm), P->c, yout)));
     return FDE_OK;
   };
   auto apply_Pinv = [&](const double* r, double* out) -> int {
     if (!precond) { CU(cudaMemcpyAsync(out, r, (size_t)n * 8, cudaMemcpyDeviceToDevice, s)); return FDE_OK; }
-    PK((k_td_block_solve<<<(nb + 127) / 128, 128, 0, s>>>(n, D(oLo), D(oCp), D(oDd), r, D(oY))));
-    PK((k_td_reduced<<<1, 32, 0, s>>>(n, nb, D(oSv), D(oSw), D(oY), D(oAb), D(oRw))));
-    PK((k_td_reconstruct<<<gn, 256, 0, s>>>(n, nb, D(oY), D(oSv), D(oSw), D(oAb), out)));
+    PK((k_td_block_solve<<<(nb + 127) / 128, 128, 0, s>>>(n, D(P->oLo), D(P->oCp), D(P->oDd), r, D(P->oY))));
+    PK((k_td_reduced<<<1, 32, 0, s>>>(n, nb, D(P->oSv), D(P->oSw), D(P->oY), D(P->oAb), D(P->oRw))));
+    PK((k_td_reconstruct<<<gn, 256, 0, s>>>(n, nb, D(P->oY), D(P->oSv), D(P->oSw), D(P->oAb), out)));
     return FDE_OK;
   };
   auto nrm = [&](const double* v, double* out) -> int {     // out = ||v||
-    PK((k_gm_dots<<<nparts, GM_T, 0, s>>>(n, 1, v, v, D(oPart))));
-    PK((k_gm_sum<<<1, 128, 0, s>>>(1, nparts, D(oPart), out)));
+    PK((k_gm_dots<<<nparts, GM_T, 0, s>>>(n, 1, v, v, D(P->oPart))));
+    PK((k_gm_sum<<<1, 128, 0, s>>>(1, nparts, D(P->oPart), out)));
     PK((k_sqrt1<<<1, 1, 0, s>>>(out)));
     return FDE_OK;
   };
-  double* V = D(oV);
-  double* H = D(oH);
+  double* V = D(P->oV);
+  double* H = D(P->oH);
   // r0 = P^{-1} b (x0 = 0), beta, v_0
-  PG(apply_Pinv(b, D(oR)));
-  PG(nrm(D(oR), D(oSc)));
-  PK((k_gm_scale<<<gn, 256, 0, s>>>(n, D(oR), D(oSc), V)));
-  PK((k_gm_setg<<<1, 1, 0, s>>>(D(oGs), D(oSc))));
+  TRY(apply_Pinv(b, D(P->oR)));
+  TRY(nrm(D(P->oR), D(P->oSc)));
+  PK((k_gm_scale<<<gn, 256, 0, s>>>(n, D(P->oR), D(P->oSc), V)));
+  PK((k_gm_setg<<<1, 1, 0, s>>>(D(P->oGs), D(P->oSc))));
   CU(cudaMemsetAsync(H, 0, 128 * 129 * sizeof(double), s));
   double beta = 0.0, res = 1.0;
-  CU(cudaMemcpyAsync(&beta, D(oSc), sizeof(double), cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(&beta, D(P->oSc), sizeof(double), cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
   int k = 0;
   if (beta > 0.0) {
     for (k = 0; k < K; ++k) {
-      PG(apply_A(V + (size_t)k * n, D(oR)));
-      PG(apply_Pinv(D(oR), D(oW)));
+      TRY(apply_A(V + (size_t)k * n, D(P->oR)));
+      TRY(apply_Pinv(D(P->oR), D(P->oW)));
       // classical Gram-Schmidt twice: h = V^T w, w -= V h (x2), H[:, k] = h1 + h2
       double* Hc = H + (size_t)k * 128;
       for (int pass = 0; pass < 2; ++pass) {
-        PK((k_gm_dots<<<nparts, GM_T, 0, s>>>(n, k + 1, V, D(oW), D(oPart))));
-        PK((k_gm_sum<<<1, 128, 0, s>>>(k + 1, nparts, D(oPart), D(oHp))));
-        PK((k_gm_axpy<<<gn, 256, 0, s>>>(n, k + 1, V, D(oHp), D(oW))));
-        PK((k_add_vec<<<1, 128, 0, s>>>(k + 1, D(oHp), Hc)));
+        PK((k_gm_dots<<<nparts, GM_T, 0, s>>>(n, k + 1, V, D(P->oW), D(P->oPart))));
+        PK((k_gm_sum<<<1, 128, 0, s>>>(k + 1, nparts, D(P->oPart), D(P->oHp))));
+        PK((k_gm_axpy<<<gn, 256, 0, s>>>(n, k + 1, V, D(P->oHp), D(P->oW))));
+        PK((k_add_vec<<<1, 128, 0, s>>>(k + 1, D(P->oHp), Hc)));
       }
-      PG(nrm(D(oW), Hc + k + 1));
-      PK((k_gm_scale<<<gn, 256, 0, s>>>(n, D(oW), Hc + k + 1, V + (size_t)(k + 1) * n)));
-      PK((k_gm_givens<<<1, 1, 0, s>>>(k, Hc, D(oGs), D(oSc) + 1)));
-      CU(cudaMemcpyAsync(&res, D(oSc) + 1, sizeof(double), cudaMemcpyDeviceToHost, s));
+      TRY(nrm(D(P->oW), Hc + k + 1));
+      PK((k_gm_scale<<<gn, 256, 0, s>>>(n, D(P->oW), Hc + k + 1, V + (size_t)(k + 1) * n)));
+      PK((k_gm_givens<<<1, 1, 0, s>>>(k, Hc, D(P->oGs), D(P->oSc) + 1)));
+      CU(cudaMemcpyAsync(&res, D(P->oSc) + 1, sizeof(double), cudaMemcpyDeviceToHost, s));
       CU(cudaStreamSynchronize(s));
       if (res <= tol * beta) { ++k; break; }
     }
     if (k > K) k = K;
-    PK((k_gm_backsolve<<<1, 1, 0, s>>>(k, H, D(oGs), D(oYv))));
+    PK((k_gm_backsolve<<<1, 1, 0, s>>>(k, H, D(P->oGs), D(P->oYv))));
     CU(cudaMemsetAsync(x, 0, (size_t)n * 8, s));
-    PK((k_gm_axpy_neg<<<gn, 256, 0, s>>>(n, k, V, D(oYv), x)));
+    PK((k_gm_axpy_neg<<<gn, 256, 0, s>>>(n, k, V, D(P->oYv), x)));
   } else {
     CU(cudaMemsetAsync(x, 0, (size_t)n * 8, s));
   }
+  CU(cudaStreamSynchronize(s));
+#undef PK
   if (iters) *iters = k;
   if (relres) *relres = beta > 0.0 ? res / beta : 0.0;
-  rc = fin(FDE_OK);
-  if (rc == FDE_OK && beta > 0.0 && res > tol * beta)
+  if (beta > 0.0 && res > tol * beta)
     return set_err(FDE_ENOCONV, "PGMRES: preconditioned relative residual %.3e > tol %.1e after %d iterations",
                    res / beta, tol, k);
+  return FDE_OK;
+}
+
+extern "C" int fde1d_pgmres(int n, double alpha, double h, double dt, const double* d_plus, const double* d_minus,
+                            const double* b, double* x, int precond, double tol, int maxit, int* iters,
+                            double* relres, unsigned flags, void* stream) {
+  fde_pgmres_t P = nullptr;
+  TRY(fde1d_pgmres_plan(n, alpha, h, dt, d_plus, d_minus, precond, maxit, stream, &P));
+  const int rc = fde1d_pgmres_solve(P, b, x, tol, iters, relres, stream);
+  const std::string err = g_last_error;
+  fde1d_pgmres_destroy(P);
+  g_last_error = err;
   (void)flags;
-#undef PG
-#undef PK
   return rc;
 }
 
@@ -1627,8 +1703,8 @@ extern "C" int fde1d_apply_exact(int n, double alpha, double h, double dt, const
   {
     int dev = 0;
     CU(cudaGetDevice(&dev));
-    CU(cudaFuncSetAttribute(k_fft_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, FFT_G * 1024 * 16));
-    CU(cudaFuncSetAttribute(k_fft_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, FFT_G * 1024 * 16));
+    CU(cudaFuncSetAttribute(k_fft_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, (FFT_G + 1) * 1024 * 16));
+    CU(cudaFuncSetAttribute(k_fft_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (FFT_G + 1) * 1024 * 16));
   }
   const FftPlan fp = fft_plan(2LL * n);
   const long long M = fp.M;

@@ -240,29 +240,28 @@ k_pchol(const PcTask* __restrict__ tasks, const PcChunk* __restrict__ chunks,
 }
 
 // ---------------------------------------------------------------------------------------
-// (2) Recompression: cyclic (round-robin) Jacobi on the kr x kr Gram, one CTA per task.
+// (2) Recompression: cyclic (round-robin) Jacobi on the kr x kr Gram, one CTA per task; one warp
+// per rotation pair of a round (kr/2 disjoint pairs), applied as a row phase (A <- J^T A) and a
+// column phase (A <- A J, V <- V J) separated by barriers -- two barriers per round.
 // Writes Vkeep (kr x r, ld KRAW), the final rank r and rank_out[inst*L + level].
-#define EIG_THREADS 256
+#define EIG_THREADS 768                                  // >= KRAW/2 warps
 __global__ void __launch_bounds__(EIG_THREADS)
 k_eig(const PcTask* __restrict__ tasks, const int* __restrict__ task_kr,
       const double* __restrict__ gram, double* __restrict__ vkeep,
       int* __restrict__ task_rank, int* __restrict__ rank_out, int L,
       DevStatus* __restrict__ st) {
-  extern __shared__ double eig_smem[];                 // 4 * KRAW^2 doubles (dynamic)
+  extern __shared__ double eig_smem[];                 // [A | V] (N x N each)
   double* A = eig_smem;
-  double* B = A + KRAW * KRAW;
-  double* V = B + KRAW * KRAW;
-  double* V2 = V + KRAW * KRAW;
-  __shared__ double rc[KRAW], rs[KRAW];
-  __shared__ int partner[KRAW], isq[KRAW];
+  double* V = A + KRAW * KRAW;
   __shared__ double red[32];
   __shared__ int s_done;
   __shared__ int order[KRAW];
   __shared__ double lam[KRAW];
+  __shared__ double rc[KRAW / 2], rs[KRAW / 2];
   const int task = blockIdx.x;
   const PcTask tk = tasks[task];
   const int kr = task_kr[task];
-  const int t = threadIdx.x;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int N = kr + (kr & 1);
   const double* gt = gram + (long long)task * (KRAW * KRAW);
   for (int e = t; e < N * N; e += EIG_THREADS) {
@@ -284,38 +283,42 @@ k_eig(const PcTask* __restrict__ tasks, const int* __restrict__ task_kr,
       __syncthreads();
       if (s_done) break;
       for (int r = 0; r < N - 1; ++r) {
-        if (t < N / 2) {
+        int p = 0, q = 0;
+        if (warp < N / 2) {
           int a, b;
-          if (t == 0) { a = r; b = N - 1; }
-          else { a = (r + t) % (N - 1); b = (r - t + (N - 1)) % (N - 1); }
-          const int p = min(a, b), q = max(a, b);
+          if (warp == 0) { a = r; b = N - 1; }
+          else { a = (r + warp) % (N - 1); b = (r - warp + (N - 1)) % (N - 1); }
+          p = min(a, b); q = max(a, b);
           const double app = A[p + p * N], aqq = A[q + q * N], apq = A[p + q * N];
-          double c = 1.0, s = 0.0;
+          double c = 1.0, sn = 0.0;
           if (apq != 0.0 && fabs(apq) > 1e-300) {
             const double tau = (aqq - app) / (2.0 * apq);
             const double tt = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
             c = 1.0 / sqrt(1.0 + tt * tt);
-            s = tt * c;
+            sn = tt * c;
           }
-          rc[p] = c; rs[p] = s; partner[p] = q; isq[p] = 0;
-          rc[q] = c; rs[q] = s; partner[q] = p; isq[q] = 1;
+          if (lane == 0) { rc[warp] = c; rs[warp] = sn; }
+          __syncwarp();
+          for (int j = lane; j < N; j += 32) {             // rows p, q:  A <- J^T A
+            const double apj = A[p + j * N], aqj = A[q + j * N];
+            A[p + j * N] = c * apj - sn * aqj;
+            A[q + j * N] = sn * apj + c * aqj;
+          }
         }
         __syncthreads();
-        // A' = J^T A J,  J[p][p] = J[q][q] = c, J[p][q] = s, J[q][p] = -s;  V' = V J
-        for (int e = t; e < N * N; e += EIG_THREADS) {
-          const int i = e % N, j = e / N;
-          const int pi = partner[i], pj = partner[j];
-          const double ci = rc[i], cj = rc[j];
-          const double si = isq[i] ? rs[i] : -rs[i];
-          const double sj = isq[j] ? rs[j] : -rs[j];
-          double v = ci * cj * A[i + j * N] + ci * sj * A[i + pj * N]
-                   + si * cj * A[pi + j * N] + si * sj * A[pi + pj * N];
-          if (pi == j) v = 0.0;                          // annihilated pair entry
-          B[e] = v;
-          V2[e] = V[i + j * N] * cj + V[i + pj * N] * sj;
+        if (warp < N / 2) {
+          const double c = rc[warp], sn = rs[warp];
+          for (int i = lane; i < N; i += 32) {             // columns p, q:  A <- A J,  V <- V J
+            const double aip = A[i + p * N], aiq = A[i + q * N];
+            A[i + p * N] = c * aip - sn * aiq;
+            A[i + q * N] = sn * aip + c * aiq;
+            const double vip = V[i + p * N], viq = V[i + q * N];
+            V[i + p * N] = c * vip - sn * viq;
+            V[i + q * N] = sn * vip + c * viq;
+          }
+          __syncwarp();
+          if (lane == 0) { A[p + q * N] = 0.0; A[q + p * N] = 0.0; }   // annihilated pair entry
         }
-        __syncthreads();
-        for (int e = t; e < N * N; e += EIG_THREADS) { A[e] = B[e]; V[e] = V2[e]; }
         __syncthreads();
       }
     }

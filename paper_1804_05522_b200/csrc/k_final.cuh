@@ -197,7 +197,7 @@ __device__ void leaf_rhs_final(const TrArgs& geo, const TrArgs* tp, const LeafAr
   double xr[LEAF_MAX / 32];
 #pragma unroll
   for (int q = 0; q < LEAF_MAX / 32; ++q) xr[q] = lane + 32 * q < s ? bs[lane + 32 * q] : 0.0;
-  constexpr int QG = 6;                               // V columns per warp pass (24 loads in flight)
+  constexpr int QG = 9;                               // V columns per warp pass (36 loads in flight)
   for (int j0 = QG * warp; j0 < NC - 1; j0 += QG * LEAF_WARPS) {
     double vv[QG][LEAF_MAX / 32];
 #pragma unroll

@@ -19,31 +19,38 @@
 #define FFT_T 256
 
 // In-place radix-2 FFT (decimation in time) of `cnt` interleaved sequences of length P held in
-// shared memory as s[q * P + i] (double2), sign = -1 forward / +1 inverse (unscaled).
-__device__ void smem_fft(double2* s, int P, int lgP, int cnt, double sign) {
+// shared memory as s[q * P + i] (double2), sign = -1 forward / +1 inverse (unscaled).  tw: the P/2
+// twiddles exp(sign 2 pi i k / P) in shared memory (built by the caller).
+__device__ void smem_fft(double2* s, const double2* tw, int P, int lgP, int cnt) {
   const int t = threadIdx.x;
-  // bit reversal
-  for (int e = t; e < cnt * P; e += FFT_T) {
+  for (int e = t; e < cnt * P; e += FFT_T) {          // bit reversal
     const int q = e / P, i = e - q * P;
     const int r = __brev(i) >> (32 - lgP);
     if (i < r) { double2* a = s + q * P; const double2 x = a[i]; a[i] = a[r]; a[r] = x; }
   }
   __syncthreads();
-  for (int len = 2; len <= P; len <<= 1) {
+  for (int len = 2, lgl = 1; len <= P; len <<= 1, ++lgl) {
     const int half = len >> 1;
     for (int e = t; e < cnt * (P >> 1); e += FFT_T) {
       const int q = e / (P >> 1), b = e - q * (P >> 1);
-      const int grp = b / half, k = b - grp * half;
+      const int grp = b >> (lgl - 1), k = b & (half - 1);
       const int i0 = grp * len + k, i1 = i0 + half;
-      double sn, cs;
-      sincospi(sign * 2.0 * k / len, &sn, &cs);
+      const double2 w0 = tw[k << (lgP - lgl)];
       double2* a = s + q * P;
       const double2 u = a[i0], v = a[i1];
-      const double2 w = make_double2(cs * v.x - sn * v.y, cs * v.y + sn * v.x);
+      const double2 w = make_double2(w0.x * v.x - w0.y * v.y, w0.x * v.y + w0.y * v.x);
       a[i0] = make_double2(u.x + w.x, u.y + w.y);
       a[i1] = make_double2(u.x - w.x, u.y - w.y);
     }
     __syncthreads();
+  }
+}
+
+__device__ __forceinline__ void build_twiddles(double2* tw, int P, double sign) {
+  for (int k = threadIdx.x; k < P / 2; k += FFT_T) {
+    double sn, cs;
+    sincospi(sign * 2.0 * k / P, &sn, &cs);
+    tw[k] = make_double2(cs, sn);
   }
 }
 
@@ -52,13 +59,15 @@ __device__ void smem_fft(double2* s, int P, int lgP, int cnt, double sign) {
 __global__ void __launch_bounds__(FFT_T)
 k_fft_cols(const double2* __restrict__ x, double2* __restrict__ Y, int M1, int M2, int lgM2, double sign) {
   extern __shared__ double2 fs[];
+  double2* tw = fs + FFT_G * M2;
   const int j10 = blockIdx.x * FFT_G;
+  build_twiddles(tw, M2, sign);
   for (int e = threadIdx.x; e < FFT_G * M2; e += FFT_T) {
     const int g = e % FFT_G, j2 = e / FFT_G;
     fs[g * M2 + j2] = x[(long long)j2 * M1 + j10 + g];
   }
   __syncthreads();
-  smem_fft(fs, M2, lgM2, FFT_G, sign);
+  smem_fft(fs, tw, M2, lgM2, FFT_G);
   const long long M = (long long)M1 * M2;
   for (int e = threadIdx.x; e < FFT_G * M2; e += FFT_T) {
     const int g = e % FFT_G, k2 = e / FFT_G, j1 = j10 + g;
@@ -74,13 +83,15 @@ __global__ void __launch_bounds__(FFT_T)
 k_fft_rows(const double2* __restrict__ Y, double2* __restrict__ X, int M1, int lgM1, int M2, double sign,
            double scale) {
   extern __shared__ double2 fs[];
+  double2* tw = fs + FFT_G * M1;
   const int k20 = blockIdx.x * FFT_G;
+  build_twiddles(tw, M1, sign);
   for (int e = threadIdx.x; e < FFT_G * M1; e += FFT_T) {
     const int g = e / M1, j1 = e - g * M1;
     fs[g * M1 + j1] = Y[(long long)(k20 + g) * M1 + j1];
   }
   __syncthreads();
-  smem_fft(fs, M1, lgM1, FFT_G, sign);
+  smem_fft(fs, tw, M1, lgM1, FFT_G);
   for (int e = threadIdx.x; e < FFT_G * M1; e += FFT_T) {
     const int g = e % FFT_G, k1 = e / FFT_G;
     const double2 v = fs[g * M1 + k1];

@@ -140,3 +140,119 @@ k_solve_level(const SlArgs a) {
     __syncthreads();
   }
 }
+
+// ---- the same level step split over several CTAs per node (levels with fewer nodes than SMs):
+//   k_solve_dots  : CTA (node, chunk) -> partial a, b over its rows of the node   [2k per CTA]
+//   k_solve_small : CTA per node -> fixed-order sum of the chunks, the K solve -> sv [2k]
+//   k_solve_update: CTA (node, chunk) -> y1 -= W1 top, y2 -= W2 y_v on its rows
+// Rows of a node [r0, r0 + n1 + n2) are cut into `nch` equal chunks; a chunk may straddle the
+// child boundary (each row uses its own child's factor).  Right-hand side c = blockIdx.z.
+struct SlSplitArgs {
+  SlArgs a;
+  int nch;
+  double* part;      // [inst][node][chunk][2 KCAP] per rhs slice (c handled sequentially by grid.z)
+  double* sv;        // [inst][node][2 KCAP] per rhs
+  int c;             // current right-hand side
+};
+
+__global__ void __launch_bounds__(SL_THREADS)
+k_solve_dots(const SlSplitArgs sp) {
+  const SlArgs& a = sp.a;
+  const TreeDev& tr = a.tree;
+  const int j = blockIdx.x / sp.nch, ch = blockIdx.x % sp.nch, inst = blockIdx.y, t = threadIdx.x;
+  const int warp = t >> 5, lane = t & 31;
+  const int l = a.level, L = tr.L, k = a.k;
+  const int nd = node_index(l, j);
+  const int r0 = tr.node_r0[nd], n1 = tr.node_n1[nd], n2 = tr.node_n2[nd], nn = n1 + n2;
+  const int m = tr.lev_m[l], r = a.rank[inst * L + l];
+  const double* Ll = a.Lf + (long long)inst * a.lf_stride + tr.lev_lofs[l];
+  const double* y = a.Y + (long long)inst * a.ld * a.nrhs + (long long)sp.c * a.ld;
+  const int cs = (int)((long long)nn * ch / sp.nch), ce = (int)((long long)nn * (ch + 1) / sp.nch);
+  double* P = sp.part + (((long long)inst * (1 << l) + j) * sp.nch + ch) * 2 * KCAP;
+  // warp per (q, side) as k_solve_level, over this chunk's rows of the side's child
+  for (int w = warp; w < 2 * k; w += SL_THREADS / 32) {
+    const int q = w % k, side = w / k;         // side 0: a (child 2 rows), 1: b (child 1 rows)
+    double acc = 0.0;
+    if (side == 0) {
+      const int lo = max(cs, n1), hi = ce;     // node-local rows of child 2 in the chunk
+      if (q == k - 1) { if (lane == 0 && lo <= n1 && n1 < hi) acc = y[r0 + n1]; }
+      else if (q < r) {
+        const double* Lq = Ll + (long long)q * m;
+        for (int i = lo + lane; i < hi; i += 32) acc = fma(Lq[i - n1], y[r0 + i], acc);
+      }
+    } else {
+      const int lo = cs, hi = min(ce, n1);     // rows of child 1 in the chunk
+      if (q == k - 1) { if (lane == 0 && lo <= n1 - 1 && n1 - 1 < hi) acc = y[r0 + n1 - 1]; }
+      else if (q < r) {
+        const double* Lq = Ll + (long long)q * m;
+        for (int i = lo + lane; i < hi; i += 32) acc = fma(Lq[n1 - 1 - i], y[r0 + i], acc);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) P[side * k + q] = acc;
+  }
+}
+
+__global__ void k_solve_small(const SlSplitArgs sp) {
+  const SlArgs& a = sp.a;
+  __shared__ double z[2 * KCAP], sv[2 * KCAP];
+  const int j = blockIdx.x, inst = blockIdx.y, lane = threadIdx.x, k = a.k;
+  const double* P = sp.part + ((long long)inst * (1 << a.level) + j) * sp.nch * 2 * KCAP;
+  for (int q = lane; q < 2 * k; q += 32) {
+    double v = 0.0;
+    for (int c = 0; c < sp.nch; ++c) v += P[(long long)c * 2 * KCAP + q];
+    z[q] = v;
+  }
+  __syncwarp();
+  const double* Kn = a.Kst + (long long)inst * a.kstride_inst + a.kofs + (long long)j * 3 * k * k;
+  const double* Bk = Kn;
+  const double* Ck = Kn + k * k;
+  const double* Si = Kn + 2 * k * k;
+  for (int q = lane; q < k; q += 32) {
+    double acc = z[k + q];
+    for (int p = 0; p < k; ++p) acc = fma(-Ck[q * k + p], z[p], acc);
+    sv[k + q] = acc;
+  }
+  __syncwarp();
+  double yv0 = 0.0, yv1 = 0.0;
+  const int q0 = lane, q1 = lane + 32;
+  if (q0 < k) for (int p = 0; p < k; ++p) yv0 = fma(Si[q0 * k + p], sv[k + p], yv0);
+  if (q1 < k) for (int p = 0; p < k; ++p) yv1 = fma(Si[q1 * k + p], sv[k + p], yv1);
+  __syncwarp();
+  if (q0 < k) sv[k + q0] = yv0;
+  if (q1 < k) sv[k + q1] = yv1;
+  __syncwarp();
+  for (int q = lane; q < k; q += 32) {
+    double acc = z[q];
+    for (int p = 0; p < k; ++p) acc = fma(-Bk[q * k + p], sv[k + p], acc);
+    sv[q] = acc;
+  }
+  __syncwarp();
+  double* S = sp.sv + ((long long)inst * (1 << a.level) + j) * 2 * KCAP;
+  for (int q = lane; q < 2 * k; q += 32) S[q] = sv[q];
+}
+
+__global__ void __launch_bounds__(SL_THREADS)
+k_solve_update(const SlSplitArgs sp) {
+  const SlArgs& a = sp.a;
+  __shared__ double sv[2 * KCAP];
+  const TreeDev& tr = a.tree;
+  const int j = blockIdx.x / sp.nch, ch = blockIdx.x % sp.nch, inst = blockIdx.y, t = threadIdx.x;
+  const int l = a.level, n = tr.n, k = a.k;
+  const int nd = node_index(l, j);
+  const int r0 = tr.node_r0[nd], n1 = tr.node_n1[nd], n2 = tr.node_n2[nd], nn = n1 + n2;
+  const double* S = sp.sv + ((long long)inst * (1 << l) + j) * 2 * KCAP;
+  for (int q = t; q < 2 * k; q += SL_THREADS) sv[q] = S[q];
+  __syncthreads();
+  const double* W = a.X + (long long)inst * a.xstride + (long long)a.xcol * n;
+  double* y = a.Y + (long long)inst * a.ld * a.nrhs + (long long)sp.c * a.ld;
+  const int cs = (int)((long long)nn * ch / sp.nch), ce = (int)((long long)nn * (ch + 1) / sp.nch);
+  for (int i = cs + t; i < ce; i += SL_THREADS) {
+    const int R = r0 + i;
+    const double* s = i < n1 ? sv : sv + k;
+    double acc = 0.0;
+    for (int q = 0; q < k; ++q) acc = fma(W[(long long)q * n + R], s[q], acc);
+    y[R] -= acc;
+  }
+}

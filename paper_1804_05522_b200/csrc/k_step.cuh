@@ -58,16 +58,18 @@ k_step(const StepArgs sa) {
   // leaves of the part (per instance) and the nodes of each processed level
   const int lcnt = sa.lf1 - sa.lf0;
   const long long n_leaf = sa.do_leaf ? (long long)B * lcnt : 0;
-  long long n_lvl[LMAX];
-  int j0[LMAX], jn[LMAX];
+  __shared__ long long n_lvl[LMAX];                // (shared: indexed by the task's level)
+  __shared__ int j0[LMAX], jn[LMAX];
   long long total = 2 * n_leaf;                    // panel tasks, then projection tasks
   for (int m = L - 1; m >= 0; --m) {
     const bool on = m >= sa.mlo && m < sa.mhi;
-    j0[m] = sa.restrict_nodes ? (sa.lf0 >> (L - m)) : 0;
-    jn[m] = !on ? 0 : (sa.restrict_nodes ? (lcnt >> (L - m)) : (1 << m));
-    n_lvl[m] = (long long)B * jn[m] * a.rc[m];
-    total += n_lvl[m];
+    const int j0m = sa.restrict_nodes ? (sa.lf0 >> (L - m)) : 0;
+    const int jnm = !on ? 0 : (sa.restrict_nodes ? (lcnt >> (L - m)) : (1 << m));
+    const long long nl = (long long)B * jnm * a.rc[m];
+    if (threadIdx.x == 0) { j0[m] = j0m; jn[m] = jnm; n_lvl[m] = nl; }
+    total += nl;
   }
+  __syncthreads();
   const long long n_fin_leaves = sa.do_final ? (long long)B * lcnt : 0;
   const long long n_fin = (n_fin_leaves + TR_NL - 1) / TR_NL;
   total += n_fin;

@@ -238,3 +238,35 @@ def apply_exact(n, alpha, h, dt, d_plus, d_minus, x, y=None, stream=None):
                                         _dev(d_minus, "d_minus", n), _dev(x, "x", n), _dev(y, "y", n),
                                         _stream(stream)))
     return y
+
+
+class PgmresPlan:
+    """fde1d_pgmres_plan / _solve: the operator spectra and preconditioner factors built once,
+    then any number of solves (time-invariant coefficients)."""
+
+    def __init__(self, n, alpha, h, dt, d_plus, d_minus, precond=2, maxit=100, stream=None):
+        self.n = n
+        self._p = ctypes.c_void_p()
+        self._keep = (d_plus, d_minus)
+        check(_lib.load().fde1d_pgmres_plan(n, float(alpha), h, dt, _dev(d_plus, "d_plus", n),
+                                            _dev(d_minus, "d_minus", n), precond, maxit, _stream(stream),
+                                            ctypes.byref(self._p)))
+
+    def solve(self, b, x=None, tol=1e-7, stream=None):
+        if x is None:
+            x = torch.empty_like(b)
+        its, rel = ctypes.c_int(), ctypes.c_double()
+        check(_lib.load().fde1d_pgmres_solve(self._p, _dev(b, "b", self.n), _dev(x, "x", self.n), tol,
+                                             ctypes.byref(its), ctypes.byref(rel), _stream(stream)))
+        return x, its.value, rel.value
+
+    def close(self):
+        if self._p:
+            _lib.load().fde1d_pgmres_destroy(self._p)
+            self._p = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
