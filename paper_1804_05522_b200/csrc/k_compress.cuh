@@ -120,11 +120,11 @@ k_pchol(const PcTask* __restrict__ tasks, const PcChunk* __restrict__ chunks,
         DevStatus* __restrict__ st) {
   extern __shared__ double smem[];
   double* Lc = smem;                                  // [KRAW][PC_ROWS]
-  __shared__ double redv[32];
+  __shared__ double redv[32], redm[32];
   __shared__ int redi[32];
   __shared__ double Lp[KRAW];
   __shared__ double s_total, s_pmax;
-  __shared__ int s_p, s_wslot, s_stop;
+  __shared__ int s_p, s_stop;
 
   const PcChunk ch = chunks[blockIdx.x];
   const PcTask tk = tasks[ch.task];
@@ -143,17 +143,46 @@ k_pchol(const PcTask* __restrict__ tasks, const PcChunk* __restrict__ chunks,
   // rounding level of the residual trace.  Stopping well below tau lets the optimal
   // recompression reproduce the truncated-SVD approximant (same rank; tests/ and DESIGN.md).
   for (;;) {
-    // ---- local partials of the residual diagonal
-    double s = block_sum(d, redv);
-    double mv; int mi;
-    block_argmax(valid ? d : -1.0, valid ? i : 0x7fffffff, redv, redi, mv, mi);
-    double* slot = part + ((long long)myslot * 2 + (step & 1)) * PSTRIDE;
-    if (t == 0) { slot[0] = s; slot[1] = mv; slot[2] = (double)mi; }
-    if (valid && i == mi)
-      for (int q = 0; q < k; ++q) slot[4 + q] = Lc[q * PC_ROWS + t];
+    // ---- local partials of the residual diagonal: trace and argmax in ONE block reduction; warp 0
+    //      writes them and the candidate row of L (from shared memory) into this chunk's slot
+    {
+      double sv = valid ? d : 0.0, bv = valid ? d : -1.0;
+      int bi = valid ? i : 0x7fffffff;
+      const int lane = t & 31, w = t >> 5;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        sv += __shfl_down_sync(0xffffffffu, sv, o);
+        const double v2 = __shfl_down_sync(0xffffffffu, bv, o);
+        const int i2 = __shfl_down_sync(0xffffffffu, bi, o);
+        argmax_merge(bv, bi, v2, i2);
+      }
+      if (lane == 0) { redv[w] = sv; redm[w] = bv; redi[w] = bi; }
+      __syncthreads();
+      if (w == 0) {
+        const int nwp = PC_ROWS >> 5;
+        sv = lane < nwp ? redv[lane] : 0.0;
+        bv = lane < nwp ? redm[lane] : -1.0;
+        bi = lane < nwp ? redi[lane] : 0x7fffffff;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          sv += __shfl_down_sync(0xffffffffu, sv, o);
+          const double v2 = __shfl_down_sync(0xffffffffu, bv, o);
+          const int i2 = __shfl_down_sync(0xffffffffu, bi, o);
+          argmax_merge(bv, bi, v2, i2);
+        }
+        sv = __shfl_sync(0xffffffffu, sv, 0);
+        bv = __shfl_sync(0xffffffffu, bv, 0);
+        bi = __shfl_sync(0xffffffffu, bi, 0);
+        double* slot = part + ((long long)myslot * 2 + (step & 1)) * PSTRIDE;
+        if (lane == 0) { slot[0] = sv; slot[1] = bv; slot[2] = (double)bi; }
+        if (bv >= 0.0)
+          for (int q = lane; q < k; q += 32) slot[4 + q] = Lc[q * PC_ROWS + (bi - ch.row0)];
+      }
+    }
     ++step;
     group_barrier(myctr, step * (unsigned)G);
-    // ---- fixed-order reduction over the G chunks of this task
+    // ---- fixed-order reduction over the G chunks of this task; warp 0 then fetches the
+    //      winning chunk's pivot row of L
     if (t < 32) {
       double tot = 0.0, bv = -1.0; int bi = 0x7fffffff, bs = 0;
       for (int c = t; c < G; c += 32) {
@@ -170,24 +199,25 @@ k_pchol(const PcTask* __restrict__ tasks, const PcChunk* __restrict__ chunks,
         int s2 = __shfl_down_sync(0xffffffffu, bs, o);
         if (v2 > bv || (v2 == bv && i2 < bi)) { bv = v2; bi = i2; bs = s2; }
       }
+      tot = __shfl_sync(0xffffffffu, tot, 0);
+      bv = __shfl_sync(0xffffffffu, bv, 0);
+      bi = __shfl_sync(0xffffffffu, bi, 0);
+      bs = __shfl_sync(0xffffffffu, bs, 0);
       if (t == 0) {
         if (k == 0) s_total = fmax(tk.tau * PC_STOP, PC_EPS_TRACE * tot);   // initial trace
-        s_pmax = bv; s_p = bi; s_wslot = bs;
+        s_pmax = bv; s_p = bi;
         int stop = (tot <= s_total) || !(bv > 0.0) || (k == KRAW);
         if (k == KRAW && tot > tk.tau && ch.grank == 0)
           latch_status(st, FDE_ENOCONV, tk.inst * 65536 + tk.level);
         s_stop = stop;
       }
+      const double* o = part + ((long long)(tk.slot0 + bs) * 2 + ((step - 1) & 1)) * PSTRIDE;
+      for (int q = t; q < k; q += 32) Lp[q] = __ldcg(o + 4 + q);
     }
     __syncthreads();
     if (s_stop) break;
     const int p = s_p;
     const double sp = sqrt(s_pmax);
-    if (t < k) {
-      const double* o = part + ((long long)(tk.slot0 + s_wslot) * 2 + ((step - 1) & 1)) * PSTRIDE;
-      Lp[t] = __ldcg(o + 4 + t);
-    }
-    __syncthreads();
     double l = 0.0;
     if (valid) {
       double acc0 = gi[2 + i + p], acc1 = 0.0;       // H[i,p] = g_{2+i+p}
