@@ -339,6 +339,38 @@ def measure_cfg5(dev, world, rank, steps=16):
                       "(max over ranks); the step reads back the small quantities that steer EK"}
 
 
+def measure_cfg3_split(dev, world, rank, steps=16):
+    """ONE cfg3 trajectory split over the ranks at the top of the HODLR tree
+    (fde1d_step_split, split1d.py): strong scaling of a single problem (value = time-steps/s of the
+    one trajectory, max-over-ranks device time).  Only at N >= 2 (a power of two)."""
+    import torch
+    from paper_1804_05522_b200 import workloads as W
+    from paper_1804_05522_b200.split1d import Split1dStepper
+    wl = W.cfg3(K=steps)
+    t = lambda a: torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device=dev)
+    DP = [t(wl.coeffs(m)[0][0]) for m in range(1, steps + 1)]
+    DM = [t(wl.coeffs(m)[1][0]) for m in range(1, steps + 1)]
+    F = t(wl.source(1)[0])
+    u = [t(wl.u0[0]), torch.empty_like(t(wl.u0[0]))]
+    sp = Split1dStepper(wl.n, wl.alpha, wl.h, wl.tol, wl.leaf, world=world, rank=rank)
+    for k in range(2):
+        sp.step(wl.dt, DP[k], DM[k], F, u[k % 2], u[(k + 1) % 2])
+    torch.distributed.barrier()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for k in range(steps):
+        sp.step(wl.dt, DP[k], DM[k], F, u[k % 2], u[(k + 1) % 2])
+    b.record()
+    torch.cuda.synchronize()
+    ms = _max_over_ranks(dev, world, a.elapsed_time(b))
+    sp.close()
+    return {"workload": "cfg3 (n=65536) one trajectory split over %d GPUs at the top of the tree" % world,
+            "metric": "time-steps/s", "value": steps / (ms / 1e3), "ms_per_step": ms / steps,
+            "scaling": "strong (one problem)", "exchange": "all-gather of the level-p projected matrices "
+            "+ u row blocks per step (NCCL via torch.distributed)"}
+
+
 def measure_small(dev, name, reps=3):
     """BASELINE configs[0] / configs[1] (latency-bound sizes): the whole K-step trajectory through
     fde1d_run (refactor every step), CUDA events around the launch after a warm-up run."""
@@ -584,6 +616,11 @@ def run_ours(args, world, rank, local):
             extra["cfg4"] = measure_cfg4(dev, world, rank)
         except Exception as e:                              # reported, not fatal for the headline
             extra["cfg4"] = {"error": str(e)[:200]}
+        if world > 1 and (world & (world - 1)) == 0:
+            try:
+                extra["cfg3_split"] = measure_cfg3_split(dev, world, rank)
+            except Exception as e:
+                extra["cfg3_split"] = {"error": str(e)[:200]}
         try:
             extra["cfg5"] = measure_cfg5(dev, world, rank)
         except Exception as e:
