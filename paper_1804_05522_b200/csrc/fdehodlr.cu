@@ -167,6 +167,8 @@ struct fde_hodlr {
   const double *src_dp = nullptr, *src_dm = nullptr;   // fde2d_step: coefficient arrays factorised
   double* d_split = nullptr;        // fde1d_step_split: send staging (n doubles)
   double* d_solve_split = nullptr;  // kept-factor solve of large nodes: partials + K-solve results
+  double* d_hstage = nullptr;       // fde1d_run with FDE_HOST_PTRS: device staging
+  size_t hstage_cap = 0;
   size_t solve_split_cap = 0;
   cudaStream_t last_stream = nullptr;
 };
@@ -1463,6 +1465,33 @@ int fde1d_run(int batch, int n, const double* alpha, double h, double dt, int K,
   }
   const size_t cnt = (size_t)batch * n;
   int rc = FDE_OK;
+  if (flags & FDE_HOST_PTRS) {
+    // host arrays: stage them on the device (H2D on `stream`), run, copy every step's solution back
+    if ((coef_stride != 0 && coef_stride != (long long)cnt) || (f_stride != 0 && f_stride != (long long)cnt)) {
+      if (!cache) hodlr_destroy(H);
+      return set_err(FDE_EDIM, "FDE_HOST_PTRS: strides must be 0 or batch*n");
+    }
+    const size_t lc = coef_stride ? (size_t)K : 1, lf = f_stride ? (size_t)K : 1;
+    const size_t need = (2 * lc + lf + 1 + (size_t)K) * cnt;
+    if (need > H->hstage_cap) {
+      if (H->d_hstage) { cudaStreamSynchronize(s); cudaFree(H->d_hstage); H->allocs.erase(std::find(H->allocs.begin(), H->allocs.end(), (void*)H->d_hstage)); H->d_hstage = nullptr; }
+      TRY(dalloc(H, &H->d_hstage, need));
+      H->hstage_cap = need;
+    }
+    double *sdp = H->d_hstage, *sdm = sdp + lc * cnt, *sf = sdm + lc * cnt, *su0 = sf + lf * cnt, *sout = su0 + cnt;
+    CU(cudaMemcpyAsync(sdp, d_plus, lc * cnt * 8, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(sdm, d_minus, lc * cnt * 8, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(sf, f, lf * cnt * 8, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(su0, u0, cnt * 8, cudaMemcpyHostToDevice, s));
+    rc = fde1d_run(batch, n, alpha, h, dt, K, sdp, sdm, coef_stride, sf, f_stride, su0, sout, tol, leaf,
+                   flags & ~(FDE_HOST_PTRS | FDE_SYNC), &H, stream);
+    if (rc == FDE_OK) {
+      CU(cudaMemcpyAsync(u_out, sout, (size_t)K * cnt * 8, cudaMemcpyDeviceToHost, s));
+      rc = sync_and_status(H, s);
+    }
+    if (cache) *cache = H; else hodlr_destroy(H);
+    return rc;
+  }
   if (!H->tree_ok || H->L < 1) {                  // no pipelined path: one fused step at a time
     for (int m = 0; m < K && rc == FDE_OK; ++m)
       rc = fde1d_step(batch, n, alpha, h, dt, d_plus + m * coef_stride, d_minus + m * coef_stride,

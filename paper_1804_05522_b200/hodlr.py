@@ -137,11 +137,21 @@ class Fde1dStepper:
         if d_minus.shape[0] != d_plus.shape[0]:
             raise ValueError("d_plus and d_minus must have the same number of time levels")
         fs = cnt if f.shape[0] > 1 else 0
+        host = bool(flags & FDE_HOST_PTRS)
         if u_out is None:
             u_out = torch.empty((K,) + tuple(u0.shape), dtype=torch.float64, device=u0.device)
-        check(_lib.load().fde1d_run(self.batch, self.n, self._ap, self.h, dt, K, _dev(d_plus, "d_plus"),
-                                    _dev(d_minus, "d_minus"), cs, _dev(f, "f"), fs, _dev(u0, "u0", cnt),
-                                    _dev(u_out, "u_out", K * cnt), self.tol, self.leaf, flags,
+            if host:
+                u_out = u_out.pin_memory()
+
+        def ptr(t, name, numel=None):
+            if not host:
+                return _dev(t, name, numel)
+            if t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
+                raise TypeError("%s must be a contiguous CPU float64 tensor (pinned for async copies)" % name)
+            return ctypes.c_void_p(t.data_ptr())
+        check(_lib.load().fde1d_run(self.batch, self.n, self._ap, self.h, dt, K, ptr(d_plus, "d_plus"),
+                                    ptr(d_minus, "d_minus"), cs, ptr(f, "f"), fs, ptr(u0, "u0", cnt),
+                                    ptr(u_out, "u_out", K * cnt), self.tol, self.leaf, flags,
                                     ctypes.byref(self._cache), _stream(stream)))
         return u_out
 

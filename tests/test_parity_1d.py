@@ -425,3 +425,21 @@ def test_cfg4_pipelined_run_full_size():
             assert be["eta"] <= 1e-12, (m, b, be)
         u = out[m]
     st.close()
+
+
+@gpu
+def test_pipelined_run_host_pointers_match_device():
+    """fde1d_run with FDE_HOST_PTRS (host arrays staged by the library, the e2e path bench.py
+    times) equals the device-pointer run bitwise."""
+    from paper_1804_05522_b200.hodlr import FDE_HOST_PTRS
+    wl = W.make_1d(1000, 1.6, 64, 1e-12, K=4)
+    st = _stepper(wl)
+    DP = np.stack([wl.coeffs(m)[0] for m in range(1, 5)])
+    DM = np.stack([wl.coeffs(m)[1] for m in range(1, 5)])
+    F = np.stack([wl.source(m) for m in range(1, 5)])
+    dev = st.run(wl.dt, _t(DP), _t(DM), _t(F), _t(wl.u0)).cpu().numpy()
+    hp = lambda a: torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64).pin_memory()
+    host = st.run(wl.dt, hp(DP), hp(DM), hp(F), hp(wl.u0), flags=FDE_HOST_PTRS)
+    assert not host.is_cuda
+    np.testing.assert_array_equal(host.numpy(), dev)
+    st.close()
