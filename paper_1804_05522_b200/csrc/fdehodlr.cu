@@ -156,6 +156,7 @@ struct fde_hodlr {
   PcTask* d_tasks = nullptr;
   PcChunk* d_chunks = nullptr;
   unsigned* d_ctr = nullptr;
+  double* d_glseg = nullptr;            // S1 segment products (k_gl_seg)
   double *d_part = nullptr, *d_gram_part = nullptr, *d_gram = nullptr, *d_vkeep = nullptr;
   int *d_task_kr = nullptr, *d_task_rank = nullptr;
   DevStatus* d_status = nullptr;
@@ -326,10 +327,24 @@ static int plan_compression(fde_hodlr* H, int capacity) {
   return FDE_OK;
 }
 
+// S1: GL weights g_0..g_{n+1} of every instance (two multi-CTA passes, k_gl.cuh)
+static int launch_gl(fde_hodlr* H, cudaStream_t s) {
+  const int nk = H->n + 2, nseg = (nk - 1 + GLS_SEG - 1) / GLS_SEG;
+  { PROF("k_gl_seg"); k_gl_seg<<<dim3(nseg, H->batch), GLS_THREADS, 0, s>>>(H->d_alpha, nk, H->d_glseg); }
+  LAUNCHED();
+  { PROF("k_gl_expand"); k_gl_expand<<<dim3(nseg, H->batch), GLS_THREADS, 0, s>>>(H->d_alpha, nk, H->d_glseg, H->d_g, H->gstride); }
+  LAUNCHED();
+  return FDE_OK;
+}
+
 static int run_compression(fde_hodlr* H, cudaStream_t s) {
   if (H->L == 0) return FDE_OK;
   const int ntask = (int)H->tasks.size();
+#ifdef FDE_DEBUG
+  if (fde_dbg_env("FDE_COMP_TRACE")) { const int one = 1; CU(cudaMemcpyToSymbol(g_comp_trace, &one, sizeof(int))); }
+#endif
   CU(cudaMemsetAsync(H->d_ctr, 0, sizeof(unsigned) * ntask, s));
+  CU(cudaMemsetAsync(H->d_part, 0, sizeof(double) * std::max<size_t>(1, H->chunks.size()) * 2 * PSTRIDE, s));   // slot tags
   const size_t smem = (size_t)KRAW * PC_ROWS * sizeof(double);
   for (size_t li = 0; li + 1 < H->launch_chunk0.size(); ++li) {
     const int c0 = H->launch_chunk0[li], c1 = H->launch_chunk0[li + 1];
@@ -346,10 +361,10 @@ static int run_compression(fde_hodlr* H, cudaStream_t s) {
     double* gram = H->d_gram;
     DevStatus* st = H->d_status;
     void* args[] = {&tasks, &chunks, &g, &gs, &Lraw, &tkr, &ctr, &part, &gp, &gram, &st};
-    { PROF("k_pchol"); CU(cudaLaunchCooperativeKernel((void*)k_pchol, dim3(c1 - c0), dim3(PC_ROWS), args, smem, s)); }
+    { PROF("k_pchol"); CU(cudaLaunchCooperativeKernel((void*)k_pchol, dim3(c1 - c0), dim3(PC_THREADS), args, smem, s)); }
     LAUNCHED();
   }
-  { PROF("k_eig"); k_eig<<<ntask, EIG_THREADS, 2 * KRAW * KRAW * sizeof(double), s>>>(
+  { PROF("k_eig"); k_eig<<<ntask, EIG_THREADS, EIG_SMEM, s>>>(
       H->d_tasks, H->d_task_kr, H->d_gram, H->d_vkeep, H->d_task_rank, H->d_rank, H->L, H->d_status); }
   LAUNCHED();
   { PROF("k_ltransform"); k_ltransform<<<(int)H->chunks.size(), PC_ROWS, 0, s>>>(
@@ -381,7 +396,7 @@ static int set_attrs() {
   const unsigned long long bit = 1ULL << (dev & 63);
   if (g_attr_mask.load() & bit) return FDE_OK;
   CU(cudaFuncSetAttribute(k_pchol, cudaFuncAttributeMaxDynamicSharedMemorySize, KRAW * PC_ROWS * 8));
-  CU(cudaFuncSetAttribute(k_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * KRAW * KRAW * 8));
+  CU(cudaFuncSetAttribute(k_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, EIG_SMEM));
   CU(cudaFuncSetAttribute(k_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           LEAF_SMEM));
   CU(cudaFuncSetAttribute(k_lvl_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_REDUCE));
@@ -780,7 +795,7 @@ static int build_impl(int batch, int n, const double* alpha, double h, double dt
   // capacity for the cooperative compression
   int dev = 0, nsm = 0, per_sm = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pchol, PC_ROWS, KRAW * PC_ROWS * 8) != cudaSuccess)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pchol, PC_THREADS, KRAW * PC_ROWS * 8) != cudaSuccess)
     return fail(set_err(FDE_ECUDA, "device query failed: %s", cudaGetErrorString(cudaGetLastError())));
   if ((rc = plan_compression(H, std::max(1, nsm * per_sm))) != FDE_OK) return fail(rc);
   const int L = H->L;
@@ -800,6 +815,7 @@ static int build_impl(int batch, int n, const double* alpha, double h, double dt
       (rc = dalloc(H, &H->d_tasks, std::max<size_t>(1, ntask))) ||
       (rc = dalloc(H, &H->d_chunks, std::max<size_t>(1, nch))) ||
       (rc = dalloc(H, &H->d_ctr, std::max<size_t>(1, ntask))) ||
+      (rc = dalloc(H, &H->d_glseg, B * (size_t)((n + 1 + GLS_SEG - 1) / GLS_SEG))) ||
       (rc = dalloc(H, &H->d_part, std::max<size_t>(1, nch) * 2 * PSTRIDE)) ||
       (rc = dalloc(H, &H->d_gram_part, std::max<size_t>(1, nch) * KRAW * KRAW)) ||
       (rc = dalloc(H, &H->d_gram, std::max<size_t>(1, ntask) * KRAW * KRAW)) ||
@@ -825,9 +841,7 @@ static int build_impl(int batch, int n, const double* alpha, double h, double dt
   if ((flags & FDE_CHECK) && dp && dm && (rc = check_nonneg(H, H->d_dp, H->d_dm, s)) != FDE_OK) return fail(rc);
   if ((rc = set_dt(H, dt, s)) != FDE_OK) return fail(rc);
   // S1: GL weights
-  { PROF("k_gl_weights"); k_gl_weights<<<batch, GL_THREADS, 0, s>>>(H->d_alpha, n + 2, H->d_g, H->gstride); }
-  if (cudaGetLastError() != cudaSuccess) return fail(set_err(FDE_ECUDA, "k_gl_weights launch failed"));
-  g_launches++;
+  if ((rc = launch_gl(H, s)) != FDE_OK) return fail(rc);
   // S2: compression
   if ((rc = run_compression(H, s)) != FDE_OK) return fail(rc);
   if (flags & FDE_COMPRESS_ONLY) {                  // S1-S2 only (rank studies): no factor layout
@@ -1148,6 +1162,9 @@ static int run_chunk(fde_hodlr* H, int K, double dt, const double* d_plus, const
       const double c = (double)K * B * H->nleaf * 1965.0;
       fprintf(stderr, "k_run A phases (us avg per leaf): build+gj0 %.2f lu+store %.2f panel %.2f\n",
               pf[16] / c, pf[17] / c, pf[20] / c);
+      const double cb = (double)std::max(1ULL, pf[27]) * 1965.0;
+      fprintf(stderr, "k_run B phases (us avg over %llu): V+X staging %.2f dmma %.2f\n",
+              pf[27], pf[25] / cb, pf[26] / cb);
     }
     for (int g = 0; g < 2; ++g) {
       const double c = (double)std::max(1ULL, pf[8 * g + 7]);
@@ -1337,8 +1354,7 @@ int fde1d_step(int batch, int n, const double* alpha, double h, double dt, const
   }
   if ((flags & FDE_CHECK)) TRY(check_nonneg(H, dp, dm, s));
   if ((flags & FDE_RECOMPRESS) && !fresh) {               // S1 + S2 again, same workspaces
-    { PROF("k_gl_weights"); k_gl_weights<<<batch, GL_THREADS, 0, s>>>(H->d_alpha, n + 2, H->d_g, H->gstride); }
-    LAUNCHED();
+    TRY(launch_gl(H, s));
     TRY(run_compression(H, s));
   }
   int rc;

@@ -500,8 +500,13 @@ __device__ __noinline__ void leaf_coop_stripe(const double* __restrict__ A, int 
 // after all stripes: the LU + stripe buffers are reused for V (NV x 128 col-major) and
 // chunks of X re-read from L2.  DMMA tiles: warp unit = (m-tile, 2 n-tiles), A reused.
 __device__ void leaf_project(const LeafArgs& a, double* big, const PanelCol* pcd, int c_begin,
-                             int NC, int s, int sp, const double* Xi, double* Qo, int c_lo = 0) {
+                             int NC, int s, int sp, const double* Xi, double* Qo, int c_lo = 0,
+                             unsigned long long* prof = nullptr) {
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31, gid = lane >> 2, tig = lane & 3;
+  long long ph_t = clock64();
+  auto ph = [&](int i) {                              // (debug: B phase cycle sums, prof[i])
+    if (prof && t == 0) { const long long t_ = clock64(); atomicAdd(prof + i, (unsigned long long)(t_ - ph_t)); ph_t = t_; }
+  };
   const int n = a.tree.n, NV = NC - 1, NVP = round_up(NV, 8), MT = NVP >> 3;
   double* Vs = big;                                   // [NVP cols][LDA_LEAF]
   double* Xs = big + NVP * LDA_LEAF;
@@ -533,6 +538,7 @@ __device__ void leaf_project(const LeafArgs& a, double* big, const PanelCol* pcd
     cp_async_commit();
     cp_async_wait_all();
     __syncthreads();
+    ph(1);
     // warp unit = (m-tile pair) x (n-tile pair): 2 A + 2 B fragments feed 4 DMMAs per k-step
     for (int u = warp; u < MP * npc; u += LEAF_WARPS) {
       const int mp = u % MP, n0 = (u / MP) * 16;
@@ -565,8 +571,10 @@ __device__ void leaf_project(const LeafArgs& a, double* big, const PanelCol* pcd
       }
     }
     __syncthreads();
+    ph(2);
     c0 += ncp;
   }
+  if (prof && t == 0) atomicAdd(prof + 3, 1ULL);
 }
 
 // COOP: solve a last round of 1-2 stripes with 4-warp groups (k_run; the extra call raises the
@@ -853,5 +861,6 @@ __device__ __forceinline__ void leaf_proj_task(const LeafArgs& a, double* smem, 
     pcd[cc] = panel_col(a, inst, leaf, r0, c_begin + cc, c_end);
   const double* Xi = a.X + (long long)inst * a.xstride + r0;
   leaf_project(a, smem + LEAF_FRONT, pcd, c_begin, c_end, s, sp, Xi,
-               a.Q + (long long)inst * a.qinst + (long long)leaf * a.qstride, c_begin);
+               a.Q + (long long)inst * a.qinst + (long long)leaf * a.qstride, c_begin,
+               a.prof ? a.prof + 8 : nullptr);
 }
