@@ -574,9 +574,9 @@ static int tree_layout(fde_hodlr* H) {
   o = round_up((int)o, 2);
   g.off_S = (int)o; o += (long long)K4 * g.lds;
   g.off_T = (int)o;                                   // union { T + Z (S phase), U (Q update) }
-  g.off_Z = (int)(o + (long long)kp * g.lds);
+  g.off_Z = round_up((int)(o + (long long)kp * g.lds), 2);   // (16-byte aligned: contiguous staging)
   g.off_U = (int)o;
-  o += std::max((long long)kp * g.lds + 2LL * H->kmax * NC, 2LL * TR_STG * (TR_SUB * NC + 2));
+  o += std::max((long long)(g.off_Z - o) + 2LL * H->kmax * NC + 6, 2LL * TR_STG * (TR_SUB * NC + 2));
   // final pass: 4 v vectors + max(4 warps x 2 S buffers, X block + partials)
   const long long fin = 4LL * round_up(NC, 8) + std::max(8LL * H->kmax * NC, (long long)NC * 128 + 256);
   const size_t bytes = (size_t)std::max(o, fin) * sizeof(double);
@@ -1168,9 +1168,9 @@ static int run_chunk(fde_hodlr* H, int K, double dt, const double* d_plus, const
     }
     for (int g = 0; g < 2; ++g) {
       const double c = (double)std::max(1ULL, pf[8 * g + 7]);
-      fprintf(stderr, "k_run %s phases (us avg over %llu): issue %.2f S %.2f v %.2f Xv %.2f LUwait %.2f solve %.2f\n",
+      fprintf(stderr, "k_run %s phases (us avg over %llu): issue %.2f S %.2f v %.2f Xv %.2f LUwait %.2f solve %.2f x0+Q0 %.2f\n",
               g ? "final-only" : "B'", pf[8 * g + 7], pf[8 * g + 6] / c / 1965.0, pf[8 * g + 1] / c / 1965.0, pf[8 * g + 2] / c / 1965.0,
-              pf[8 * g + 3] / c / 1965.0, pf[8 * g + 4] / c / 1965.0, pf[8 * g + 5] / c / 1965.0);
+              pf[8 * g + 3] / c / 1965.0, pf[8 * g + 4] / c / 1965.0, pf[8 * g + 5] / c / 1965.0, pf[8 * g] / c / 1965.0);
     }
     FILE* fo = fopen(fde_dbg_env("FDE_TRACE_RUN"), "w");
     if (fo) {

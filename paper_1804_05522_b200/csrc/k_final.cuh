@@ -52,20 +52,24 @@ __device__ void leaf_rhs_final(const TrArgs& geo, const TrArgs* tp, const LeafAr
     int m0 = 0;
     bool lu_issued = la == nullptr;
     while (m0 < L) {
+      // a batch of levels whose S_side blocks (k x xm row-major, one contiguous run each in HBM)
+      // fit behind the LU; staged with 16-byte copies
       int m1 = m0, used = 0;
       while (m1 < L) {
-        const int sz = ((a.xc[m1 + 1] - a.xc[m1]) | 1) * a.xc[m1];   // (odd row pitch kp)
+        const int sz = round_up((a.xc[m1 + 1] - a.xc[m1]) * a.xc[m1] + 2, 2);
         if (m1 > m0 && used + sz > scap) break;
         used += sz; ++m1;
       }
+      auto S_src = [&](int m) {
+        const int xm = a.xc[m], k = a.xc[m + 1] - xm;
+        const int jn = leaf >> (L - m), side = (leaf >> (L - m - 1)) & 1;
+        return Sg + a.slev[m] + (long long)jn * 2 * k * xm + (long long)side * k * xm;
+      };
       int o = 0;
       for (int m = m0; m < m1; ++m) {
         const int xm = a.xc[m], k = a.xc[m + 1] - xm;
-        const int jn = leaf >> (L - m), side = (leaf >> (L - m - 1)) & 1;
-        const double* gp = Sg + a.slev[m] + (long long)jn * 2 * k * xm + (long long)side * k * xm;
-        for (int q = warp; q < k; q += LEAF_WARPS)
-          for (int c = lane; c < xm; c += 32) cp_async8(Ss + o + c * (k | 1) + q, gp + q * xm + c);
-        o += (k | 1) * xm;
+        cp_contig(Ss + o, S_src(m), k * xm, t, LEAF_THREADS);
+        o += round_up(k * xm + 2, 2);
       }
       cp_async_commit();
       if (!lu_issued) { issue_lu(); lu_issued = true; RN_PH(6); cp_async_wait_group1(); } else { RN_PH(6); cp_async_wait_all(); }
@@ -76,20 +80,20 @@ __device__ void leaf_rhs_final(const TrArgs& geo, const TrArgs* tp, const LeafAr
         double* vp = part;                            // [8 warps][32 rows] partial sums
         for (int m = m0; m < m1; ++m) {
           const int xm = a.xc[m], k = a.xc[m + 1] - xm;
-          const int kp = k | 1;                      // odd pitch: conflict-free stores and loads
-          const double* St = Ss + o2;                 // [xm][kp]
+          const double* St = cp_contig_dst(Ss + o2, S_src(m));   // [k][xm]
           const int cw = (xm + LEAF_WARPS - 1) / LEAF_WARPS, c0 = warp * cw, c1 = min(xm, c0 + cw);
           for (int q0 = 0; q0 < k; q0 += 32) {
             const int q = q0 + lane;
             double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
             if (q < k) {
+              const double* sr = St + q * xm;
               int c = c0;
 #pragma unroll 2
               for (; c + 3 < c1; c += 4) {
-                a0 = fma(St[c * kp + q], vs[c], a0); a1 = fma(St[(c + 1) * kp + q], vs[c + 1], a1);
-                a2 = fma(St[(c + 2) * kp + q], vs[c + 2], a2); a3 = fma(St[(c + 3) * kp + q], vs[c + 3], a3);
+                a0 = fma(sr[c], vs[c], a0); a1 = fma(sr[c + 1], vs[c + 1], a1);
+                a2 = fma(sr[c + 2], vs[c + 2], a2); a3 = fma(sr[c + 3], vs[c + 3], a3);
               }
-              for (; c < c1; ++c) a0 = fma(St[c * kp + q], vs[c], a0);
+              for (; c < c1; ++c) a0 = fma(sr[c], vs[c], a0);
             }
             vp[warp * 32 + lane] = (a0 + a1) + (a2 + a3);
             __syncthreads();
@@ -101,7 +105,7 @@ __device__ void leaf_rhs_final(const TrArgs& geo, const TrArgs* tp, const LeafAr
             }
             __syncthreads();
           }
-          o2 += (k | 1) * xm;
+          o2 += round_up(k * xm + 2, 2);
         }
       }
       __syncthreads();
@@ -220,5 +224,6 @@ __device__ void leaf_rhs_final(const TrArgs& geo, const TrArgs* tp, const LeafAr
       if (lane == 0 && j0 + jj < NC - 1) Qo[(long long)(j0 + jj) * NC] = v;
     }
   }
+  if (prof) { __syncthreads(); RN_PH(0); }
 }
 

@@ -511,6 +511,8 @@ __device__ void leaf_project(const LeafArgs& a, double* big, const PanelCol* pcd
   double* Vs = big;                                   // [NVP cols][LDA_LEAF]
   double* Xs = big + NVP * LDA_LEAF;
   const int XCH = min(((LEAF_BIG - NVP * LDA_LEAF) / LDA_LEAF) & ~15, round_up(NC - c_lo, 16));
+  // row pairs of X are 16-byte aligned when the leaf start, n and the instance stride are even
+  const bool xvec = (reinterpret_cast<unsigned long long>(Xi) & 15) == 0 && (n & 1) == 0;
   __syncthreads();                                    // every warp is done with the LU
   for (int j = warp; j < NVP; j += LEAF_WARPS) {
     const PanelCol pc = j < NV ? pcd[j + 1 - c_begin] : PanelCol{a.Lf, 0, 0, 0, 0, 0};
@@ -529,12 +531,26 @@ __device__ void leaf_project(const LeafArgs& a, double* big, const PanelCol* pcd
   for (int ch = 0; ch < nchunk; ++ch) {
     const int npc = (NPT * (ch + 1)) / nchunk - (NPT * ch) / nchunk;   // n-pairs in this chunk
     const int ncp = 16 * npc;
-    for (int cc = warp; cc < ncp; cc += LEAF_WARPS)
-      for (int q = 0; q < LEAF_MAX / 32; ++q) {
-        const int i = lane + 32 * q;
-        if (c0 + cc < NC && i < s) cp_async8(&Xs[i + cc * LDA_LEAF], Xi + (long long)(c0 + cc) * n + i);
-        else Xs[i + cc * LDA_LEAF] = 0.0;
-      }
+    if (xvec) {                                        // 16-byte copies of row pairs
+      for (int cc = warp; cc < ncp; cc += LEAF_WARPS)
+#pragma unroll
+        for (int q = 0; q < LEAF_MAX / 64; ++q) {
+          const int i = 2 * lane + 64 * q;
+          double* d = &Xs[i + cc * LDA_LEAF];
+          if (c0 + cc < NC && i + 1 < s) cp_async16(d, Xi + (long long)(c0 + cc) * n + i);
+          else {
+            d[0] = (c0 + cc < NC && i < s) ? __ldcg(Xi + (long long)(c0 + cc) * n + i) : 0.0;
+            d[1] = 0.0;
+          }
+        }
+    } else {
+      for (int cc = warp; cc < ncp; cc += LEAF_WARPS)
+        for (int q = 0; q < LEAF_MAX / 32; ++q) {
+          const int i = lane + 32 * q;
+          if (c0 + cc < NC && i < s) cp_async8(&Xs[i + cc * LDA_LEAF], Xi + (long long)(c0 + cc) * n + i);
+          else Xs[i + cc * LDA_LEAF] = 0.0;
+        }
+    }
     cp_async_commit();
     cp_async_wait_all();
     __syncthreads();

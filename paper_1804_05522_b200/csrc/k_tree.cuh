@@ -197,8 +197,12 @@ __device__ void tr_unit(const TrArgs& a, double* sm, int inst, int m, int j, int
   double* M2 = sm + a.off_M2;
   double* Ss = sm + a.off_S;      // rows 0..k-1: S_top; rows k..2k-1: T, then S_bot (ld lds)
   double* Ts = sm + a.off_T;      // k x xm scratch (S_bot before it moves into Ss)
-  double* Z1 = sm + a.off_Z;      // level-m rows of Q_c1 / Q_c2 (k x ncol1 each)
-  double* Z2 = Z1 + k * ncol1;
+  // level-m rows of Q_c1 / Q_c2 (k x ncol1 each; contiguous runs staged by 16-byte copies, each
+  // placed at its base + the source parity)
+  const long long qs1_ = (long long)(ncol1 - 1) * ncol1;
+  const double* Q1s = a.Q + (long long)inst * a.qinst + a.qlev[m + 1] + (long long)(2 * j) * qs1_ + (long long)(xm - 1) * ncol1;
+  double* Z1 = cp_contig_dst(sm + a.off_Z, Q1s);
+  double* Z2 = cp_contig_dst(sm + a.off_Z + round_up(k * ncol1 + 2, 2), Q1s + qs1_);
   double* Ub = sm + a.off_U;      // TR_STG buffers x [Q_c1 rows | Q_c2 rows] (TR_SUB x ncol1 each);
                                   // aliases Ts and Z: streamed only after the S phase
   const long long qs1 = (long long)(ncol1 - 1) * ncol1;
@@ -228,10 +232,8 @@ __device__ void tr_unit(const TrArgs& a, double* sm, int inst, int m, int j, int
 #define TPH(i) do { if (tdbg) { const long long t_ = clock64(); atomicAdd(a.trace + tsl + (i), (unsigned long long)(t_ - tcl)); tcl = t_; } } while (0)
   if (tdbg) atomicAdd(a.trace + tsl + 7, 1ULL);
   // 1. stage the level-m rows of both children (+ the first Q sub-chunk, in flight meanwhile)
-  for (int e = t; e < k * ncol1; e += TR_THREADS) {
-    cp_async8(Z1 + e, Q1 + (long long)r0 * ncol1 + e);
-    cp_async8(Z2 + e, Q2 + (long long)r0 * ncol1 + e);
-  }
+  cp_contig(sm + a.off_Z, Q1 + (long long)r0 * ncol1, k * ncol1, t, TR_THREADS);
+  cp_contig(sm + a.off_Z + round_up(k * ncol1 + 2, 2), Q2 + (long long)r0 * ncol1, k * ncol1, t, TR_THREADS);
   cp_async_commit();
   cp_async_wait_all();
   __syncthreads();
@@ -302,7 +304,8 @@ __device__ void tr_unit(const TrArgs& a, double* sm, int inst, int m, int j, int
   __syncthreads();
   if (chunk == 0) {                       // keep S for the per-leaf v recursion
     double* So = a.Sst + (long long)inst * a.sinst + a.slev[m] + (long long)j * 2 * k * xm;
-    for (int e = t; e < 2 * k * xm; e += TR_THREADS) So[e] = Ss[(e / xm) * lds + e % xm];
+    for (int q = warp; q < 2 * k; q += TR_WARPS)
+      for (int c = lane; c < xm; c += 32) So[q * xm + c] = Ss[q * lds + c];
   }
   TPH(3);
   if (nsub == 0) { __syncthreads(); return; }

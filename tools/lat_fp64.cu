@@ -7,6 +7,11 @@
 
 #define N 256
 
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+
 __device__ __forceinline__ double rcp_approx(double x) {
   double y;
   asm volatile("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
@@ -90,6 +95,53 @@ __global__ void k_lat(double* out, long long* cyc, double seed, volatile double*
     cyc[k] = (c1 - c0) * N / 32;
   }
   ++k;
+  {                                                     // 13 DMMA dependent chain
+    double c0 = x, c1 = 0.0;
+    c0 = clock64();
+    c0 = x;
+    long long s0 = clock64();
+    for (int i = 0; i < N; ++i) dmma884(c0, c1, 1.0000001, 0.5);
+    long long s1 = clock64();
+    if (t == 0) cyc[k] = s1 - s0;
+    ++k;
+    x += c0 + c1;
+  }
+  {                                                     // 14 DMMA 4 independent chains (per DMMA)
+    double c[4][2] = {{x, 0}, {x, 1}, {x, 2}, {x, 3}};
+    long long s0 = clock64();
+    for (int i = 0; i < N / 4; ++i) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) dmma884(c[u][0], c[u][1], 1.0000001, 0.5);
+    }
+    long long s1 = clock64();
+    if (t == 0) cyc[k] = s1 - s0;
+    ++k;
+    x += c[0][0] + c[1][0] + c[2][0] + c[3][0];
+  }
+  {                                                     // 15 DMMA 8 independent chains (per DMMA)
+    double c[8][2];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) { c[u][0] = x + u; c[u][1] = 0.0; }
+    long long s0 = clock64();
+    for (int i = 0; i < N / 8; ++i) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) dmma884(c[u][0], c[u][1], 1.0000001, 0.5);
+    }
+    long long s1 = clock64();
+    if (t == 0) cyc[k] = s1 - s0;
+    ++k;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x += c[u][0];
+  }
+  {                                                     // 16 shfl (double) chain
+    double v = x;
+    long long s0 = clock64();
+    for (int i = 0; i < N; ++i) v = __shfl_sync(0xffffffffu, v, (t + 1) & 31) + 1e-9;
+    long long s1 = clock64();
+    if (t == 0) cyc[k] = s1 - s0;
+    ++k;
+    x += v;
+  }
   out[t] = x;
 }
 
@@ -105,7 +157,8 @@ int main() {
   cudaMemset(flag, 0, 8192 * 8);
   const char* names[] = {"dfma", "sqrt(f64)", "div(f64)", "rcp.approx.f64", "rsqrt(f64)", "lds+cvt chain",
                          "__syncthreads", "L2 load (dep)", "threadfence+st", "fence.acq_rel.gpu",
-                         "st.release+ld.relaxed poll", "atomicAdd (rt)", "nanosleep(16)"};
+                         "st.release+ld.relaxed poll", "atomicAdd (rt)", "nanosleep(16)",
+                         "dmma dep chain", "dmma 4 chains (per op)", "dmma 8 chains (per op)", "shfl f64 + dadd chain"};
   for (int warps : {8, 16}) {
     for (int rep = 0; rep < 2; ++rep) {
       cudaMemset(flag, 0, 8192 * 8);
@@ -114,9 +167,9 @@ int main() {
       if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); return 1; }
     }
     long long h[64];
-    cudaMemcpy(h, cyc, 13 * 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(h, cyc, 17 * 8, cudaMemcpyDeviceToHost);
     printf("warps=%d\n", warps);
-    for (int i = 0; i < 13; ++i) printf("  %-28s %7.1f cycles\n", names[i], (double)h[i] / N);
+    for (int i = 0; i < 17; ++i) printf("  %-28s %7.1f cycles\n", names[i], (double)h[i] / N);
   }
   return 0;
 }
