@@ -397,6 +397,7 @@ static int set_attrs() {
   if (g_attr_mask.load() & bit) return FDE_OK;
   CU(cudaFuncSetAttribute(k_pchol, cudaFuncAttributeMaxDynamicSharedMemorySize, KRAW * PC_ROWS * 8));
   CU(cudaFuncSetAttribute(k_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, EIG_SMEM));
+  CU(cudaFuncSetAttribute(k_solve_level, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * KCAP * KCAP * 8));
   CU(cudaFuncSetAttribute(k_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           LEAF_SMEM));
   CU(cudaFuncSetAttribute(k_lvl_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_REDUCE));
@@ -967,7 +968,7 @@ static int solve_impl(fde_hodlr* H, const double* b, const double* f, double* y,
     // instance's arithmetic must not depend on how many instances share the launch (the sharded
     // cfg4 slices are bitwise equal to the full batch, tests/test_parity_full.py)
     if (node_rows < 4096) {
-      { PROF("k_solve_level"); k_solve_level<<<dim3(1 << l, B, std::max(1, std::min(nrhs, 32))), SL_THREADS, 0, s>>>(sl); }
+      { PROF("k_solve_level"); k_solve_level<<<dim3(1 << l, B, std::max(1, std::min(nrhs, 32))), SL_THREADS, (size_t)3 * sl.k * sl.k * sizeof(double), s>>>(sl); }
       LAUNCHED();
       continue;
     }

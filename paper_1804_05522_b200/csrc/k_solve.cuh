@@ -11,10 +11,12 @@
 // Per step the factor data are streamed once: HBM-bound by design.
 #pragma once
 #include "fde_common.cuh"
+#include "fde_dmma.cuh"
 
 #define SA_THREADS 256
 #define SL_THREADS 256
 #define SA_COLS 4                      // right-hand sides per pass of k_leaf_apply
+#define SL_WQ 3                        // (q, side) reductions per warp at once (k_solve_level)
 
 struct SaArgs {
   TreeDev tree;
@@ -60,6 +62,21 @@ k_leaf_apply(const SaArgs a) {
   }
 }
 
+// sum_q W[q * n] s[q] for one row of the level's panel columns: 4 loads in flight per step,
+// two FMA chains (fixed order; measured: 8 in flight is slower for k_solve_update)
+__device__ __forceinline__ double sl_wdot(const double* wr, int n, const double* s, int k) {
+  double a0 = 0.0, a1 = 0.0;
+  int q = 0;
+  for (; q + 3 < k; q += 4) {
+    const double w0 = wr[(long long)q * n], w1 = wr[(long long)(q + 1) * n];
+    const double w2 = wr[(long long)(q + 2) * n], w3 = wr[(long long)(q + 3) * n];
+    a0 = fma(w0, s[q], a0); a1 = fma(w1, s[q + 1], a1);
+    a0 = fma(w2, s[q + 2], a0); a1 = fma(w3, s[q + 3], a1);
+  }
+  for (; q < k; ++q) a0 = fma(wr[(long long)q * n], s[q], a0);
+  return a0 + a1;
+}
+
 struct SlArgs {
   TreeDev tree;
   int level, k, xcol;                  // level, columns per level (max rank + 1), first X column
@@ -70,10 +87,13 @@ struct SlArgs {
   double* Y; int nrhs, ld;
 };
 
+// dynamic shared memory: the node's kept B, C, Sc^{-1} (3 k^2 doubles, prefetched by cp.async
+// while the dot products run)
 __global__ void __launch_bounds__(SL_THREADS, 4)   // (4 CTAs per SM: the right-hand-side loop over grid.z must not raise the register count)
 k_solve_level(const SlArgs a) {
   __shared__ double z[2 * KCAP];                 // [a (k) | b (k)]
   __shared__ double sv[2 * KCAP];                // [top (k) | y_v (k)]
+  extern __shared__ double Ks[];                 // [B | C | Sc^{-1}] (k x k row-major each)
   const TreeDev& tr = a.tree;
   const int j = blockIdx.x, inst = blockIdx.y, t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int l = a.level, n = tr.n, L = tr.L, k = a.k;
@@ -83,30 +103,47 @@ k_solve_level(const SlArgs a) {
   const double* Ll = a.Lf + (long long)inst * a.lf_stride + tr.lev_lofs[l];
   const double* Kn = a.Kst + (long long)inst * a.kstride_inst + a.kofs + (long long)j * 3 * k * k;
   const double* W = a.X + (long long)inst * a.xstride + (long long)a.xcol * n;
+  for (int e = t; e < 3 * k * k; e += SL_THREADS) cp_async8(Ks + e, Kn + e);
+  cp_async_commit();
+  const double* Bk = Ks;
+  const double* Ck = Ks + k * k;
+  const double* Si = Ks + 2 * k * k;
   for (int c = blockIdx.z; c < a.nrhs; c += gridDim.z) {   // (right-hand sides over grid.z)
     double* y = a.Y + (long long)inst * a.ld * a.nrhs + (long long)c * a.ld;
-    // a_q = V12[:, q]^T y2 (child 2 rows), b_q = V21[:, q]^T y1 (child 1 rows)
-    for (int w = warp; w < 2 * k; w += SL_THREADS / 32) {
-      const int q = w % k, side = w / k;       // side 0: a (child 2), 1: b (child 1)
-      double acc = 0.0;
-      if (q == k - 1) {                        // exact column: single row
-        if (lane == 0) acc = side == 0 ? y[r0 + n1] : y[r0 + n1 - 1];
-      } else if (q < r) {
-        const double* Lq = Ll + (long long)q * m;
-        if (side == 0)
-          for (int i2 = lane; i2 < n2; i2 += 32) acc = fma(Lq[i2], y[r0 + n1 + i2], acc);
-        else
-          for (int j1 = lane; j1 < n1; j1 += 32) acc = fma(Lq[n1 - 1 - j1], y[r0 + j1], acc);
+    // a_q = V12[:, q]^T y2 (child 2 rows), b_q = V21[:, q]^T y1 (child 1 rows): a warp per
+    // SL_WQ items w = (q, side) at once (independent chains, interleaved reductions)
+    for (int w0 = warp; w0 < 2 * k; w0 += SL_WQ * (SL_THREADS / 32)) {
+      double acc[SL_WQ];
+#pragma unroll
+      for (int u = 0; u < SL_WQ; ++u) {
+        const int w = w0 + u * (SL_THREADS / 32);
+        acc[u] = 0.0;
+        if (w >= 2 * k) continue;
+        const int q = w % k, side = w / k;     // side 0: a (child 2), 1: b (child 1)
+        if (q == k - 1) {                      // exact column: single row
+          if (lane == 0) acc[u] = side == 0 ? y[r0 + n1] : y[r0 + n1 - 1];
+        } else if (q < r) {
+          const double* Lq = Ll + (long long)q * m;
+          if (side == 0)
+            for (int i2 = lane; i2 < n2; i2 += 32) acc[u] = fma(Lq[i2], y[r0 + n1 + i2], acc[u]);
+          else
+            for (int j1 = lane; j1 < n1; j1 += 32) acc[u] = fma(Lq[n1 - 1 - j1], y[r0 + j1], acc[u]);
+        }
       }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) z[side * k + q] = acc;
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int u = 0; u < SL_WQ; ++u) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], o);
+      if (lane == 0)
+#pragma unroll
+        for (int u = 0; u < SL_WQ; ++u) {
+          const int w = w0 + u * (SL_THREADS / 32);
+          if (w < 2 * k) z[(w / k) * k + w % k] = acc[u];
+        }
     }
+    cp_async_wait_all();
     __syncthreads();
     if (warp == 0) {                           // y_v = Sc^{-1}(b - C a) ; top = a - B y_v
-      const double* Bk = Kn;
-      const double* Ck = Kn + k * k;
-      const double* Si = Kn + 2 * k * k;
       for (int q = lane; q < k; q += 32) {
         double acc = z[k + q];
         for (int p = 0; p < k; ++p) acc = fma(-Ck[q * k + p], z[p], acc);
@@ -130,12 +167,10 @@ k_solve_level(const SlArgs a) {
       }
     }
     __syncthreads();
-    // y1 -= W1 top (child 1 rows), y2 -= W2 y_v (child 2 rows)
+    // y1 -= W1 top (child 1 rows), y2 -= W2 y_v (child 2 rows): 4 W loads in flight per step
     for (int R = r0 + t; R < r0 + n1 + n2; R += SL_THREADS) {
       const double* s = R < r0 + n1 ? sv : sv + k;
-      double acc = 0.0;
-      for (int q = 0; q < k; ++q) acc = fma(W[(long long)q * n + R], s[q], acc);
-      y[R] -= acc;
+      y[R] -= sl_wdot(W + R, n, s, k);
     }
     __syncthreads();
   }
@@ -251,8 +286,6 @@ k_solve_update(const SlSplitArgs sp) {
   for (int i = cs + t; i < ce; i += SL_THREADS) {
     const int R = r0 + i;
     const double* s = i < n1 ? sv : sv + k;
-    double acc = 0.0;
-    for (int q = 0; q < k; ++q) acc = fma(W[(long long)q * n + R], s[q], acc);
-    y[R] -= acc;
+    y[R] -= sl_wdot(W + R, n, s, k);
   }
 }
