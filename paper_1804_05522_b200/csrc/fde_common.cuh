@@ -13,9 +13,27 @@
 // the environment, so its behaviour is fixed by the C-ABI arguments alone.
 #ifdef FDE_DEBUG
 #include <cstdlib>
+#include <cstdio>
 static inline const char* fde_dbg_env(const char* name) { return getenv(name); }
 #else
 static inline const char* fde_dbg_env(const char*) { return nullptr; }
+#endif
+
+// Device bounds / invariant checks of the diagnostics build (compute-sanitizer is not available
+// on the GPU pool, profiles/r02_sanitizer.md): a failed check prints its location and traps, so
+// the launch fails with an error instead of touching memory it does not own.  Compiled out of
+// the product library.
+#ifdef FDE_DEBUG
+#define FDE_ASSERT(c)                                                               \
+  do {                                                                              \
+    if (!(c)) {                                                                     \
+      printf("FDE_ASSERT failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #c, \
+             (int)blockIdx.x, (int)threadIdx.x);                                    \
+      __trap();                                                                     \
+    }                                                                               \
+  } while (0)
+#else
+#define FDE_ASSERT(c) do { } while (0)
 #endif
 
 // ---- capacities ---------------------------------------------------------------------

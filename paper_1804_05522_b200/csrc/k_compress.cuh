@@ -258,6 +258,7 @@ k_pchol(const PcTask* __restrict__ tasks, const PcChunk* __restrict__ chunks,
       asm volatile("bar.sync 1, %0;" ::"n"(PC_THREADS) : "memory");
     }
     const int p = s_p;
+    FDE_ASSERT(s_stop || (p >= 0 && p < m && k < KRAW));
     double hv[PC_RPT];
 #pragma unroll
     for (int u = 0; u < PC_RPT; ++u) hv[u] = (valid[u] && !s_stop) ? gi[2 + ri[u] + p] : 0.0;   // H[i,p] = g_{2+i+p}

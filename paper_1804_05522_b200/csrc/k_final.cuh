@@ -37,6 +37,7 @@ __device__ void leaf_rhs_final(const TrArgs& geo, const TrArgs* tp, const LeafAr
   double* Ss = LUs + LEAF_MAX * LEAF_MAX;             // S_side blocks of a batch of levels
   PanelCol* pcd = reinterpret_cast<PanelCol*>(Ss);   // then: V-column descriptors (NC - 1)
   const int scap = smem_doubles - RN_FRONT - LEAF_MAX * LEAF_MAX;
+  FDE_ASSERT(s >= 1 && s <= LEAF_MAX && NC <= NCOL_MAX && scap > 0 && r0 + s <= n);
   // ---- the first batch of S blocks, then the stored LU, in flight while the final is formed
   auto issue_lu = [&]() {
     const double* LUg = la->LU + (long long)inst * la->lustride + (long long)leaf * LEAF_SLOT;
@@ -71,6 +72,7 @@ __device__ void leaf_rhs_final(const TrArgs& geo, const TrArgs* tp, const LeafAr
         cp_contig(Ss + o, S_src(m), k * xm, t, LEAF_THREADS);
         o += round_up(k * xm + 2, 2);
       }
+      FDE_ASSERT(o <= scap);
       cp_async_commit();
       if (!lu_issued) { issue_lu(); lu_issued = true; RN_PH(6); cp_async_wait_group1(); } else { RN_PH(6); cp_async_wait_all(); }
       __syncthreads();

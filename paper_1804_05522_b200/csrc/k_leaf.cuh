@@ -508,6 +508,7 @@ __device__ void leaf_project(const LeafArgs& a, double* big, const PanelCol* pcd
     if (prof && t == 0) { const long long t_ = clock64(); atomicAdd(prof + i, (unsigned long long)(t_ - ph_t)); ph_t = t_; }
   };
   const int n = a.tree.n, NV = NC - 1, NVP = round_up(NV, 8), MT = NVP >> 3;
+  FDE_ASSERT((long long)NV * NC <= a.qstride && NVP * LDA_LEAF + 16 * LDA_LEAF <= LEAF_BIG && s <= LEAF_MAX);
   double* Vs = big;                                   // [NVP cols][LDA_LEAF]
   double* Xs = big + NVP * LDA_LEAF;
   const int XCH = min(((LEAF_BIG - NVP * LDA_LEAF) / LDA_LEAF) & ~15, round_up(NC - c_lo, 16));
@@ -612,6 +613,7 @@ __device__ __forceinline__ void leaf_task(const LeafArgs& a, double* smem, int l
   const int r0 = tr.leaf_r0[leaf], s = tr.leaf_n[leaf];
   const int sp = round_up(s, 32), nb = sp >> 5;
   const int where = inst * 65536 + leaf;
+  FDE_ASSERT(s >= 1 && s <= LEAF_MAX && r0 >= 0 && r0 + s <= tr.n && a.xcol[tr.L] <= NCOL_MAX);
   double* LUg = a.LU + (long long)inst * a.lustride + (long long)leaf * LEAF_SLOT;
   double acc[16][2];
   // debug (FDE_TRACE_LEVELS): per-CTA globaltimer stamps at the phase boundaries

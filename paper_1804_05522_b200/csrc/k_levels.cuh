@@ -106,6 +106,7 @@ __device__ void lv_pass(const LvArgs& a, const LvSmem& sm, int inst, int nsub, i
   const int NC = solve ? a.nrhs : (upd >= 0 ? a.xcol[upd] : a.xcol[red + 1]) - tb;
   const int NCP = round_up(NC, 8);
   if (NC <= 0 && red < 0) return;                 // root without fused right-hand side
+  FDE_ASSERT(NCP <= a.lds && rb0 <= n && (nsub < 2 || rb1 <= n) && ra0 >= 0);
   double* T;
   long long cst;
   if (solve) { T = a.Y + (long long)inst * a.ystride; cst = a.ld; }

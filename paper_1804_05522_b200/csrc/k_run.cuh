@@ -85,6 +85,7 @@ __device__ __forceinline__ long long rn_release(const RunArgs& ra, int step, int
   const int rc = ra.tas[0].rc[m];
   for (int c = 1; c < rc; ++c) {
     const unsigned slot = atomicAdd(ra.heads + 2, 1u);
+    FDE_ASSERT((long long)slot < ra.rq_cap);
     const unsigned long long v = (unsigned long long)rn_tid(step, m, c, jj) + 1ULL;
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(ra.rq + slot), "l"(v) : "memory");
   }
@@ -102,6 +103,7 @@ k_run(const RunArgs ra) {
   __shared__ TrArgs s_ta, s_tp;
   __shared__ int s_la_step, s_ta_step, s_tp_step;   // which step's block each copy holds
   if (threadIdx.x == 0) { s_la_step = -1; s_ta_step = -1; s_tp_step = -1; }
+  FDE_ASSERT((long long)ra.smem_doubles * 8 >= LEAF_SMEM);
   const TrArgs& a0 = ra.tas[0];
   const int L = a0.L, nleaf = a0.nleaf;
   const long long n_leaf = (long long)a0.batch * nleaf;
@@ -154,6 +156,8 @@ k_run(const RunArgs ra) {
       const int kind = step == ra.K ? 3 : (int)(tk / n_leaf);
       tk -= (kind == 3 ? 0 : kind) * n_leaf;
       const int inst = (int)(tk / nleaf), leaf = (int)(tk % nleaf);
+      FDE_ASSERT(step >= 0 && step <= ra.K && kind >= 0 && kind <= 3 && (kind == 3) == (step == ra.K));
+      FDE_ASSERT(inst >= 0 && inst < a0.batch && leaf >= 0 && leaf < nleaf);
       int* dn = ra.done + (long long)step * ra.per_step;
       if (kind == 0) {                                // A: build, LU (stored), U columns
         if (s_la_step != step) { rn_copy(&s_la, &ra.las[step]); if (threadIdx.x == 0) s_la_step = step; }
@@ -184,6 +188,8 @@ k_run(const RunArgs ra) {
       const int step = (int)(task >> 48), m = (int)((task >> 40) & 0xff), chunk = (int)((task >> 32) & 0xff);
       const long long jj = task & 0xffffffffLL;
       const int inst = (int)(jj >> m), j = (int)(jj & ((1LL << m) - 1));
+      FDE_ASSERT(step >= 0 && step < ra.K && m >= 0 && m < L && chunk >= 0 && chunk < a0.rc[m]);
+      FDE_ASSERT(inst >= 0 && inst < a0.batch && j >= 0 && j < (1 << m));
       int* dn = ra.done + (long long)step * ra.per_step;
       if (s_ta_step != step) { rn_copy(&s_ta, &ra.tas[step]); if (threadIdx.x == 0) s_ta_step = step; }
       const TrArgs& a = s_ta;

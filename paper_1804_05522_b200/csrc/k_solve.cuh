@@ -103,6 +103,7 @@ k_solve_level(const SlArgs a) {
   const double* Ll = a.Lf + (long long)inst * a.lf_stride + tr.lev_lofs[l];
   const double* Kn = a.Kst + (long long)inst * a.kstride_inst + a.kofs + (long long)j * 3 * k * k;
   const double* W = a.X + (long long)inst * a.xstride + (long long)a.xcol * n;
+  FDE_ASSERT(r0 >= 0 && r0 + n1 + n2 <= n && k >= 1 && k <= KCAP && r <= k - 1);
   for (int e = t; e < 3 * k * k; e += SL_THREADS) cp_async8(Ks + e, Kn + e);
   cp_async_commit();
   const double* Bk = Ks;

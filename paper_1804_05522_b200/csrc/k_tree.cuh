@@ -214,6 +214,7 @@ __device__ void tr_unit(const TrArgs& a, double* sm, int inst, int m, int j, int
   const int rch = m > 0 ? round_up((nrow + a.rc[m] - 1) / a.rc[m], 8) : 0;
   const int ra = chunk * rch, rb = m > 0 ? min(nrow, ra + rch) : 0;
   const int nsub = rb > ra ? (rb - ra + TR_SUB - 1) / TR_SUB : 0;
+  FDE_ASSERT(k >= 1 && k <= a.kmaxc && rb <= max(nrow, 0) && ra >= 0 && ncol1 <= a.NC);
   // sub-chunk buffers: [U1 | U2] x TR_STG, each TR_SUB x ncol1 (+2 spare doubles: 16-byte copies)
   const int usz = TR_SUB * ncol1 + 2;
   auto ubuf = [&](int sc, int which) -> double* {
