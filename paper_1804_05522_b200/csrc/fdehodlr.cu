@@ -157,6 +157,8 @@ struct fde_hodlr {
   PcChunk* d_chunks = nullptr;
   unsigned* d_ctr = nullptr;
   double* d_glseg = nullptr;            // S1 segment products (k_gl_seg)
+  double* d_Kr[2] = {nullptr, nullptr}; // k_run split units: node stores [C | Sc^-1 | G] (2 parities)
+  long long krlev[LMAX] = {}, krinst = 0;
   double *d_part = nullptr, *d_gram_part = nullptr, *d_gram = nullptr, *d_vkeep = nullptr;
   int *d_task_kr = nullptr, *d_task_rank = nullptr;
   DevStatus* d_status = nullptr;
@@ -1041,19 +1043,39 @@ static int run_chunk(fde_hodlr* H, int K, double dt, const double* d_plus, const
     TRY(dalloc(H, &H->d_LUr[0], (size_t)B * H->lustride));
     TRY(dalloc(H, &H->d_LUr[1], (size_t)B * H->lustride));
   }
+  if (!H->d_Kr[0]) {                                 // split units: [C | Sc^-1 | G] per node, 2 parities
+    long long ko = 0;
+    for (int m = 0; m < L; ++m) { H->krlev[m] = ko; ko += (1LL << m) * 3LL * H->kl[m] * H->kl[m]; }
+    H->krinst = std::max(1LL, ko);
+    TRY(dalloc(H, &H->d_Kr[0], (size_t)B * H->krinst));
+    TRY(dalloc(H, &H->d_Kr[1], (size_t)B * H->krinst));
+  }
   // per-step counters: A done [n_leaf], B' done [n_leaf], pair counters [B 2^(L-1)], per
   // level m: chunk completions [B 2^m] and completed children [B 2^m]; ready queue: one slot
   // per tree unit of the run
   const long long n_leaf = (long long)B * H->nleaf;
   RunArgs ra{};
+  // split tree units: per node a U unit (all columns but the right-hand side, off the
+  // step-to-step chain) and an R unit (the right-hand-side column, on it) -- k_tree.cuh tr_unit_R.
+  // It shortens the chain of latency-bound runs and costs ~25 us of SM time per step (511 more
+  // small tasks at cfg3): measured (tools/small_cfgs.py, us/step, unsplit -> split) cfg1 64 -> 53,
+  // cfg2 153 -> 117, n=8192 138 -> 124, n=16384 194 -> 167, n=32768 287 -> 288, cfg3 618 -> 638;
+  // so split while the run has fewer than 2 leaves per SM.
+  {
+    int dev = 0, nsm = 148;
+    CU(cudaGetDevice(&dev));
+    CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    ra.split = (long long)B * H->nleaf < 2LL * nsm;
+  }
+  if (const char* e = fde_dbg_env("FDE_RUN_SPLIT")) ra.split = atoi(e) != 0;   // (diagnostics build)
   long long o = 0, units = 0;
   ra.o_A = o; o += n_leaf;
   ra.o_R = o; o += n_leaf;
-  ra.o_pair = o; o += (long long)B << (L - 1);
   for (int m = 0; m < L; ++m) {
     ra.o_lvl[m] = o; o += (long long)B << m;
-    ra.o_kid[m] = o; o += (long long)B << m;
-    units += ((long long)B << m) * H->trc[m];
+    ra.o_ku[m] = o; o += (long long)B << m;
+    ra.o_kr[m] = o; o += (long long)B << m;
+    units += ((long long)B << m) * (ra.split ? 2 : 1);
   }
   ra.per_step = o;
   const long long need = 4 + (long long)K * o;
@@ -1074,7 +1096,7 @@ static int run_chunk(fde_hodlr* H, int K, double dt, const double* d_plus, const
   ra.done = H->d_runctr + 4;
   ra.rq = H->d_runrq;
   ra.rq_cap = nrq;
-  ra.use_rq = 0;
+  ra.use_rq = ra.split;
   // per-step argument blocks (k_run.cuh RunArgs), copied to the device once per call
   LeafArgs la{};
   la.tree = H->tree; la.mode = 0; la.shift = H->shift; la.cfac = H->d_cfac; la.dt = dt;
@@ -1113,6 +1135,8 @@ static int run_chunk(fde_hodlr* H, int K, double dt, const double* d_plus, const
     // come free from leaf work; measured 630 vs 663 us/step at cfg3
     for (int l = 0; l < L; ++l) tm.rc[l] = 1;
     tm.Q = Qp[p]; tm.Qleaf = Qp[p] + H->qlev[L]; tm.Sst = Sp[p]; tm.X = Xp[p];
+    tm.Kr = ra.split ? H->d_Kr[p] : nullptr; tm.krinst = H->krinst;
+    for (int l = 0; l < L; ++l) tm.krlev[l] = H->krlev[l];
     tm.u = u_out + m * cnt;
   }
   static unsigned long long* run_trace = nullptr;

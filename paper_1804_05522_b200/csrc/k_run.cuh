@@ -49,7 +49,9 @@ struct RunArgs {
   long long rq_cap;              // slots
   int use_rq;                    // some level splits its nodes into row chunks
   int* done; long long per_step; // step m counters: done + m * per_step (m = 0..K-1)
-  long long o_A, o_R, o_pair, o_lvl[LMAX], o_kid[LMAX];   // o_kid[m]: completed children of level-m nodes
+  long long o_A, o_R, o_lvl[LMAX];   // A done, B' done [leaf]; R unit done [node of level m]
+  long long o_ku[LMAX], o_kr[LMAX];  // release counters of level-m nodes: U (2 inputs), R (3 inputs)
+  int split;                         // 1: U / R tree units (one of each per node)
   unsigned long long* trace;     // optional (FDE_TRACE_RUN): [0] count, then [start,end,code,sm]
   unsigned long long* prof;      // optional: B' phase cycle sums [16]
   long long trace_cap;
@@ -81,15 +83,23 @@ __device__ __forceinline__ long long rn_tid(int step, int m, int chunk, long lon
 
 // Node jj of level m (step `step`) just became ready: its chunk 0 is this CTA's continuation,
 // chunks 1.. go to the ready queue.  (thread 0)
+__device__ __forceinline__ void rn_push(const RunArgs& ra, long long tid) {
+  const unsigned slot = atomicAdd(ra.heads + 2, 1u);
+  FDE_ASSERT((long long)slot < ra.rq_cap);
+  const unsigned long long v = (unsigned long long)tid + 1ULL;
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(ra.rq + slot), "l"(v) : "memory");
+}
 __device__ __forceinline__ long long rn_release(const RunArgs& ra, int step, int m, long long jj) {
   const int rc = ra.tas[0].rc[m];
-  for (int c = 1; c < rc; ++c) {
-    const unsigned slot = atomicAdd(ra.heads + 2, 1u);
-    FDE_ASSERT((long long)slot < ra.rq_cap);
-    const unsigned long long v = (unsigned long long)rn_tid(step, m, c, jj) + 1ULL;
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(ra.rq + slot), "l"(v) : "memory");
-  }
+  for (int c = 1; c < rc; ++c) rn_push(ra, rn_tid(step, m, c, jj));
   return rn_tid(step, m, 0, jj);
+}
+// split run: a unit (part 0 = U, 1 = R) became ready -- the continuation if the CTA has none yet,
+// else the ready queue  (thread 0)
+__device__ __forceinline__ void rn_ready_unit(const RunArgs& ra, int step, int m, int part, long long jj,
+                                              long long& cont) {
+  const long long tid = rn_tid(step, m, part, jj);
+  if (cont < 0) cont = tid; else rn_push(ra, tid);
 }
 
 __global__ void __launch_bounds__(TR_THREADS, 1)
@@ -108,7 +118,7 @@ k_run(const RunArgs ra) {
   const int L = a0.L, nleaf = a0.nleaf;
   const long long n_leaf = (long long)a0.batch * nleaf;
   long long Tt = 0;
-  for (int m = 0; m < L; ++m) Tt += (long long)a0.batch * (1LL << m) * a0.rc[m];
+  for (int m = 0; m < L; ++m) Tt += (long long)a0.batch * (1LL << m) * (ra.split ? 2 : a0.rc[m]);
   const unsigned tot_t = (unsigned)(Tt * ra.K), tot_l = (unsigned)(3 * n_leaf * ra.K + n_leaf);
   volatile unsigned* vh = ra.heads;     // [0] tree units completed, [1] leaf tickets, [2] rq tail, [3] rq head
   long long held = -1;                  // thread 0: leaf ticket not yet runnable
@@ -180,7 +190,12 @@ k_run(const RunArgs ra) {
         if (kind == 2) atomicAdd(dn + ra.o_R + tk, 1);
         if (kind >= 1) {
           const long long jj = (long long)inst * (1 << (L - 1)) + (leaf >> 1);
-          if (atomicAdd(dn + ra.o_pair + jj, 1) == 3) cont = rn_release(ra, step, L - 1, jj);
+          if (ra.split) {                           // B -> U of the bottom node; B' -> its R
+            if (kind == 1) { if (atomicAdd(dn + ra.o_ku[L - 1] + jj, 1) == 1) rn_ready_unit(ra, step, L - 1, 0, jj, cont); }
+            else if (atomicAdd(dn + ra.o_kr[L - 1] + jj, 1) == 2) rn_ready_unit(ra, step, L - 1, 1, jj, cont);
+          } else if (atomicAdd(dn + ra.o_ku[L - 1] + jj, 1) == 3) {
+            cont = rn_release(ra, step, L - 1, jj);
+          }
         }
       }
       code = 100 + kind + 1000 * step;
@@ -188,22 +203,32 @@ k_run(const RunArgs ra) {
       const int step = (int)(task >> 48), m = (int)((task >> 40) & 0xff), chunk = (int)((task >> 32) & 0xff);
       const long long jj = task & 0xffffffffLL;
       const int inst = (int)(jj >> m), j = (int)(jj & ((1LL << m) - 1));
-      FDE_ASSERT(step >= 0 && step < ra.K && m >= 0 && m < L && chunk >= 0 && chunk < a0.rc[m]);
+      FDE_ASSERT(step >= 0 && step < ra.K && m >= 0 && m < L && chunk >= 0 && chunk < (ra.split ? 2 : a0.rc[m]));
       FDE_ASSERT(inst >= 0 && inst < a0.batch && j >= 0 && j < (1 << m));
       int* dn = ra.done + (long long)step * ra.per_step;
       if (s_ta_step != step) { rn_copy(&s_ta, &ra.tas[step]); if (threadIdx.x == 0) s_ta_step = step; }
       const TrArgs& a = s_ta;
-      tr_unit(a, smem, inst, m, j, chunk);
+      const bool runit = ra.split && chunk == 1;
+      if (runit) tr_unit_R(a, smem, inst, m, j);
+      else tr_unit(a, smem, inst, m, j, ra.split ? 0 : chunk);
       __syncthreads();
       if (threadIdx.x == 0) {
         __threadfence();
-        if (atomicAdd(dn + ra.o_lvl[m] + jj, 1) == a.rc[m] - 1 && m > 0) {
-          const long long pj = (long long)inst * (1 << (m - 1)) + (j >> 1);   // node complete
-          if (atomicAdd(dn + ra.o_kid[m - 1] + pj, 1) == 1) cont = rn_release(ra, step, m - 1, pj);
+        const long long pj = m > 0 ? (long long)inst * (1 << (m - 1)) + (j >> 1) : 0;
+        if (!ra.split) {
+          if (atomicAdd(dn + ra.o_lvl[m] + jj, 1) == a.rc[m] - 1 && m > 0) {   // node complete
+            if (atomicAdd(dn + ra.o_ku[m - 1] + pj, 1) == 1) cont = rn_release(ra, step, m - 1, pj);
+          }
+        } else if (!runit) {                        // U: parent's U (2 children), own R (+1)
+          if (m > 0 && atomicAdd(dn + ra.o_ku[m - 1] + pj, 1) == 1) rn_ready_unit(ra, step, m - 1, 0, pj, cont);
+          if (atomicAdd(dn + ra.o_kr[m] + jj, 1) == 2) rn_ready_unit(ra, step, m, 1, jj, cont);
+        } else {                                    // R: node done, parent's R (+1)
+          atomicAdd(dn + ra.o_lvl[m] + jj, 1);
+          if (m > 0 && atomicAdd(dn + ra.o_kr[m - 1] + pj, 1) == 2) rn_ready_unit(ra, step, m - 1, 1, pj, cont);
         }
         atomicAdd(ra.heads, 1u);
       }
-      code = m + 1000 * step;
+      code = (runit ? 50 : 0) + m + 1000 * step;
     }
     if (ra.trace && threadIdx.x == 0) {
       const unsigned long long e = atomicAdd(ra.trace, 1ULL);

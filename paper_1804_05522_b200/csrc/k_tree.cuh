@@ -45,6 +45,8 @@ struct TrArgs {
   unsigned* bar;
   DevStatus* st;
   unsigned long long* trace;     // optional: globaltimer after every level (FDE_TRACE_LEVELS)
+  double* Kr;                    // k_run split units: node store [C | Sc^{-1} | G] (k x k each) per node, or null
+  long long krlev[LMAX], krinst; // per-instance offset of level m's node store, instance stride
   int kp, lds, ldk, lda, rch_max;  // smem geometry (host computed)
   int off_B, off_C, off_M, off_M2, off_S, off_T, off_Z, off_U;
 };
@@ -294,6 +296,15 @@ __device__ void tr_unit(const TrArgs& a, double* sm, int inst, int m, int j, int
   TPH(2);
   tr_dmma(Gs, ldk, nullptr, 0, Bz, ncol1, Mi, ldk, k, k, k, 1.0);          // G = B Sc^{-1}
   __syncthreads();
+  if (a.Kr && chunk == 0) {               // U unit of the split run: what the R unit needs
+    double* Kn = a.Kr + (long long)inst * a.krinst + a.krlev[m] + (long long)j * 3 * k * k;
+    for (int e = t; e < k * k; e += TR_THREADS) {
+      const int q = e / k, p = e - q * k;
+      Kn[e] = Cz[q * ncol1 + p];
+      Kn[k * k + e] = Mi[q * ldk + p];
+      Kn[2 * k * k + e] = Gs[q * ldk + p];
+    }
+  }
   // 4. S_bot = Sc^{-1} T -> Ss rows k..2k-1 ; S_top = R_top - G T -> Ss rows 0..k-1
   tr_dmma(Ss + k * lds, lds, nullptr, 0, Mi, ldk, Ts, lds, k, xm, k, 1.0);
   tr_dmma(Ss, lds, Z2, ncol1, Gs, ldk, Ts, lds, k, xm, k, -1.0);
@@ -361,6 +372,68 @@ __device__ void tr_unit(const TrArgs& a, double* sm, int inst, int m, int j, int
   }
   TPH(4);
 #undef TPH
+}
+
+// R unit of node (m, j) in the split pipelined run (k_run.cuh): the right-hand-side column alone.
+// The node's U unit (tr_unit over all columns, column 0 left as don't-care) stored C, Sc^{-1} and
+// G = B Sc^{-1}; with R_top0 = Q_c2[lvl m, 0], R_bot0 = Q_c1[lvl m, 0]:
+//   t = R_bot0 - C R_top0,  S_bot[:, 0] = Sc^{-1} t,  S_top[:, 0] = R_top0 - G t,
+//   Q_node[r, 0] = Q_c1[r, 0] + Q_c2[r, 0] - Q_c1[r, m-cols] S_top[:, 0] - Q_c2[r, m-cols] S_bot[:, 0]
+// (the same algebra as tr_unit, restricted to column 0).
+__device__ void tr_unit_R(const TrArgs& a, double* sm, int inst, int m, int j) {
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int xm = a.xc[m], k = a.xc[m + 1] - xm, ncol1 = a.xc[m + 1];
+  const long long qs1 = (long long)(ncol1 - 1) * ncol1;
+  const double* Q1 = a.Q + (long long)inst * a.qinst + a.qlev[m + 1] + (long long)(2 * j) * qs1;
+  const double* Q2 = Q1 + qs1;
+  const double* Kn = a.Kr + (long long)inst * a.krinst + a.krlev[m] + (long long)j * 3 * k * k;
+  const int nr = ncol1 - 1;                          // rows of the child Q (incl. the level-m rows)
+  const int kp1 = k + 1;                             // staged row: [column 0 | m-cols]
+  double* Ks = sm;                                   // [C | Sc^-1 | G]
+  double* R1 = Ks + 3 * k * k;                       // [nr][k+1] of Q_c1
+  double* R2 = R1 + nr * kp1;                        // [nr][k+1] of Q_c2
+  double* tv = R2 + nr * kp1;                        // t [k], s_top [k], s_bot [k]
+  FDE_ASSERT(xm >= 1 && k >= 1 && ncol1 <= a.NC);
+  for (int e = t; e < 3 * k * k; e += TR_THREADS) cp_async8(Ks + e, Kn + e);
+  for (int e = t; e < nr * kp1; e += TR_THREADS) {
+    const int r = e / kp1, c = e - r * kp1;
+    const int col = c == 0 ? 0 : xm + c - 1;
+    cp_async8(R1 + e, Q1 + (long long)r * ncol1 + col);
+    cp_async8(R2 + e, Q2 + (long long)r * ncol1 + col);
+  }
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncthreads();
+  const double* C = Ks;
+  const double* Mi = Ks + k * k;
+  const double* G = Ks + 2 * k * k;
+  if (warp == 0) {
+    for (int q = lane; q < k; q += 32) {           // t = R_bot0 - C R_top0
+      double acc = R1[(xm - 1 + q) * kp1];
+      for (int p = 0; p < k; ++p) acc = fma(-C[q * k + p], R2[(xm - 1 + p) * kp1], acc);
+      tv[q] = acc;
+    }
+    __syncwarp();
+    for (int q = lane; q < k; q += 32) {           // S_bot0 = Sc^-1 t ; S_top0 = R_top0 - G t
+      double sb = 0.0, st = R2[(xm - 1 + q) * kp1];
+      for (int p = 0; p < k; ++p) { sb = fma(Mi[q * k + p], tv[p], sb); st = fma(-G[q * k + p], tv[p], st); }
+      tv[k + q] = st; tv[2 * k + q] = sb;
+    }
+  }
+  __syncthreads();
+  double* So = a.Sst + (long long)inst * a.sinst + a.slev[m] + (long long)j * 2 * k * xm;
+  for (int q = t; q < 2 * k; q += TR_THREADS) So[(long long)q * xm] = tv[k + q];   // [S_top; S_bot][:, 0]
+  if (m > 0) {
+    double* Qo = a.Q + (long long)inst * a.qinst + a.qlev[m] + (long long)j * (long long)(xm - 1) * xm;
+    for (int r = t; r < xm - 1; r += TR_THREADS) {
+      const double* r1 = R1 + r * kp1;
+      const double* r2 = R2 + r * kp1;
+      double acc = r1[0] + r2[0];
+      for (int q = 0; q < k; ++q) acc = fma(-r1[1 + q], tv[k + q], fma(-r2[1 + q], tv[2 * k + q], acc));
+      Qo[(long long)r * xm] = acc;
+    }
+  }
+  __syncthreads();
 }
 
 #define TR_NL 4                  // leaves per final-pass group (one warp each in the v phase)

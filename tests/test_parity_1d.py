@@ -340,6 +340,35 @@ def test_pipelined_run_matches_steps_and_oracle(n, alpha, leaf, batch):
     st.close(); st2.close()
 
 
+@gpu
+def test_pipelined_run_split_and_unsplit_tree_units_agree():
+    """k_run splits every tree unit into a U unit (all columns but the right-hand side) and an R
+    unit (the right-hand-side column) while the run has fewer than 2 leaves per SM, and runs whole
+    units otherwise (csrc/fdehodlr.cu run_chunk).  The same instance alone (128 leaves: split) and
+    inside a batch of 3 (384 leaves: whole units) agree to rounding, and both follow the dense
+    oracle trajectory."""
+    n, K, batch = 2000, 4, 3
+    wl = W.make_1d(n, np.array([1.7, 1.4, 1.55]), 16, 1e-12, K=K, batch=batch)
+    from paper_1804_05522_b200.hodlr import Fde1dStepper
+    DP = torch.stack([_t(wl.coeffs(m)[0]) for m in range(1, K + 1)])
+    DM = torch.stack([_t(wl.coeffs(m)[1]) for m in range(1, K + 1)])
+    F = torch.stack([_t(wl.source(m)) for m in range(1, K + 1)])
+    st3 = _stepper(wl)
+    assert 3 * 128 >= 2 * torch.cuda.get_device_properties(0).multi_processor_count > 128
+    out3 = st3.run(wl.dt, DP, DM, F, _t(wl.u0)).cpu().numpy()
+    st1 = Fde1dStepper(n, wl.alpha[:1], wl.h, wl.tol, wl.leaf, batch=1)
+    out1 = st1.run(wl.dt, DP[:, :1].contiguous(), DM[:, :1].contiguous(), F[:, :1].contiguous(),
+                   _t(wl.u0[:1])).cpu().numpy()
+    uo = wl.u0
+    for m in range(1, K + 1):
+        assert _rel(out1[m - 1, 0], out3[m - 1, 0]) <= 1e-12, (m, _rel(out1[m - 1, 0], out3[m - 1, 0]))
+        uo = np.stack([_oracle_step(wl, m, uo, b) for b in range(batch)])
+        for b in range(batch):
+            assert _rel(out3[m - 1, b], uo[b]) <= 1e-8, (m, b)
+        assert _rel(out1[m - 1, 0], uo[0]) <= 1e-8, m
+    st1.close(); st3.close()
+
+
 RUN_EDGE = [  # n, alpha, leaf, K, batch
     (300, 1.3, 40, 3, 1),      # ragged leaves, odd leaf offsets
     (1001, 1.9, 100, 4, 2),    # odd n (misaligned row pairs), batch

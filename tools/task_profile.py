@@ -40,6 +40,7 @@ def main():
     rows = [tuple(int(x) for x in ln.split()) for ln in open(path)]
     os.remove(path)
     names = {100: "A", 101: "B", 102: "B'", 103: "final"}
+    names.update({50 + m: "R%d" % m for m in range(24)})   # split run: right-hand-side units
     by = collections.defaultdict(list)
     t0, t1 = min(r[0] for r in rows), max(r[1] for r in rows)
     nsm = len(set(r[3] for r in rows))

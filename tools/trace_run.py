@@ -27,6 +27,7 @@ t0 = min(r[0] for r in rows)
 t1 = max(r[1] for r in rows)
 span = (t1 - t0) / 1e3
 names = {100: "A leaf", 101: "B proj", 102: "B' rhs", 103: "final"}
+names.update({50 + m: "R%d" % m for m in range(24)})   # split run: right-hand-side units
 by = collections.defaultdict(list)
 step_end = collections.defaultdict(int)
 busy = 0
