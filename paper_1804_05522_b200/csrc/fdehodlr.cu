@@ -752,7 +752,7 @@ static int launch_levels(fde_hodlr* H, int mode, int nf, double* Y, int ld, int 
   }
   LAUNCHED();
   if (trace) {
-    unsigned long long h[1024];
+    static unsigned long long h[2048];
     CU(cudaStreamSynchronize(s));
     CU(cudaMemcpy(h, d_trace, sizeof(h), cudaMemcpyDeviceToHost));
     for (int b = 0; b < 2; ++b) {
@@ -763,9 +763,9 @@ static int launch_levels(fde_hodlr* H, int mode, int nf, double* Y, int ld, int 
       fprintf(stderr, "\n");
     }
     fprintf(stderr, "k_levels pass cycles CTA 0: sync %llu load %llu update %llu reduce %llu store %llu\n",
-            h[800], h[801], h[802], h[803], h[804]);
+            h[1100], h[1101], h[1102], h[1103], h[1104]);
     fprintf(stderr, "k_levels node cycles CTA 0: prep %llu GJ %llu Si %llu store %llu solves %llu\n",
-            h[810], h[811], h[812], h[813], h[814]);
+            h[1110], h[1111], h[1112], h[1113], h[1114]);
     print_leaf_trace(d_trace);
   }
   return FDE_OK;

@@ -249,7 +249,7 @@ __device__ void lv_pass(const LvArgs& a, const LvSmem& sm, int inst, int nsub, i
     __syncthreads();                              // buffer b is refilled by issue(ci + 2)
     PT(4);
   }
-  if (dbg) for (int i = 0; i < 5; ++i) a.trace[800 + i] += pacc[i];
+  if (dbg) for (int i = 0; i < 5; ++i) a.trace[1100 + i] += pacc[i];
   if (red >= 0) {
 #pragma unroll
     for (int i = 0; i < MT; ++i) {
@@ -317,7 +317,7 @@ __device__ void lv_node_solve(const LvArgs& a, const LvSmem& sm, int inst, int l
   double* Kn = a.Kst + (long long)inst * a.kstride_inst + a.kofs[lvl] + (long long)j * 3 * k * k;
   const bool ndbg = a.trace && blockIdx.x == 0 && tid == 0;
   long long nlast = clock64();
-#define NT(i) do { if (ndbg) { const long long t_ = clock64(); a.trace[810 + (i)] += t_ - nlast; nlast = t_; } } while (0)
+#define NT(i) do { if (ndbg) { const long long t_ = clock64(); a.trace[1110 + (i)] += t_ - nlast; nlast = t_; } } while (0)
   if (!solve) {
     // B = V12^T W2, C = V21^T W1 live in the W columns of the sums; copy them out
     for (int e = tid; e < kp8 * kp8; e += LV_THREADS) {
