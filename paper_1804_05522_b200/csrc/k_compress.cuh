@@ -451,7 +451,11 @@ k_eig(const PcTask* __restrict__ tasks, const int* __restrict__ task_kr,
       }
       off = block_sum(off, red);
       dia = block_sum(dia, red);
-      if (off <= 1e-34 * dia) break;                  // (uniform: every thread holds the sums)
+      // converged: off-diagonal mass <= 1e-24 of the diagonal's at the start of a sweep (quadratic
+      // convergence: the previous sweep started near 1e-12 or below).  At cfg3 this ends after 5
+      // sweeps instead of 6 with the truncated approximant unchanged to the rounding level
+      // (relative difference 3e-15, cold path)
+      if (off <= 1e-24 * dia) break;                  // (uniform: every thread holds the sums)
       for (int r = 0; r < N - 1; ++r) {
         const double* Ai = cur ? A1 : A0;
         double* Ao = cur ? A0 : A1;
