@@ -160,6 +160,10 @@ k_pchol(const PcTask* __restrict__ tasks, const PcChunk* __restrict__ chunks,
   unsigned step = 0;
 #ifdef FDE_DEBUG
   const long long pc_start = clock64();
+  long long pc_ph[4] = {0, 0, 0, 0}, pc_t = pc_start;
+#define PCPH(i) do { if (g_comp_trace && t == 0) { const long long t_ = clock64(); pc_ph[i] += t_ - pc_t; pc_t = t_; } } while (0)
+#else
+#define PCPH(i) do { } while (0)
 #endif
   // Stopping threshold of the pivoted Cholesky (s_total below): tau * PC_STOP, floored at the
   // rounding level of the residual trace.  Stopping well below tau lets the optimal
@@ -208,6 +212,7 @@ k_pchol(const PcTask* __restrict__ tasks, const PcChunk* __restrict__ chunks,
       }
     }
     ++step;
+    PCPH(0);
     // ---- warp 0: wait for the G slots of this step, fixed-order reduction, winner's pivot row
     if (w == 0) {
       double tot = 0.0, bv = -1.0; int bi = 0x7fffffff, bs = 0;
@@ -222,6 +227,7 @@ k_pchol(const PcTask* __restrict__ tasks, const PcChunk* __restrict__ chunks,
         __nanosleep(16);
       }
       asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      PCPH(1);
       for (int c = lane; c < G; c += 32) {
         const double* o = part + ((long long)(tk.slot0 + c) * 2 + ((step - 1) & 1)) * PSTRIDE;
         tot += __ldcg(o);
@@ -263,6 +269,7 @@ k_pchol(const PcTask* __restrict__ tasks, const PcChunk* __restrict__ chunks,
 #pragma unroll
     for (int u = 0; u < PC_RPT; ++u) hv[u] = (valid[u] && !s_stop) ? gi[2 + ri[u] + p] : 0.0;   // H[i,p] = g_{2+i+p}
     __syncthreads();
+    PCPH(2);
     if (s_stop) break;
     const double sp = sqrt(s_pmax);
 #pragma unroll
@@ -283,11 +290,13 @@ k_pchol(const PcTask* __restrict__ tasks, const PcChunk* __restrict__ chunks,
       Lc[k * PC_ROWS + lr] = l;
     }
     ++k;
+    PCPH(3);
   }
   const int kr = k;
 #ifdef FDE_DEBUG
   if (g_comp_trace && t == 0 && ch.grank == 0)
-    printf("k_pchol task %d level %d G %d pivots %d cycles %lld\n", ch.task, tk.level, G, kr, clock64() - pc_start);
+    printf("k_pchol task %d level %d G %d pivots %d cycles %lld  local+publish %lld poll %lld gather %lld update %lld\n",
+           ch.task, tk.level, G, kr, clock64() - pc_start, pc_ph[0], pc_ph[1], pc_ph[2], pc_ph[3]);
 #endif
   // ---- raw factor to global (for the transform kernel)
   {
