@@ -822,7 +822,8 @@ __device__ __forceinline__ void leaf_task(const LeafArgs& a, double* smem, int l
     }
     stamp(3);
     if (a.Q && do_proj)
-      leaf_project(a, A, pcd, c_begin, c_end, s, sp, Xi, a.Q + (long long)inst * a.qinst + (long long)leaf * a.qstride);
+      leaf_project(a, A, pcd, c_begin, c_end, s, sp, Xi, a.Q + (long long)inst * a.qinst + (long long)leaf * a.qstride,
+                   c_begin);
     stamp(4);
   } else {
     // ---- solve mode: factor from HBM, right-hand sides b (+ dt f) -> y (y may alias b)
