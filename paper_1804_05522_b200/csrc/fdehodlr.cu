@@ -10,6 +10,9 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "fde_common.cuh"
 #include "k_gl.cuh"
 #include "k_compress.cuh"
@@ -173,8 +176,17 @@ struct fde_hodlr {
   double* d_hstage = nullptr;       // fde1d_run with FDE_HOST_PTRS: device staging
   size_t hstage_cap = 0;
   size_t solve_split_cap = 0;
+  // TMA tensor maps of the projection (k_leaf.cuh leaf_project_tma): per (instance, level) a
+  // 2D map of L_l (rows x rank, box 132 x rank), then the 3D maps of X and X2 (n x NC x batch,
+  // box 132 x 16 x 1); null when some operand is not 16-byte aligned (the projection then
+  // stages through cp.async)
+  CUtensorMap* d_tmaps = nullptr;
+  bool tma_ok = false;
   cudaStream_t last_stream = nullptr;
 };
+
+static int tmaps_build(fde_hodlr* H, const std::vector<int>& rk);
+static int tmaps_add_x2(fde_hodlr* H);
 
 template <typename T>
 static int dalloc(fde_hodlr* H, T** p, size_t count) {
@@ -709,6 +721,7 @@ static int finalize_layout(fde_hodlr* H, cudaStream_t s) {
   if (!post.empty())
     CU(cudaMemcpy(H->d_post, post.data(), post.size() * sizeof(int), cudaMemcpyHostToDevice));
   TRY(tree_layout(H));
+  TRY(tmaps_build(H, rk));
   H->layout_done = true;
   return FDE_OK;
 }
@@ -924,6 +937,8 @@ static int factor_impl(fde_hodlr* H, const double* dp, const double* dm, int nf,
   la.xcol[L] = H->xcol[L];
   la.X = H->d_X; la.xstride = H->xstride; la.LU = H->d_LU; la.lustride = H->lustride;
   la.keep = keep; la.nf = nf; la.u_prev = u_prev; la.f = f; la.st = H->d_status;
+  la.lmap = H->tma_ok ? H->d_tmaps : nullptr;
+  la.xmap = H->tma_ok ? H->d_tmaps + (size_t)B * L : nullptr;
   TRY(trace_reset(s));
   la.trace = g_trace;
   const bool tree = nf == 1 && !keep && H->tree_ok && !fde_dbg_env("FDE_LEVEL_PASSES");
@@ -1027,6 +1042,75 @@ static int matvec_impl(fde_hodlr* H, const double* x, double* y, int nrhs, int l
 }
 
 // ---------------------------------------------------------------------------------------
+// ---- TMA tensor maps (cuTensorMapEncodeTiled through the runtime's driver entry point) ----
+static PFN_cuTensorMapEncodeTiled_v12000 g_tmap_encode = nullptr;
+static bool tmap_encode(CUtensorMap* m, int rank, void* base, const cuuint64_t* dims,
+                        const cuuint64_t* strides_bytes, const cuuint32_t* box) {
+  if (!g_tmap_encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn) {
+      cudaGetLastError();
+      return false;
+    }
+    g_tmap_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return g_tmap_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)rank, base, dims, strides_bytes, box,
+                       estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// X map of one panel buffer (slot B*L or B*L+1 of d_tmaps)
+static bool tmap_x(fde_hodlr* H, int slot, double* X, CUtensorMap* out) {
+  const int NC = H->xcol[H->L];
+  if ((H->n & 1) || (reinterpret_cast<unsigned long long>(X) & 15)) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)H->n, (cuuint64_t)NC, (cuuint64_t)H->batch};
+  const cuuint64_t str[2] = {(cuuint64_t)H->n * 8, (cuuint64_t)H->xstride * 8};
+  const cuuint32_t box[3] = {(cuuint32_t)LEAF_LDV, 16, 1};
+  (void)slot;
+  return tmap_encode(out, 3, X, dims, str, box);
+}
+// All maps of a handle after the layout (ranks known): L maps + the X map of d_X (+ d_X2 if any).
+static int tmaps_build(fde_hodlr* H, const std::vector<int>& rk) {
+  const int L = H->L, B = H->batch;
+  H->tma_ok = false;
+  if (L == 0) return FDE_OK;
+  std::vector<CUtensorMap> m((size_t)B * L + 2);
+  bool ok = true;
+  for (int b = 0; b < B && ok; ++b)
+    for (int l = 0; l < L && ok; ++l) {
+      const int r = rk[(size_t)b * L + l], ml = H->lev_m[l];
+      if (r == 0) continue;
+      double* base = H->d_Lf + (long long)b * H->lf_stride + H->lev_lofs[l];
+      if ((ml & 1) || (reinterpret_cast<unsigned long long>(base) & 15)) { ok = false; break; }
+      const cuuint64_t dims[2] = {(cuuint64_t)ml, (cuuint64_t)r};
+      const cuuint64_t str[1] = {(cuuint64_t)ml * 8};
+      const cuuint32_t box[2] = {(cuuint32_t)LEAF_LDV, (cuuint32_t)r};
+      ok = tmap_encode(&m[(size_t)b * L + l], 2, base, dims, str, box);
+    }
+  ok = ok && tmap_x(H, B * L, H->d_X, &m[(size_t)B * L]);
+  if (ok && H->d_X2) ok = tmap_x(H, B * L + 1, H->d_X2, &m[(size_t)B * L + 1]);
+  if (!ok) return FDE_OK;                            // (the cp.async projection is used)
+  if (!H->d_tmaps) {
+    void* q = nullptr;
+    CU(cudaMalloc(&q, m.size() * sizeof(CUtensorMap)));
+    H->allocs.push_back(q);
+    H->d_tmaps = reinterpret_cast<CUtensorMap*>(q);
+  }
+  CU(cudaMemcpy(H->d_tmaps, m.data(), m.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+  H->tma_ok = true;
+  return FDE_OK;
+}
+// the map of X2 once the pipelined run allocates it
+static int tmaps_add_x2(fde_hodlr* H) {
+  if (!H->tma_ok) return FDE_OK;
+  CUtensorMap mx;
+  if (!tmap_x(H, H->batch * H->L + 1, H->d_X2, &mx)) { H->tma_ok = false; return FDE_OK; }
+  CU(cudaMemcpy(H->d_tmaps + (size_t)H->batch * H->L + 1, &mx, sizeof(mx), cudaMemcpyHostToDevice));
+  return FDE_OK;
+}
+
 // C-ABI
 // One k_run launch of K <= RUN_KMAX pipelined steps: u_out[m] = A_m^{-1}(u^(m-1) + dt f^(m)),
 // u^(-1) = u0 (the caller's chunk base pointers).
@@ -1042,6 +1126,7 @@ static int run_chunk(fde_hodlr* H, int K, double dt, const double* d_plus, const
     TRY(dalloc(H, &H->d_S2, (size_t)B * H->sinst));
     TRY(dalloc(H, &H->d_LUr[0], (size_t)B * H->lustride));
     TRY(dalloc(H, &H->d_LUr[1], (size_t)B * H->lustride));
+    TRY(tmaps_add_x2(H));
   }
   if (!H->d_Kr[0]) {                                 // split units: [C | Sc^-1 | G] per node, 2 parities
     long long ko = 0;
@@ -1128,6 +1213,8 @@ static int run_chunk(fde_hodlr* H, int K, double dt, const double* d_plus, const
     lm.dp = d_plus + m * coef_stride; lm.dm = d_minus + m * coef_stride; lm.f = f + m * f_stride;
     lm.u_prev = m == 0 ? u0 : u_out + (m - 1) * cnt;
     lm.X = Xp[p]; lm.LU = H->d_LUr[p]; lm.Q = Qp[p] + H->qlev[L];
+    lm.lmap = H->tma_ok ? H->d_tmaps : nullptr;
+    lm.xmap = H->tma_ok ? H->d_tmaps + (size_t)B * L + p : nullptr;
     TrArgs& tm = H->run_tas[m];
     tm = a;
     // one unit per node in the pipelined run: the row-chunk split that shortens k_step's exposed
@@ -1190,6 +1277,8 @@ static int run_chunk(fde_hodlr* H, int K, double dt, const double* d_plus, const
       const double cb = (double)std::max(1ULL, pf[27]) * 1965.0;
       fprintf(stderr, "k_run B phases (us avg over %llu): V+X staging %.2f dmma %.2f\n",
               pf[27], pf[25] / cb, pf[26] / cb);
+      fprintf(stderr, "k_run B tma (warp 1, us avg): setup %.2f Vwait+swap %.2f compute %.2f fullwait %.2f tail-sync %.2f\n",
+              pf[28] / cb, pf[29] / cb, pf[30] / cb, pf[31] / cb, pf[32] / cb);
     }
     for (int g = 0; g < 2; ++g) {
       const double c = (double)std::max(1ULL, pf[8 * g + 7]);

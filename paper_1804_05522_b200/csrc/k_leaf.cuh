@@ -36,6 +36,8 @@
 #define LEAF_SMEM ((LEAF_FRONT + LEAF_BIG) * 8)
 #define GJ_WARPS 4                   // warps of the 32 x 32 diagonal-block Gauss-Jordan
 #define LEAF_OVW 8                   // register tiles per warp of an overwrite GEMM
+#define LEAF_LDV 132                 // row pitch of the TMA boxes of the projection (= LDA_LEAF)
+struct alignas(64) CUtensorMapLike { unsigned long long opaque[16]; };   // (= CUtensorMap, 128 bytes)
 
 struct LeafArgs {
   TreeDev tree;
@@ -59,6 +61,8 @@ struct LeafArgs {
   unsigned long long* prof;                  // optional: phase cycle sums (k_run FDE_TRACE_RUN)
   DevStatus* st;
   unsigned long long* trace;                 // optional phase clocks (FDE_TRACE_LEVELS)
+  const void* lmap;                          // TMA maps of L_l: [inst * L + l] (CUtensorMap), or null
+  const void* xmap;                          // TMA map of this X buffer (n x NC x batch), or null
 };
 
 // ---- DMMA GEMMs on column-major shared-memory operands ---------------------------------
@@ -594,6 +598,176 @@ __device__ void leaf_project(const LeafArgs& a, double* big, const PanelCol* pcd
   if (prof && t == 0) atomicAdd(prof + 3, 1ULL);
 }
 
+// The same projection for whole leaves (s % 32 == 0) with every operand moved by the TMA
+// engine (cp.async.bulk.tensor, host-encoded maps, LeafArgs::lmap / xmap) and no CTA barrier
+// in the product loop:
+//   * V: one 132 x r_l box of L_l per level (rows li0 .. li0+131, or li0-s+1 .. for a child-0
+//     leaf, whose run is then reversed in place); each level's k_l columns form a 128-byte
+//     aligned block at pitch LEAF_LDV (colofs[j] = shared offset of V column j); the exact /
+//     padding columns are written by the threads;
+//   * X: 132 x 16 boxes (16 panel columns) through a ring of NB slots, each with a "full"
+//     mbarrier (bytes in flight) and a shared counter of the warps done with it: the last warp
+//     to finish a chunk refills its slot with chunk c + NB at once (no producer warp);
+//   * work unit = (m-tile pair) x (16-column chunk); unit u of the global order (chunk-major)
+//     belongs to warp (u + 1) % 8, balanced across chunks (warp 0, which issues the first
+//     copies, gets the smaller share).
+// Output rows >= NV / columns >= NC of a tile are dropped (a product column depends only on its
+// own B column; out-of-range box columns are zero-filled by the TMA).  Same per-element
+// arithmetic as leaf_project: Q[j][c] = sum over k0 ascending of the 4-term DMMA k-steps.
+#define PB_NB_MAX 4
+__device__ __forceinline__ void tma_load_2d(void* dst, const void* map, int c0, int c1, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+               ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const void* map, int c0, int c1, int c2,
+                                            unsigned long long* bar) {
+  asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+               ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ bool leaf_project_tma(const LeafArgs& a, double* smem, const PanelCol* pcd,
+                                                 int c_begin, int NC, int s, int inst, int r0, double* Qo,
+                                                 int c_lo, unsigned long long* prof = nullptr) {
+  __shared__ unsigned long long bars[1 + PB_NB_MAX];   // [0] V, [1..NB] chunk slots "full"
+  __shared__ int cnt[PB_NB_MAX];                        // warps done with a chunk slot
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31, gid = lane >> 2, tig = lane & 3;
+  const TreeDev& tr = a.tree;
+  const int L = tr.L, NV = NC - 1, MP = (NV + 15) >> 4;
+  constexpr int LDV = LEAF_LDV, CW = 16;
+  const int NCOL = NC - c_lo, NCH = (NCOL + CW - 1) / CW;
+  if (!a.lmap || !a.xmap || (s & 31) || s > LEAF_MAX || NCOL < 1 || L < 1) return false;
+  long long ph_t = clock64();
+  const bool pw = prof && t == 32;                    // (debug: warp 1's phase clocks)
+  auto ph = [&](int i) {
+    if (pw) { const long long t_ = clock64(); atomicAdd(prof + i, (unsigned long long)(t_ - ph_t)); ph_t = t_; }
+  };
+  // shared layout: colofs (ints) in the front scratch; V level blocks after the descriptors
+  int* colofs = reinterpret_cast<int*>(smem);
+  // (offsets from the dynamic shared array itself, so that the loads below stay LDS)
+  int voff = (int)(reinterpret_cast<const double*>(pcd + (NC - c_begin)) - smem);
+  voff += (int)(((128u - ((smem_u32(smem) + 8u * (unsigned)voff) & 127u)) & 127u) >> 3);
+  double* Vs = smem + voff;
+  auto lev_block = [&](int l) { return round_up(a.kl[l] * LDV, 16); };
+  int vtot = 0;
+  for (int l = 0; l < L; ++l) vtot += lev_block(l);
+  double* Xb = Vs + vtot;
+  const int NB = min(PB_NB_MAX, (int)((smem + LEAF_FRONT + LEAF_BIG - Xb) / (CW * LDV)));
+  if (NB < 2) return false;
+  for (int j = t; j < NV; j += LEAF_THREADS) {        // V column j = X column j + 1
+    int l = 0, o = 0;
+    while (l + 1 < L && a.xcol[l + 1] - 1 <= j) { o += lev_block(l); ++l; }
+    colofs[j] = o + (j - (a.xcol[l] - 1)) * LDV;
+  }
+  const unsigned xbytes = CW * LDV * 8;
+  auto issue_chunk = [&](int c) {                     // (lane 0 of the issuing warp)
+    unsigned long long* fb = bars + 1 + (c % NB);
+    mbar_expect_tx(fb, xbytes);
+    tma_load_3d(Xb + (c % NB) * CW * LDV, a.xmap, r0, c_lo + c * CW, inst, fb);
+  };
+  if (warp == 0) {
+    // the previous task's generic accesses of this shared memory, and X (written by other CTAs,
+    // acquired by the scheduler), ordered before the TMA (async proxy)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    const int rl = lane < L ? a.rank[inst * L + lane] : 0;
+    int vbytes = rl * LDV * 8;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) vbytes += __shfl_xor_sync(0xffffffffu, vbytes, o);
+    if (lane == 0) {
+      for (int i = 0; i < 1 + PB_NB_MAX; ++i) mbar_init(bars + i, 1u);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_expect_tx(bars, (unsigned)vbytes);
+    }
+    __syncwarp();
+    if (rl > 0) {                                     // lane l: the kind-2 columns of level l
+      int o = 0;
+      for (int l = 0; l < lane; ++l) o += lev_block(l);
+      const PanelCol pc = pcd[a.xcol[lane] - c_begin];
+      const int row0 = pc.lstep < 0 ? pc.li0 - (s - 1) : pc.li0;
+      tma_load_2d(Vs + o, static_cast<const CUtensorMapLike*>(a.lmap) + (inst * L + lane), row0, 0, bars);
+    }
+    if (lane == 0)
+      for (int c = 0; c < min(NB, NCH); ++c) issue_chunk(c);
+  } else if (t >= 32 && t < 32 + PB_NB_MAX) {
+    cnt[t - 32] = 0;
+  }
+  __syncthreads();                                    // (colofs complete)
+  // exact / padding V columns: warp per column, lanes over rows (columns the TMA does not touch)
+  for (int j = warp; j < NV; j += LEAF_WARPS) {
+    const PanelCol pc = pcd[j + 1 - c_begin];
+    if (pc.kind != 2)
+      for (int i = lane; i < s; i += 32) Vs[colofs[j] + i] = (pc.kind == 3 && pc.li0 + pc.lstep * i == 0) ? 1.0 : 0.0;
+  }
+  ph(4);
+  mbar_wait(bars, 0);
+  ph(5);
+  // child-0 runs arrived forward: reverse them in place (warp per column, lanes over pairs)
+  for (int j = warp; j < NV; j += LEAF_WARPS) {
+    const PanelCol pc = pcd[j + 1 - c_begin];
+    if (pc.kind == 2 && pc.lstep < 0) {
+      double* col = Vs + colofs[j];
+      for (int i = lane; i < (s >> 1); i += 32) {
+        const double x = col[i], y = col[s - 1 - i];
+        col[i] = y; col[s - 1 - i] = x;
+      }
+    }
+  }
+  __syncthreads();
+  for (int c = 0; c < NCH; ++c) {
+    ph(6);
+    mbar_wait(bars + 1 + c % NB, (c / NB) & 1);
+    ph(7);
+    const double* Xs = Xb + (c % NB) * CW * LDV;
+    const int col0 = c_lo + c * CW;
+    for (int mp = (warp - 1 - (c * MP) % LEAF_WARPS + 2 * LEAF_WARPS) % LEAF_WARPS; mp < MP; mp += LEAF_WARPS) {
+      const int j0 = 16 * mp + gid, j1 = j0 + 8;
+      const double* ap0 = Vs + colofs[j0 < NV ? j0 : 0] + tig;
+      const double* ap1 = Vs + colofs[j1 < NV ? j1 : 0] + tig;
+      const double* bp0 = Xs + gid * LDV + tig;
+      const double* bp1 = bp0 + 8 * LDV;
+      double d[2][2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};
+#pragma unroll 4
+      for (int k0 = 0; k0 < s; k0 += 4) {
+        const double a0 = ap0[k0], a1 = ap1[k0], b0 = bp0[k0], b1 = bp1[k0];
+        dmma884(d[0][0][0], d[0][0][1], a0, b0);
+        dmma884(d[0][1][0], d[0][1][1], a0, b1);
+        dmma884(d[1][0][0], d[1][0][1], a1, b0);
+        dmma884(d[1][1][0], d[1][1][1], a1, b1);
+      }
+#pragma unroll
+      for (int hm = 0; hm < 2; ++hm) {
+        const int j = 16 * mp + 8 * hm + gid;
+        if (j < NV) {
+          double* qr = Qo + (long long)j * NC;
+#pragma unroll
+          for (int hn = 0; hn < 2; ++hn) {
+            const int cc = col0 + 8 * hn + 2 * tig;
+            if (cc < NC) qr[cc] = d[hm][hn][0];
+            if (cc + 1 < NC) qr[cc + 1] = d[hm][hn][1];
+          }
+        }
+      }
+    }
+    // the last warp done with this slot refills it with chunk c + NB
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      if (atomicAdd(&cnt[c % NB], 1) == LEAF_WARPS - 1 && c + NB < NCH) {
+        cnt[c % NB] = 0;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue_chunk(c + NB);
+      }
+    }
+  }
+  ph(6);
+  __syncthreads();                                    // (smem and barriers free for the next task)
+  ph(8);
+  if (pw) atomicAdd(prof + 3, 1ULL);
+  if (t == 0)
+    for (int i = 0; i < 1 + PB_NB_MAX; ++i) mbar_inval(bars + i);
+  return true;
+}
+
 // COOP: solve a last round of 1-2 stripes with 4-warp groups (k_run; the extra call raises the
 // register pressure of the fused k_step kernel into spills, so it stays off there)
 template <bool COOP = false>
@@ -879,7 +1053,10 @@ __device__ __forceinline__ void leaf_proj_task(const LeafArgs& a, double* smem, 
   for (int cc = threadIdx.x; cc < c_end - c_begin; cc += LEAF_THREADS)
     pcd[cc] = panel_col(a, inst, leaf, r0, c_begin + cc, c_end);
   const double* Xi = a.X + (long long)inst * a.xstride + r0;
-  leaf_project(a, smem + LEAF_FRONT, pcd, c_begin, c_end, s, sp, Xi,
-               a.Q + (long long)inst * a.qinst + (long long)leaf * a.qstride, c_begin,
+  double* Qo = a.Q + (long long)inst * a.qinst + (long long)leaf * a.qstride;
+  __syncthreads();                                    // (descriptors visible)
+  if (leaf_project_tma(a, smem, pcd, c_begin, c_end, s, inst, r0, Qo, c_begin, a.prof ? a.prof + 8 : nullptr))
+    return;
+  leaf_project(a, smem + LEAF_FRONT, pcd, c_begin, c_end, s, sp, Xi, Qo, c_begin,
                a.prof ? a.prof + 8 : nullptr);
 }

@@ -74,6 +74,35 @@ __global__ void k1688(double* out, int iters, long long* cyc) {
   if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
+template <int ACC>
+__global__ void k16816(double* out, int iters, long long* cyc) {
+  double a[8], b[4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = threadIdx.x * 1e-9 + 0.125 * i;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) b[i] = 0.5 + 0.25 * i;
+  double d[ACC][4];
+#pragma unroll
+  for (int k = 0; k < ACC; ++k) { d[k][0] = 0; d[k][1] = 0; d[k][2] = 0; d[k][3] = 0; }
+  __syncthreads();
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < ACC; ++k)
+      asm volatile("mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7,%8,%9,%10,%11}, {%12,%13,%14,%15}, {%0,%1,%2,%3};"
+                   : "+d"(d[k][0]), "+d"(d[k][1]), "+d"(d[k][2]), "+d"(d[k][3])
+                   : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]),
+                     "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < ACC; ++k) s += d[k][0] + d[k][1] + d[k][2] + d[k][3];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
 __global__ void kshfl(double* out, int iters, long long* cyc) {
   double v = threadIdx.x;
   __syncthreads();
@@ -141,6 +170,12 @@ int main() {
            c8 = run(k1688<8>, w, it, out, cyc, nsm);
     printf("m16n8k8 warps %2d: acc1 %.1f (lat) acc4 %.1f acc8 %.1f | flop/clk/SM acc4 %.1f acc8 %.1f\n",
            w, c1, c4, c8, 2048.0 * 4 * w / c4, 2048.0 * 8 * w / c8);
+  }
+  for (int w : ws) {
+    double c1 = run(k16816<1>, w, it, out, cyc, nsm), c2 = run(k16816<2>, w, it, out, cyc, nsm),
+           c4 = run(k16816<4>, w, it, out, cyc, nsm);
+    printf("m16n8k16 warps %2d: acc1 %.1f (lat) acc2 %.1f acc4 %.1f | flop/clk/SM acc1 %.1f acc2 %.1f acc4 %.1f\n",
+           w, c1, c2, c4, 4096.0 * w / c1, 4096.0 * 2 * w / c2, 4096.0 * 4 * w / c4);
   }
   printf("shfl f64 dependent latency: %.1f cycles\n", run(kshfl, 1, it, out, cyc, nsm));
   printf("lds f64 dependent latency: %.1f cycles\n", run(klds, 1, it, out, cyc, nsm));
