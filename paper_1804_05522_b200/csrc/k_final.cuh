@@ -35,13 +35,32 @@ __device__ void leaf_rhs_final(const TrArgs& geo, const TrArgs* tp, const LeafAr
   double* zs = part + 4 * LEAF_MAX;                   // [32]
   double* LUs = sm + RN_FRONT;                        // [sp x sp] column-major, ld = sp
   double* Ss = LUs + LEAF_MAX * LEAF_MAX;             // S_side blocks of a batch of levels
-  PanelCol* pcd = reinterpret_cast<PanelCol*>(Ss);   // then: V-column descriptors (NC - 1)
   const int scap = smem_doubles - RN_FRONT - LEAF_MAX * LEAF_MAX;
   FDE_ASSERT(s >= 1 && s <= LEAF_MAX && NC <= NCOL_MAX && scap > 0 && r0 + s <= n);
-  // ---- the first batch of S blocks, then the stored LU, in flight while the final is formed
+  // ---- the first batch of S blocks, then the stored LU, in flight while the final is formed.
+  //      The LU (one contiguous 8 sp^2-byte run) is one bulk copy of the TMA engine (mbarrier
+  //      rn_bar[0]) when the run is 16-byte aligned, else cp.async.
+  __shared__ unsigned long long rn_bar[1];
+  const double* LUg = la ? la->LU + (long long)inst * la->lustride + (long long)leaf * LEAF_SLOT : nullptr;
+  const bool lu_bulk = la && (reinterpret_cast<unsigned long long>(LUg) & 15) == 0;
+  if (la && t == 0) {
+    mbar_init(rn_bar, 1u);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   auto issue_lu = [&]() {
-    const double* LUg = la->LU + (long long)inst * la->lustride + (long long)leaf * LEAF_SLOT;
-    for (int e = 2 * t; e < sp * sp; e += 2 * LEAF_THREADS) cp_async16(LUs + e, LUg + e);
+    if (lu_bulk) {
+      if (t == 0) {
+        // the previous task's generic accesses of this shared memory, and the LU (written by
+        // another CTA, acquired by the scheduler), ordered before the async-proxy copy
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        mbar_expect_tx(rn_bar, (unsigned)(sp * sp * 8));
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(smem_u32(LUs)), "l"(LUg), "r"((unsigned)(sp * sp * 8)), "r"(smem_u32(rn_bar)) : "memory");
+      }
+    } else {
+      for (int e = 2 * t; e < sp * sp; e += 2 * LEAF_THREADS) cp_async16(LUs + e, LUg + e);
+    }
     cp_async_commit();
   };
   if (tp) {
@@ -161,6 +180,7 @@ __device__ void leaf_rhs_final(const TrArgs& geo, const TrArgs* tp, const LeafAr
   if (!la) return;
   if (t >= s && t < sp) bs[t] = 0.0;
   cp_async_wait_all();
+  if (lu_bulk) mbar_wait(rn_bar, 0);
   __syncthreads();
   RN_PH(4);
   // ---- x0 = A_leaf^{-1} b with the stored LU (k_leaf.cuh inverse-diagonal form: off-diagonal
@@ -196,9 +216,10 @@ __device__ void leaf_rhs_final(const TrArgs& geo, const TrArgs* tp, const LeafAr
   RN_PH(5);
   double* X0 = la->X + (long long)inst * la->xstride + r0;
   if (t < s) X0[t] = bs[t];
-  for (int j = t; j < NC - 1; j += LEAF_THREADS) pcd[j] = panel_col(*la, inst, leaf, r0, 1 + j, NC);
+  PanelCol* pcq = reinterpret_cast<PanelCol*>(Ss);   // V-column descriptors (NC - 1)
+  for (int j = t; j < NC - 1; j += LEAF_THREADS) pcq[j] = panel_col(*la, inst, leaf, r0, 1 + j, NC);
   __syncthreads();
-  // ---- Q[j][0] = V_all[:, j]^T x0: a warp per 4 V columns, lanes over rows (fixed order)
+  // ---- Q[j][0] = V_all[:, j]^T x0: a warp per QG V columns, lanes over rows (fixed order)
   double* Qo = la->Q + (long long)inst * la->qinst + (long long)leaf * la->qstride;
   double xr[LEAF_MAX / 32];
 #pragma unroll
@@ -208,7 +229,7 @@ __device__ void leaf_rhs_final(const TrArgs& geo, const TrArgs* tp, const LeafAr
     double vv[QG][LEAF_MAX / 32];
 #pragma unroll
     for (int jj = 0; jj < QG; ++jj) {
-      const PanelCol pc = j0 + jj < NC - 1 ? pcd[j0 + jj] : PanelCol{la->Lf, 0, 0, 0, 0, 0};
+      const PanelCol pc = j0 + jj < NC - 1 ? pcq[j0 + jj] : PanelCol{la->Lf, 0, 0, 0, 0, 0};
 #pragma unroll
       for (int q = 0; q < LEAF_MAX / 32; ++q) {
         const int r = lane + 32 * q, rc = r < s ? r : s - 1;
@@ -226,6 +247,8 @@ __device__ void leaf_rhs_final(const TrArgs& geo, const TrArgs* tp, const LeafAr
       if (lane == 0 && j0 + jj < NC - 1) Qo[(long long)(j0 + jj) * NC] = v;
     }
   }
+  __syncthreads();                                    // (barriers and shared memory free)
+  if (t == 0) mbar_inval(rn_bar);
   if (prof) { __syncthreads(); RN_PH(0); }
 }
 
