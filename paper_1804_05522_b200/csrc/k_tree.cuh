@@ -189,6 +189,45 @@ __device__ __noinline__ void tr_warp_gj(const double* M, double* Mi, int ldm, in
       if (c < k) Mi[r * ldm + c] = row[c];
 }
 
+// One warp's share of a TR_SUB-row sub-chunk of the node update (tr_unit step 5): m-tile
+// warp % TR_MW, n-tiles warp / TR_MW + TR_NS i (i < NTI, all with columns < xm):
+//   Q_mu[r][c] = U1[r][c] + U2[r][c] - sum_q [U1 m-cols | U2 m-cols][r][q] S[q][c].
+template <int NTI>
+__device__ __forceinline__ void tr_upd_tiles(const double* U1, const double* U2, const double* Ss, double* Qo,
+                                             int rs, int nr, int ncol1, int xm, int k, int K4, int lds) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gid = lane >> 2, tig = lane & 3;
+  const int mt = warp % TR_MW, nt0 = warp / TR_MW;
+  const int r = 8 * mt + gid;
+  const bool rok = r < nr;
+  if (8 * mt >= nr) return;
+  double d[NTI][2];
+#pragma unroll
+  for (int i = 0; i < NTI; ++i) {
+    const int c = 8 * (nt0 + TR_NS * i) + 2 * tig;
+    d[i][0] = (rok && c < xm) ? U1[r * ncol1 + c] + U2[r * ncol1 + c] : 0.0;
+    d[i][1] = (rok && c + 1 < xm) ? U1[r * ncol1 + c + 1] + U2[r * ncol1 + c + 1] : 0.0;
+  }
+  const double* bp = Ss + tig * lds + 8 * nt0 + gid;
+  const double* u1 = U1 + r * ncol1 + xm;
+  const double* u2 = U2 + r * ncol1 + xm - k;
+#pragma unroll 4
+  for (int k0 = 0; k0 < K4; k0 += 4) {
+    const int q = k0 + tig;                          // A = -[U1 m-cols | U2 m-cols] (zero padded)
+    const double av = (rok && q < 2 * k) ? -(q < k ? u1[q] : u2[q]) : 0.0;
+#pragma unroll
+    for (int i = 0; i < NTI; ++i) dmma884(d[i][0], d[i][1], av, bp[k0 * lds + 8 * TR_NS * i]);
+  }
+  if (rok) {
+    double* qr = Qo + (long long)(rs + r) * xm;
+#pragma unroll
+    for (int i = 0; i < NTI; ++i) {
+      const int c = 8 * (nt0 + TR_NS * i) + 2 * tig;
+      if (c < xm) qr[c] = d[i][0];
+      if (c + 1 < xm) qr[c + 1] = d[i][1];
+    }
+  }
+}
+
 // One (node, row chunk) unit of level m.  All global reads are asynchronous copies into
 // shared memory (cp.async), so the latency of L2/HBM is paid once per stage, not per load.
 __device__ void tr_unit(const TrArgs& a, double* sm, int inst, int m, int j, int chunk) {
@@ -322,53 +361,90 @@ __device__ void tr_unit(const TrArgs& a, double* sm, int inst, int m, int j, int
   TPH(3);
   if (nsub == 0) { __syncthreads(); return; }
   // 5. Q_mu rows [ra, rb) = Q1 + Q2 - [Q1 m-cols | Q2 m-cols] [S_top; S_bot], streamed in
-  //    sub-chunks of TR_SUB rows (TR_STG - 1 sub-chunks' copies in flight during one's DMMA)
+  //    sub-chunks of TR_SUB rows.  Warp -> m-tile (warp % TR_MW) x n-tiles (warp / TR_MW) +
+  //    TR_NS i: A fragment reused TR_NT times.
   double* Qo = a.Q + (long long)inst * a.qinst + a.qlev[m] + (long long)j * (long long)nrow * xm;
-  for (int sc = 0; sc < TR_STG - 1 && sc < nsub; ++sc) issue_sub(sc);
-  for (int sc = 0; sc < nsub; ++sc) {
-    if (sc + TR_STG - 1 < nsub) issue_sub(sc + TR_STG - 1);
-    TPH(5);                                            // (issue)
-    const int ahead = min(TR_STG - 1, nsub - 1 - sc);   // groups allowed to stay in flight
-    if (ahead >= 3) asm volatile("cp.async.wait_group 3;" ::: "memory");
-    else if (ahead == 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
-    else if (ahead == 1) cp_async_wait_group1();
-    else cp_async_wait_all();
+  // valid n-tiles of this warp (cols < xm): a warp-uniform trip count, so the DMMA loop has no
+  // per-instruction predicate (a predicated mma.sync costs a WARPSYNC each)
+  const int nti = max(0, min(TR_NT, ((xm + 7) / 8 - warp / TR_MW + TR_NS - 1) / TR_NS));
+  auto update = [&](const double* U1, const double* U2, int rs, int nr) {
+    switch (nti) {
+      case 6: tr_upd_tiles<6>(U1, U2, Ss, Qo, rs, nr, ncol1, xm, k, K4, lds); break;
+      case 5: tr_upd_tiles<5>(U1, U2, Ss, Qo, rs, nr, ncol1, xm, k, K4, lds); break;
+      case 4: tr_upd_tiles<4>(U1, U2, Ss, Qo, rs, nr, ncol1, xm, k, K4, lds); break;
+      case 3: tr_upd_tiles<3>(U1, U2, Ss, Qo, rs, nr, ncol1, xm, k, K4, lds); break;
+      case 2: tr_upd_tiles<2>(U1, U2, Ss, Qo, rs, nr, ncol1, xm, k, K4, lds); break;
+      case 1: tr_upd_tiles<1>(U1, U2, Ss, Qo, rs, nr, ncol1, xm, k, K4, lds); break;
+      default: break;
+    }
+  };
+  // TMA-engine path: each sub-chunk's Q1 / Q2 rows are one contiguous run (rounded up to an
+  // even count of doubles: the extra one stays inside the child Q) -> two bulk copies into a
+  // ring slot with an mbarrier; the last warp done with a slot refills it (no CTA barrier).
+  __shared__ unsigned long long qbar[TR_STG];
+  __shared__ int qcnt[TR_STG];
+  const bool qbulk = ((reinterpret_cast<unsigned long long>(Q1) | reinterpret_cast<unsigned long long>(Q2) |
+                       reinterpret_cast<unsigned long long>(Ub)) & 15) == 0 && (ra & 1) == 0 && TR_SUB % 2 == 0;
+  if (qbulk) {
+    auto issue_b = [&](int sc) {                      // (one thread)
+      const int rs = ra + sc * TR_SUB, nr = min(TR_SUB, rb - rs);
+      const unsigned bytes = (unsigned)round_up(nr * ncol1, 2) * 8u;
+      double* dst = Ub + (sc % TR_STG) * 2 * usz;
+      mbar_expect_tx(qbar + sc % TR_STG, 2 * bytes);
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(smem_u32(dst)), "l"(Q1 + (long long)rs * ncol1), "r"(bytes), "r"(smem_u32(qbar + sc % TR_STG)) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(smem_u32(dst + usz)), "l"(Q2 + (long long)rs * ncol1), "r"(bytes), "r"(smem_u32(qbar + sc % TR_STG)) : "memory");
+    };
+    if (t == 0) {
+      for (int i = 0; i < TR_STG; ++i) mbar_init(qbar + i, 1u);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      // (generic accesses of the aliased staging buffers, and Q written by other CTAs, before
+      //  the async-proxy copies)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      for (int sc = 0; sc < TR_STG && sc < nsub; ++sc) issue_b(sc);
+    } else if (t >= 32 && t < 32 + TR_STG) {
+      qcnt[t - 32] = 0;
+    }
     __syncthreads();
-    TPH(6);                                            // (wait)
-    const int rs = ra + sc * TR_SUB, nr = min(TR_SUB, rb - rs);
-    const double* U1 = ubuf(sc, 0);
-    const double* U2 = ubuf(sc, 1);
-    // warp -> m-tile (warp % TR_MW) x n-tiles (warp / TR_MW) + TR_NS i: A fragment reused TR_NT times
-    const int mt = warp % TR_MW, nt0 = warp / TR_MW, NT8 = xmp >> 3;
-    const int r = 8 * mt + gid;
-    const bool rok = r < nr;
-    if (8 * mt < nr) {
-      double d[TR_NT][2];
-#pragma unroll
-      for (int i = 0; i < TR_NT; ++i) {
-        const int c = 8 * (nt0 + TR_NS * i) + 2 * tig;
-        d[i][0] = (rok && c < xm) ? U1[r * ncol1 + c] + U2[r * ncol1 + c] : 0.0;
-        d[i][1] = (rok && c + 1 < xm) ? U1[r * ncol1 + c + 1] + U2[r * ncol1 + c + 1] : 0.0;
-      }
-      const double* bp = Ss + tig * lds + 8 * nt0 + gid;
-      for (int k0 = 0; k0 < K4; k0 += 4) {
-        const int q = k0 + tig;                    // A = -[U1 m-cols | U2 m-cols] (zero padded)
-        const double av = (rok && q < 2 * k) ? -(q < k ? U1[r * ncol1 + xm + q] : U2[r * ncol1 + xm + q - k]) : 0.0;
-#pragma unroll
-        for (int i = 0; i < TR_NT; ++i)
-          if (nt0 + TR_NS * i < NT8) dmma884(d[i][0], d[i][1], av, bp[k0 * lds + 8 * TR_NS * i]);
-      }
-      if (rok) {
-        double* qr = Qo + (long long)(rs + r) * xm;
-#pragma unroll
-        for (int i = 0; i < TR_NT; ++i) {
-          const int c = 8 * (nt0 + TR_NS * i) + 2 * tig;
-          if (c < xm) qr[c] = d[i][0];
-          if (c + 1 < xm) qr[c + 1] = d[i][1];
+    for (int sc = 0; sc < nsub; ++sc) {
+      mbar_wait(qbar + sc % TR_STG, (sc / TR_STG) & 1);
+      TPH(6);                                            // (wait)
+      const int rs = ra + sc * TR_SUB;
+      const double* U1 = Ub + (sc % TR_STG) * 2 * usz;
+      update(U1, U1 + usz, rs, min(TR_SUB, rb - rs));
+      TPH(5);                                            // (update)
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();
+        if (atomicAdd(&qcnt[sc % TR_STG], 1) == TR_WARPS - 1 && sc + TR_STG < nsub) {
+          qcnt[sc % TR_STG] = 0;
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue_b(sc + TR_STG);
         }
       }
     }
     __syncthreads();
+    if (t == 0)
+      for (int i = 0; i < TR_STG; ++i) mbar_inval(qbar + i);
+  } else {
+    // cp.async pipeline (TR_STG - 1 sub-chunks' copies in flight during one's DMMA)
+    for (int sc = 0; sc < TR_STG - 1 && sc < nsub; ++sc) issue_sub(sc);
+    for (int sc = 0; sc < nsub; ++sc) {
+      if (sc + TR_STG - 1 < nsub) issue_sub(sc + TR_STG - 1);
+      TPH(5);                                            // (issue)
+      const int ahead = min(TR_STG - 1, nsub - 1 - sc);   // groups allowed to stay in flight
+      if (ahead >= 3) asm volatile("cp.async.wait_group 3;" ::: "memory");
+      else if (ahead == 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
+      else if (ahead == 1) cp_async_wait_group1();
+      else cp_async_wait_all();
+      __syncthreads();
+      TPH(6);                                            // (wait)
+      const int rs = ra + sc * TR_SUB;
+      update(ubuf(sc, 0), ubuf(sc, 1), rs, min(TR_SUB, rb - rs));
+      __syncthreads();
+    }
   }
   TPH(4);
 #undef TPH
