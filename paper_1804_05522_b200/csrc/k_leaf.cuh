@@ -79,39 +79,49 @@ __device__ __forceinline__ bool gj_role(int warp) { return SPLIT ? (warp & 2) ==
 template <bool SPLIT>
 __device__ __forceinline__ int role_idx(int warp) { return SPLIT ? (warp & 1) | ((warp >> 2) << 1) : warp & 3; }
 
-template <bool ADD = false>
+// A predicated mma.sync costs the warp a WARPSYNC + branch per instruction, so the DMMA loops
+// below run a warp-uniform, compile-time number of tiles; only loads / stores are guarded.
+// The skip block (skip_m0 = skip_n0 = 0: the leading 32 x 32 tiles, already updated by the
+// lookahead) is left out of the tile enumeration.
+template <bool ADD = false, int U = 4>
 __device__ __forceinline__ void cm_gemm_sub(double* C, int ldc, const double* A, int lda,
                                             const double* B, int ldb, int M, int N, int K, int w0,
                                             int nw, int skip_m0 = -1, int skip_n0 = -1) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, gid = lane >> 2, tig = lane & 3;
   const int w = warp - w0;
   if (w < 0 || w >= nw) return;
-  const int MB = M >> 3, NT = MB * (N >> 3);
-  for (int t0 = w; t0 < NT; t0 += 4 * nw) {
-    double d[4][2];
-    int mo[4], no[4];
-    bool ok[4];
+  FDE_ASSERT(skip_m0 < 0 || (skip_m0 == 0 && skip_n0 == 0 && M >= 32 && N >= 32));
+  const int MB = M >> 3, NB8 = N >> 3;
+  const bool skip = skip_m0 >= 0;
+  const int ns = skip ? 4 * (MB - 4) : 0;            // tiles of the first 4 n-tiles (below the skip)
+  const int NT = MB * NB8 - (skip ? 16 : 0);
+  auto tile = [&](int t, int& mo, int& no) {
+    if (t < ns) { no = (t / (MB - 4)) * 8; mo = (4 + t % (MB - 4)) * 8; }
+    else { const int t2 = t - ns; no = ((skip ? 4 : 0) + t2 / MB) * 8; mo = (t2 % MB) * 8; }
+  };
+  for (int t0 = w; t0 < NT; t0 += U * nw) {
+    double d[U][2];
+    const double* ap[U];
+    const double* bp[U];
+    bool ok[U];
+    int mo[U], no[U];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int t = t0 + u * nw;
-      mo[u] = (t % MB) * 8; no[u] = (t / MB) * 8;
-      ok[u] = t < NT && !(skip_m0 >= 0 && mo[u] >= skip_m0 && mo[u] < skip_m0 + 32 &&
-                          no[u] >= skip_n0 && no[u] < skip_n0 + 32);
-      if (ok[u]) {
-        d[u][0] = C[mo[u] + gid + (no[u] + 2 * tig) * ldc];
-        d[u][1] = C[mo[u] + gid + (no[u] + 2 * tig + 1) * ldc];
-      }
+      ok[u] = t < NT;
+      tile(ok[u] ? t : t0, mo[u], no[u]);             // (a valid tile for the unused slots)
+      d[u][0] = ok[u] ? C[mo[u] + gid + (no[u] + 2 * tig) * ldc] : 0.0;
+      d[u][1] = ok[u] ? C[mo[u] + gid + (no[u] + 2 * tig + 1) * ldc] : 0.0;
+      ap[u] = A + mo[u] + gid + tig * lda;
+      bp[u] = B + tig + (no[u] + gid) * ldb;
     }
     for (int k0 = 0; k0 < K; k0 += 4) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (ok[u])
-          dmma884(d[u][0], d[u][1], ADD ? A[mo[u] + gid + (k0 + tig) * lda]
-                                         : -A[mo[u] + gid + (k0 + tig) * lda],
-                  B[k0 + tig + (no[u] + gid) * ldb]);
+      for (int u = 0; u < U; ++u)
+        dmma884(d[u][0], d[u][1], ADD ? ap[u][k0 * lda] : -ap[u][k0 * lda], bp[u][k0]);
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < U; ++u)
       if (ok[u]) {
         C[mo[u] + gid + (no[u] + 2 * tig) * ldc] = d[u][0];
         C[mo[u] + gid + (no[u] + 2 * tig + 1) * ldc] = d[u][1];
@@ -127,11 +137,21 @@ struct OvwTiles {
   int cnt;
 };
 
+template <int CNT>
+__device__ __forceinline__ void ovw_mma(OvwTiles& T, const double* A, int lda, const double* B, int ldb, int K) {
+  const int lane = threadIdx.x & 31, gid = lane >> 2, tig = lane & 3;
+  for (int k0 = 0; k0 < K; k0 += 4) {
+#pragma unroll
+    for (int u = 0; u < CNT; ++u)
+      dmma884(T.d[u][0], T.d[u][1], A[T.mo[u] + gid + (k0 + tig) * lda], B[k0 + tig + (T.no[u] + gid) * ldb]);
+  }
+}
+
 // tiles over the rows [r_lo, r_hi) and [r2_lo, r2_hi) (two row ranges) x N columns
 __device__ __forceinline__ void ovw_compute(OvwTiles& T, const double* A, int lda, const double* B,
                                             int ldb, int r_lo, int r_hi, int r2_lo, int r2_hi, int N,
                                             int K) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, gid = lane >> 2, tig = lane & 3;
+  const int warp = threadIdx.x >> 5;
   const int M1 = (r_hi - r_lo) >> 3, M2 = (r2_hi - r2_lo) >> 3, MB = M1 + M2;
   const int NT = MB * (N >> 3);
   T.cnt = 0;
@@ -144,12 +164,16 @@ __device__ __forceinline__ void ovw_compute(OvwTiles& T, const double* A, int ld
     T.d[u][0] = 0.0; T.d[u][1] = 0.0;
     if (t < NT) T.cnt = u + 1;
   }
-  for (int k0 = 0; k0 < K; k0 += 4) {
-#pragma unroll
-    for (int u = 0; u < LEAF_OVW; ++u)
-      if (u < T.cnt)
-        dmma884(T.d[u][0], T.d[u][1], A[T.mo[u] + gid + (k0 + tig) * lda],
-                B[k0 + tig + (T.no[u] + gid) * ldb]);
+  switch (T.cnt) {                                   // (warp-uniform)
+    case 8: ovw_mma<8>(T, A, lda, B, ldb, K); break;
+    case 7: ovw_mma<7>(T, A, lda, B, ldb, K); break;
+    case 6: ovw_mma<6>(T, A, lda, B, ldb, K); break;
+    case 5: ovw_mma<5>(T, A, lda, B, ldb, K); break;
+    case 4: ovw_mma<4>(T, A, lda, B, ldb, K); break;
+    case 3: ovw_mma<3>(T, A, lda, B, ldb, K); break;
+    case 2: ovw_mma<2>(T, A, lda, B, ldb, K); break;
+    case 1: ovw_mma<1>(T, A, lda, B, ldb, K); break;
+    default: break;
   }
 }
 
@@ -280,7 +304,7 @@ __device__ void leaf_block_lu(double* A, int sp, double* prow, DevStatus* st, in
       double* Akk = A + k1 + k1 * LDA_LEAF;
       const double* Lk = A + k1 + k0 * LDA_LEAF;
       const double* Uk = A + k0 + k1 * LDA_LEAF;
-      cm_gemm_sub<true>(Akk, LDA_LEAF, Lk, LDA_LEAF, Uk, LDA_LEAF, 32, 32, 32, 0, LEAF_WARPS);
+      cm_gemm_sub<true, 2>(Akk, LDA_LEAF, Lk, LDA_LEAF, Uk, LDA_LEAF, 32, 32, 32, 0, LEAF_WARPS);
       __syncthreads();
       LUT(2);
 #ifdef FDE_LU_SERIAL
@@ -335,8 +359,8 @@ __device__ __forceinline__ void stripe_solve(double (&acc)[16][2], const double*
         const double b = Ys[4 * k4 + tig + gid * YLD];
         const double* Ak = A + (kb * 32 + 4 * k4 + tig) * LDA_LEAF + gid;
 #pragma unroll
-        for (int t = 4 * (kb + 1); t < 16; ++t)
-          if (t < 4 * nb) dmma884(acc[t][0], acc[t][1], Ak[8 * t], b);
+        for (int t = 4 * (kb + 1); t < 16; ++t)      // (tiles >= 4 nb: unused accumulators)
+          dmma884(acc[t][0], acc[t][1], Ak[8 * t], b);
       }
       __syncwarp();
     }
@@ -625,6 +649,21 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const void* map, int c0, 
                ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)) : "memory");
 }
 
+// 2 x 2 DMMA tiles of the projection over K = S (S = 0: runtime K = s)
+template <int S>
+__device__ __forceinline__ void proj_tile2x2(double (&d)[2][2][2], const double* ap0, const double* ap1,
+                                             const double* bp0, const double* bp1, int s) {
+  const int K = S ? S : s;
+#pragma unroll 8
+  for (int k0 = 0; k0 < K; k0 += 4) {
+    const double a0 = ap0[k0], a1 = ap1[k0], b0 = bp0[k0], b1 = bp1[k0];
+    dmma884(d[0][0][0], d[0][0][1], a0, b0);
+    dmma884(d[0][1][0], d[0][1][1], a0, b1);
+    dmma884(d[1][0][0], d[1][0][1], a1, b0);
+    dmma884(d[1][1][0], d[1][1][1], a1, b1);
+  }
+}
+
 __device__ __forceinline__ bool leaf_project_tma(const LeafArgs& a, double* smem, const PanelCol* pcd,
                                                  int c_begin, int NC, int s, int inst, int r0, double* Qo,
                                                  int c_lo, unsigned long long* prof = nullptr) {
@@ -726,14 +765,8 @@ __device__ __forceinline__ bool leaf_project_tma(const LeafArgs& a, double* smem
       const double* bp0 = Xs + gid * LDV + tig;
       const double* bp1 = bp0 + 8 * LDV;
       double d[2][2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};
-#pragma unroll 4
-      for (int k0 = 0; k0 < s; k0 += 4) {
-        const double a0 = ap0[k0], a1 = ap1[k0], b0 = bp0[k0], b1 = bp1[k0];
-        dmma884(d[0][0][0], d[0][0][1], a0, b0);
-        dmma884(d[0][1][0], d[0][1][1], a0, b1);
-        dmma884(d[1][0][0], d[1][0][1], a1, b0);
-        dmma884(d[1][1][0], d[1][1][1], a1, b1);
-      }
+      if (s == LEAF_MAX) proj_tile2x2<LEAF_MAX>(d, ap0, ap1, bp0, bp1, s);   // (compile-time trip count)
+      else proj_tile2x2<0>(d, ap0, ap1, bp0, bp1, s);
 #pragma unroll
       for (int hm = 0; hm < 2; ++hm) {
         const int j = 16 * mp + 8 * hm + gid;
@@ -887,8 +920,9 @@ __device__ __forceinline__ void leaf_task(const LeafArgs& a, double* smem, int l
     const int nstripe = (c_end - c_begin + 7) >> 3;
     double* Xi = a.X + (long long)inst * a.xstride + r0;
     const bool ptr = a.trace && t == 0 && leaf == 0 && inst == 0;
-    long long pt0 = clock64();
-#define PTR(i) do { if (ptr) { const long long t_ = clock64(); a.trace[970 + (i)] += t_ - pt0; pt0 = t_; } } while (0)
+    long long pt0 = clock64(), pt1 = clock64();
+#define PTR(i) do { if (ptr) { const long long t_ = clock64(); a.trace[970 + (i)] += t_ - pt0; pt0 = t_; } \
+                       if (a.prof && t == 0) { const long long t_ = clock64(); atomicAdd(a.prof + 5 + (i), (unsigned long long)(t_ - pt1)); pt1 = t_; } } while (0)
     // software pipeline: the raw L_l gathers of the warp's next stripe are in flight (in
     // registers) while the current stripe is solved
     double pv[8][4];
@@ -912,7 +946,11 @@ __device__ __forceinline__ void leaf_task(const LeafArgs& a, double* smem, int l
     // it holds at most 2 stripes, each is solved by a group of 4 warps that split its row blocks
     // (leaf_coop_stripe), and the per-warp loop stops at the last full round.
     const int ntail = nstripe % LEAF_WARPS;
+#ifdef FDE_ALL_COOP
+    const int nsolo = (COOP && nb > 1) ? 0 : nstripe;
+#else
     const int nsolo = (COOP && ntail >= 1 && ntail <= 2 && nb > 1) ? nstripe - ntail : nstripe;
+#endif
     if (warp < nsolo) load_raw(warp);
     for (int st = warp; st < nsolo; st += LEAF_WARPS) {
       // scale the 8 panel columns into the warp's stripe buffer, then into registers
@@ -967,10 +1005,12 @@ __device__ __forceinline__ void leaf_task(const LeafArgs& a, double* smem, int l
 #undef PTR
     if (COOP && nsolo < nstripe) {
       __syncthreads();                               // (every warp-private stripe buffer free)
-      const int g = warp >> 2;                       // group g solves stripe nsolo + g
-      if (nsolo + g < nstripe)
-        leaf_coop_stripe(A, nb, s, c, a, pcd, c_begin, c_end, nsolo + g, dps, dms, bs,
+      const int g = warp >> 2;                       // group g solves stripes nsolo + g, + 2, ..
+      for (int st2 = nsolo + g; st2 < nstripe; st2 += 2) {
+        if (st2 > nsolo + g) asm volatile("bar.sync %0, %1;" ::"r"(2 + g), "n"(128) : "memory");
+        leaf_coop_stripe(A, nb, s, c, a, pcd, c_begin, c_end, st2, dps, dms, bs,
                          A + LEAF_MAX * LDA_LEAF + (4 * g) * 8 * YLD, Xi, n);
+      }
       __syncthreads();
     }
     lph(4);
