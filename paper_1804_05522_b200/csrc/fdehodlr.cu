@@ -590,14 +590,8 @@ static int tree_layout(fde_hodlr* H) {
   g.off_S = (int)o; o += (long long)K4 * g.lds;
   g.off_T = (int)o;                                   // union { T + Z (S phase), U (Q update) }
   g.off_Z = round_up((int)(o + (long long)kp * g.lds), 2);   // (16-byte aligned: contiguous staging)
-  g.off_U = (int)o;                                   // ring slots 2, 3 (alias T + Z)
-  {
-    const long long slot2 = 2LL * (TR_SUB * NC + 2);  // one ring slot: [Q_c1 rows | Q_c2 rows]
-    o += std::max((long long)(g.off_Z - o) + 2LL * H->kmax * NC + 6, 2 * slot2);
-    o = round_up((int)o, 2);
-    g.off_U01 = (int)o;                               // ring slots 0, 1 (filled during the S phase)
-    o += 2 * slot2;
-  }
+  g.off_U = (int)o;
+  o += std::max((long long)(g.off_Z - o) + 2LL * H->kmax * NC + 6, 2LL * TR_STG * (TR_SUB * NC + 2));
   // final pass: 4 v vectors + max(4 warps x 2 S buffers, X block + partials)
   const long long fin = 4LL * round_up(NC, 8) + std::max(8LL * H->kmax * NC, (long long)NC * 128 + 256);
   const size_t bytes = (size_t)std::max(o, fin) * sizeof(double);

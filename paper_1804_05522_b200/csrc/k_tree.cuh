@@ -49,7 +49,6 @@ struct TrArgs {
   long long krlev[LMAX], krinst; // per-instance offset of level m's node store, instance stride
   int kp, lds, ldk, lda, rch_max;  // smem geometry (host computed)
   int off_B, off_C, off_M, off_M2, off_S, off_T, off_Z, off_U;
-  int off_U01;                   // Q-update ring slots 0, 1 (not aliased: filled during the S phase)
 };
 
 __device__ __forceinline__ unsigned tr_ld_acquire(const unsigned* p) {
@@ -245,8 +244,8 @@ __device__ void tr_unit(const TrArgs& a, double* sm, int inst, int m, int j, int
   const double* Q1s = a.Q + (long long)inst * a.qinst + a.qlev[m + 1] + (long long)(2 * j) * qs1_ + (long long)(xm - 1) * ncol1;
   double* Z1 = cp_contig_dst(sm + a.off_Z, Q1s);
   double* Z2 = cp_contig_dst(sm + a.off_Z + round_up(k * ncol1 + 2, 2), Q1s + qs1_);
-  double* Ub = sm + a.off_U;      // ring slots 2, 3 of [Q_c1 rows | Q_c2 rows] (TR_SUB x ncol1 each):
-                                  // alias Ts and Z, filled only after the S phase; slots 0, 1 at off_U01
+  double* Ub = sm + a.off_U;      // TR_STG buffers x [Q_c1 rows | Q_c2 rows] (TR_SUB x ncol1 each);
+                                  // aliases Ts and Z: streamed only after the S phase
   const long long qs1 = (long long)(ncol1 - 1) * ncol1;
   const double* Q1 = a.Q + (long long)inst * a.qinst + a.qlev[m + 1] + (long long)(2 * j) * qs1;
   const double* Q2 = Q1 + qs1;
@@ -259,48 +258,16 @@ __device__ void tr_unit(const TrArgs& a, double* sm, int inst, int m, int j, int
   FDE_ASSERT(k >= 1 && k <= a.kmaxc && rb <= max(nrow, 0) && ra >= 0 && ncol1 <= a.NC);
   // sub-chunk buffers: [U1 | U2] x TR_STG, each TR_SUB x ncol1 (+2 spare doubles: 16-byte copies)
   const int usz = TR_SUB * ncol1 + 2;
-  static_assert(TR_STG == 4, "ring slots 0-1 (off_U01) + 2-3 (off_U)");
-  auto slotb = [&](int sc) -> double* {
-    const int sl = sc % TR_STG;
-    return sl < 2 ? sm + a.off_U01 + sl * 2 * usz : Ub + (sl - 2) * 2 * usz;
-  };
   auto ubuf = [&](int sc, int which) -> double* {
     const int rs = ra + sc * TR_SUB;
-    return cp_contig_dst(slotb(sc) + which * usz, (which ? Q2 : Q1) + (long long)rs * ncol1);
+    return cp_contig_dst(Ub + (sc % TR_STG) * 2 * usz + which * usz, (which ? Q2 : Q1) + (long long)rs * ncol1);
   };
   auto issue_sub = [&](int sc) {
     const int rs = ra + sc * TR_SUB, nr = min(TR_SUB, rb - rs);
-    cp_contig(slotb(sc), Q1 + (long long)rs * ncol1, nr * ncol1, t, TR_THREADS);
-    cp_contig(slotb(sc) + usz, Q2 + (long long)rs * ncol1, nr * ncol1, t, TR_THREADS);
+    cp_contig(Ub + (sc % TR_STG) * 2 * usz, Q1 + (long long)rs * ncol1, nr * ncol1, t, TR_THREADS);
+    cp_contig(Ub + (sc % TR_STG) * 2 * usz + usz, Q2 + (long long)rs * ncol1, nr * ncol1, t, TR_THREADS);
     cp_async_commit();
   };
-  // TMA-engine path of the update: each sub-chunk's Q1 / Q2 rows are one contiguous run (rounded
-  // up to an even count of doubles: the extra one stays inside the child Q) -> two bulk copies
-  // into a ring slot with an mbarrier; slots 0 and 1 are filled while the S phase runs
-  __shared__ unsigned long long qbar[TR_STG];
-  __shared__ int qcnt[TR_STG];
-  const bool qbulk = nsub > 0 && ((reinterpret_cast<unsigned long long>(Q1) | reinterpret_cast<unsigned long long>(Q2) |
-                                   reinterpret_cast<unsigned long long>(Ub) |
-                                   reinterpret_cast<unsigned long long>(sm + a.off_U01)) & 15) == 0 && (ra & 1) == 0;
-  auto issue_b = [&](int sc) {                        // (one thread)
-    const int rs = ra + sc * TR_SUB, nr = min(TR_SUB, rb - rs);
-    const unsigned bytes = (unsigned)round_up(nr * ncol1, 2) * 8u;
-    double* dst = slotb(sc);
-    mbar_expect_tx(qbar + sc % TR_STG, 2 * bytes);
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"(smem_u32(dst)), "l"(Q1 + (long long)rs * ncol1), "r"(bytes), "r"(smem_u32(qbar + sc % TR_STG)) : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"(smem_u32(dst + usz)), "l"(Q2 + (long long)rs * ncol1), "r"(bytes), "r"(smem_u32(qbar + sc % TR_STG)) : "memory");
-  };
-  if (qbulk && t == 0) {
-    for (int i = 0; i < TR_STG; ++i) mbar_init(qbar + i, 1u);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    // (the previous task's generic accesses of these slots, and Q written by other CTAs, before
-    //  the async-proxy copies)
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-    for (int sc = 0; sc < 2 && sc < nsub; ++sc) issue_b(sc);
-  }
   const bool tdbg = a.trace && t == 0;
   long long tcl = clock64();
   const int tsl = 1100 + (m == a.L - 1 ? 0 : 8);   // phase clocks: bottom level / the others
@@ -411,10 +378,32 @@ __device__ void tr_unit(const TrArgs& a, double* sm, int inst, int m, int j, int
       default: break;
     }
   };
+  // TMA-engine path: each sub-chunk's Q1 / Q2 rows are one contiguous run (rounded up to an
+  // even count of doubles: the extra one stays inside the child Q) -> two bulk copies into a
+  // ring slot with an mbarrier; the last warp done with a slot refills it (no CTA barrier).
+  __shared__ unsigned long long qbar[TR_STG];
+  __shared__ int qcnt[TR_STG];
+  const bool qbulk = ((reinterpret_cast<unsigned long long>(Q1) | reinterpret_cast<unsigned long long>(Q2) |
+                       reinterpret_cast<unsigned long long>(Ub)) & 15) == 0 && (ra & 1) == 0 && TR_SUB % 2 == 0;
   if (qbulk) {
+    auto issue_b = [&](int sc) {                      // (one thread)
+      const int rs = ra + sc * TR_SUB, nr = min(TR_SUB, rb - rs);
+      const unsigned bytes = (unsigned)round_up(nr * ncol1, 2) * 8u;
+      double* dst = Ub + (sc % TR_STG) * 2 * usz;
+      mbar_expect_tx(qbar + sc % TR_STG, 2 * bytes);
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(smem_u32(dst)), "l"(Q1 + (long long)rs * ncol1), "r"(bytes), "r"(smem_u32(qbar + sc % TR_STG)) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(smem_u32(dst + usz)), "l"(Q2 + (long long)rs * ncol1), "r"(bytes), "r"(smem_u32(qbar + sc % TR_STG)) : "memory");
+    };
     if (t == 0) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // (S-phase use of slots 2, 3)
-      for (int sc = 2; sc < TR_STG && sc < nsub; ++sc) issue_b(sc);
+      for (int i = 0; i < TR_STG; ++i) mbar_init(qbar + i, 1u);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      // (generic accesses of the aliased staging buffers, and Q written by other CTAs, before
+      //  the async-proxy copies)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      for (int sc = 0; sc < TR_STG && sc < nsub; ++sc) issue_b(sc);
     } else if (t >= 32 && t < 32 + TR_STG) {
       qcnt[t - 32] = 0;
     }
@@ -423,7 +412,7 @@ __device__ void tr_unit(const TrArgs& a, double* sm, int inst, int m, int j, int
       mbar_wait(qbar + sc % TR_STG, (sc / TR_STG) & 1);
       TPH(6);                                            // (wait)
       const int rs = ra + sc * TR_SUB;
-      const double* U1 = slotb(sc);
+      const double* U1 = Ub + (sc % TR_STG) * 2 * usz;
       update(U1, U1 + usz, rs, min(TR_SUB, rb - rs));
       TPH(5);                                            // (update)
       __syncwarp();
