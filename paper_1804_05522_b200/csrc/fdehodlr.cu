@@ -121,6 +121,7 @@ struct fde_hodlr {
   double *d_dp = nullptr, *d_dm = nullptr;
   double *d_X = nullptr, *d_LU = nullptr, *d_P = nullptr;
   long long gstride = 0, xstride = 0, lustride = 0, pstride_seg = 0, pstride_inst = 0;
+  long long lurstride = 0;          // stored run LUs (k_run): LEAF_RSLOT doubles per leaf
   int ncap = 0;
   // level layout (host-known after the compression): k_l = max rank over the batch + 1
   bool layout_done = false;
@@ -1124,8 +1125,9 @@ static int run_chunk(fde_hodlr* H, int K, double dt, const double* d_plus, const
     TRY(dalloc(H, &H->d_X2, (size_t)B * H->xstride));
     TRY(dalloc(H, &H->d_Q2, (size_t)B * H->qinst));
     TRY(dalloc(H, &H->d_S2, (size_t)B * H->sinst));
-    TRY(dalloc(H, &H->d_LUr[0], (size_t)B * H->lustride));
-    TRY(dalloc(H, &H->d_LUr[1], (size_t)B * H->lustride));
+    H->lurstride = (long long)H->nleaf * LEAF_RSLOT;
+    TRY(dalloc(H, &H->d_LUr[0], (size_t)B * H->lurstride));
+    TRY(dalloc(H, &H->d_LUr[1], (size_t)B * H->lurstride));
     TRY(tmaps_add_x2(H));
   }
   if (!H->d_Kr[0]) {                                 // split units: [C | Sc^-1 | G] per node, 2 parities
@@ -1189,7 +1191,7 @@ static int run_chunk(fde_hodlr* H, int K, double dt, const double* d_plus, const
   la.Lf = H->d_Lf; la.lf_stride = H->lf_stride; la.rank = H->d_rank;
   for (int l = 0; l < L; ++l) { la.kl[l] = H->kl[l]; la.xcol[l] = H->xcol[l]; }
   la.xcol[L] = H->xcol[L];
-  la.xstride = H->xstride; la.lustride = H->lustride; la.keep = 0; la.st = H->d_status;
+  la.xstride = H->xstride; la.lustride = H->lurstride; la.keep = 0; la.st = H->d_status;
   la.qinst = H->qinst; la.qstride = (long long)(H->xcol[L] - 1) * H->xcol[L];
   la.trace = nullptr; la.nf = 0; la.store_lu = 1;
   TrArgs a = H->tr_geo;

@@ -33,15 +33,15 @@ __device__ void leaf_rhs_final(const TrArgs& geo, const TrArgs* tp, const LeafAr
   double* vs = bs + LEAF_MAX;                         // v (NC)
   double* part = vs + NCOL_MAX;                       // [4][128]
   double* zs = part + 4 * LEAF_MAX;                   // [32]
-  double* LUs = sm + RN_FRONT;                        // [sp x sp] column-major, ld = sp
-  double* Ss = LUs + LEAF_MAX * LEAF_MAX;             // S_side blocks of a batch of levels
-  const int scap = smem_doubles - RN_FRONT - LEAF_MAX * LEAF_MAX;
+  double* LUs = sm + RN_FRONT;                        // [sp cols] column-major, ld = LDA_LEAF
+  double* Ss = LUs + LEAF_RSLOT;                      // S_side blocks of a batch of levels
+  const int scap = smem_doubles - RN_FRONT - LEAF_RSLOT;
   FDE_ASSERT(s >= 1 && s <= LEAF_MAX && NC <= NCOL_MAX && scap > 0 && r0 + s <= n);
   // ---- the first batch of S blocks, then the stored LU, in flight while the final is formed.
   //      The LU (one contiguous 8 sp^2-byte run) is one bulk copy of the TMA engine (mbarrier
   //      rn_bar[0]) when the run is 16-byte aligned, else cp.async.
   __shared__ unsigned long long rn_bar[1];
-  const double* LUg = la ? la->LU + (long long)inst * la->lustride + (long long)leaf * LEAF_SLOT : nullptr;
+  const double* LUg = la ? la->LU + (long long)inst * la->lustride + (long long)leaf * LEAF_RSLOT : nullptr;
   const bool lu_bulk = la && (reinterpret_cast<unsigned long long>(LUg) & 15) == 0;
   if (la && t == 0) {
     mbar_init(rn_bar, 1u);
@@ -54,12 +54,12 @@ __device__ void leaf_rhs_final(const TrArgs& geo, const TrArgs* tp, const LeafAr
         // another CTA, acquired by the scheduler), ordered before the async-proxy copy
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("fence.proxy.async.global;" ::: "memory");
-        mbar_expect_tx(rn_bar, (unsigned)(sp * sp * 8));
+        mbar_expect_tx(rn_bar, (unsigned)(sp * LDA_LEAF * 8));
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                     ::"r"(smem_u32(LUs)), "l"(LUg), "r"((unsigned)(sp * sp * 8)), "r"(smem_u32(rn_bar)) : "memory");
+                     ::"r"(smem_u32(LUs)), "l"(LUg), "r"((unsigned)(sp * LDA_LEAF * 8)), "r"(smem_u32(rn_bar)) : "memory");
       }
     } else {
-      for (int e = 2 * t; e < sp * sp; e += 2 * LEAF_THREADS) cp_async16(LUs + e, LUg + e);
+      for (int e = 2 * t; e < sp * LDA_LEAF; e += 2 * LEAF_THREADS) cp_async16(LUs + e, LUg + e);
     }
     cp_async_commit();
   };
@@ -183,7 +183,7 @@ __device__ void leaf_rhs_final(const TrArgs& geo, const TrArgs* tp, const LeafAr
   if (lu_bulk) mbar_wait(rn_bar, 0);
   __syncthreads();
   RN_PH(4);
-  // ---- x0 = A_leaf^{-1} b with the stored LU (k_leaf.cuh inverse-diagonal form: off-diagonal
+  // ---- x0 = A_leaf^{-1} b with the stored LU (k_leaf.cuh inverse-diagonal form, ld LDA_LEAF: off-diagonal
   //      blocks hold -Lt / -Ut, diagonal blocks D_k = A_kk^{-1}); 2 column halves per row
   const int i = t & 127, h = t >> 7;
   for (int kb = 0; kb + 1 < nb; ++kb) {              // forward: y_i += (-Lt_ik) y_k
@@ -191,7 +191,7 @@ __device__ void leaf_rhs_final(const TrArgs& geo, const TrArgs* tp, const LeafAr
     double acc = 0.0;
     if (i >= 32 * (kb + 1) && i < sp)
 #pragma unroll
-      for (int jj = 0; jj < 16; ++jj) acc = fma(LUs[i + (c0 + jj) * sp], bs[c0 + jj], acc);
+      for (int jj = 0; jj < 16; ++jj) acc = fma(LUs[i + (c0 + jj) * LDA_LEAF], bs[c0 + jj], acc);
     part[h * LEAF_MAX + i] = acc;
     __syncthreads();
     if (t < sp && t >= 32 * (kb + 1)) bs[t] += part[t] + part[LEAF_MAX + t];
@@ -204,7 +204,7 @@ __device__ void leaf_rhs_final(const TrArgs& geo, const TrArgs* tp, const LeafAr
     double acc = 0.0;
     if (i < 32 * (kb + 1))
 #pragma unroll
-      for (int jj = 0; jj < 16; ++jj) acc = fma(LUs[i + (c0 + jj) * sp], zs[16 * h + jj], acc);
+      for (int jj = 0; jj < 16; ++jj) acc = fma(LUs[i + (c0 + jj) * LDA_LEAF], zs[16 * h + jj], acc);
     part[h * LEAF_MAX + i] = acc;
     __syncthreads();
     if (t < 32 * (kb + 1)) {

@@ -30,6 +30,7 @@
 #define LDP_LEAF 132
 #define YLD 132                      // warp stripe buffer (128 x 8) leading dim (= 4 mod 16)
 #define LEAF_SLOT (LEAF_MAX * LEAF_MAX)   // doubles per kept leaf factor
+#define LEAF_RSLOT (LEAF_MAX * LDA_LEAF)  // doubles per stored run LU (the shared-memory layout)
 #define NCOL_MAX 384                 // panel columns (1 + sum of k_l) held as descriptors in smem
 #define LEAF_FRONT (32 * 33 + 3 * LEAF_MAX + 2 * NCOL_MAX)        // doubles before the LU region
 #define LEAF_BIG (LEAF_MAX * LDA_LEAF + LEAF_WARPS * 8 * YLD)       // LU + stripe buffers (reused by Q)
@@ -57,7 +58,8 @@ struct LeafArgs {
   const double* u_prev; const double* f;     // [batch*n], factor mode with nf = 1
   const double* b; double* y; int nrhs; int ld;   // solve mode
   double* Q; long long qstride, qinst;       // factor mode: Q_leaf = V_all^T X_leaf (or null)
-  int store_lu;                              // factor mode: write the LU (inverse-diagonal form)
+  int store_lu;                              // factor mode: write the LU (inverse-diagonal form, pitch
+                                             // LDA_LEAF, LEAF_RSLOT doubles per leaf) -- k_run
   unsigned long long* prof;                  // optional: phase cycle sums (k_run FDE_TRACE_RUN)
   DevStatus* st;
   unsigned long long* trace;                 // optional phase clocks (FDE_TRACE_LEVELS)
@@ -910,9 +912,23 @@ __device__ __forceinline__ void leaf_task(const LeafArgs& a, double* smem, int l
     lph(0);
     // ---- S4: block LU (inverse-diagonal form, off-diagonal blocks negated); block 0 done
     leaf_block_lu(A, sp, S + 272, a.st, where, a.trace, true);
-    if (a.store_lu)                                  // for the deferred rhs column (leaf_rhs_task)
+    // for the deferred rhs column (leaf_rhs_final): the LU in its shared-memory layout as one
+    // bulk store of the TMA engine, overlapped with the panel (which only reads it); completed
+    // before the task ends (lu_bulk_wait)
+    double* LUr = a.store_lu ? a.LU + (long long)inst * a.lustride + (long long)leaf * LEAF_RSLOT : nullptr;
+    const bool lu_bulk = a.store_lu && (reinterpret_cast<unsigned long long>(LUr) & 15) == 0;
+    if (lu_bulk) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // (this thread's LU writes)
+      __syncthreads();
+      if (t == 0) {
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                     ::"l"(LUr), "r"(smem_u32(A)), "r"((unsigned)(sp * LDA_LEAF * 8)) : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    } else if (a.store_lu) {
       for (int j = warp; j < sp; j += LEAF_WARPS)
-        for (int i = lane; i < sp; i += 32) LUg[i + j * sp] = A[i + j * LDA_LEAF];
+        for (int i = lane; i < sp; i += 32) LUr[i + j * LDA_LEAF] = A[i + j * LDA_LEAF];
+    }
     lph(1);
     stamp(2);
     // ---- panel X = A_leaf^{-1} [b | U_0 .. U_{L-1}] by warp stripes of 8 columns
@@ -1033,6 +1049,10 @@ __device__ __forceinline__ void leaf_task(const LeafArgs& a, double* smem, int l
             LUg[i + (8 * st + 2 * tig + 1) * sp] = acc[tt][1];
           }
       }
+    }
+    if (lu_bulk && t == 0) {                         // (the store has read the LU region and landed)
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      asm volatile("fence.proxy.async.global;" ::: "memory");
     }
     stamp(3);
     if (a.Q && do_proj)
