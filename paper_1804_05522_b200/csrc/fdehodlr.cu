@@ -1278,6 +1278,7 @@ static int run_chunk(fde_hodlr* H, int K, double dt, const double* d_plus, const
               pf[16] / c, pf[17] / c, pf[20] / c);
       fprintf(stderr, "k_run A panel, warp 0 (us avg per leaf): gather+scale %.2f acc-init %.2f solve %.2f store %.2f\n",
               pf[21] / c, pf[22] / c, pf[23] / c, pf[24] / c);
+      fprintf(stderr, "k_run A panel, warp 0 first-stripe gather+scale %.2f us\n", pf[25] / c);
       const double cb = (double)std::max(1ULL, pf[27]) * 1965.0;
       fprintf(stderr, "k_run B phases (us avg over %llu): V+X staging %.2f dmma %.2f\n",
               pf[27], pf[25] / cb, pf[26] / cb);

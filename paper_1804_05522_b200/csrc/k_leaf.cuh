@@ -971,23 +971,24 @@ __device__ __forceinline__ void leaf_task(const LeafArgs& a, double* smem, int l
     for (int st = warp; st < nsolo; st += LEAF_WARPS) {
       // scale the 8 panel columns into the warp's stripe buffer, then into registers
       const int cs = c_begin + 8 * st;
+      // (branch-free: every load is unconditional and in range, the kind picks by selects, so
+      //  the 32 shared loads of a lane are in flight together)
 #pragma unroll
       for (int cc = 0; cc < 8; ++cc) {
         const PanelCol pc = cs + cc < c_end ? pcd[cs + cc - c_begin] : PanelCol{a.Lf, 0, 0, 0, 0, 0};
         const double* sc = pc.sel ? dms : dps;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const int i = lane + 32 * q;
-          double v = 0.0;
-          if (i < s) {
-            if (pc.kind == 2) v = pv[cc][q] * (-c * sc[i]);
-            else if (pc.kind == 3) v = (pc.li0 + pc.lstep * i == 0) ? -c * sc[i] : 0.0;
-            else if (pc.kind == 1) v = bs[i];
-          }
-          Ys[i + cc * YLD] = v;
+          const int i = lane + 32 * q, ic = i < s ? i : s - 1;
+          const double scv = sc[ic], bv = bs[ic];
+          const double v2 = pv[cc][q] * (-c * scv);
+          const double v3 = (pc.li0 + pc.lstep * i == 0) ? -c * scv : 0.0;
+          double v = pc.kind == 2 ? v2 : pc.kind == 3 ? v3 : pc.kind == 1 ? bv : 0.0;
+          Ys[i + cc * YLD] = i < s ? v : 0.0;
         }
       }
       __syncwarp();
+      if (a.prof && t == 0 && st == warp) { const long long t_ = clock64(); atomicAdd(a.prof + 9, (unsigned long long)(t_ - pt1)); }
       PTR(0);
 #pragma unroll
       for (int tt = 0; tt < 16; ++tt) {
