@@ -694,6 +694,8 @@ __device__ __forceinline__ bool leaf_project_tma(const LeafArgs& a, double* smem
   double* Xb = Vs + vtot;
   const int NB = min(PB_NB_MAX, (int)((smem + LEAF_FRONT + LEAF_BIG - Xb) / (CW * LDV)));
   if (NB < 2) return false;
+  FDE_ASSERT(NV <= NCOL_MAX && (smem_u32(Vs) & 127) == 0 && (smem_u32(Xb) & 127) == 0 &&
+             Xb + NB * CW * LDV <= smem + LEAF_FRONT + LEAF_BIG && s <= LDV);
   for (int j = t; j < NV; j += LEAF_THREADS) {        // V column j = X column j + 1
     int l = 0, o = 0;
     while (l + 1 < L && a.xcol[l + 1] - 1 <= j) { o += lev_block(l); ++l; }
@@ -724,6 +726,7 @@ __device__ __forceinline__ bool leaf_project_tma(const LeafArgs& a, double* smem
       int o = 0;
       for (int l = 0; l < lane; ++l) o += lev_block(l);
       const PanelCol pc = pcd[a.xcol[lane] - c_begin];
+      FDE_ASSERT(pc.kind == 2 && rl < a.kl[lane] && o + rl * LDV <= vtot);
       const int row0 = pc.lstep < 0 ? pc.li0 - (s - 1) : pc.li0;
       tma_load_2d(Vs + o, static_cast<const CUtensorMapLike*>(a.lmap) + (inst * L + lane), row0, 0, bars);
     }

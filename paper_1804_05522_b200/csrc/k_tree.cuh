@@ -389,6 +389,7 @@ __device__ void tr_unit(const TrArgs& a, double* sm, int inst, int m, int j, int
     auto issue_b = [&](int sc) {                      // (one thread)
       const int rs = ra + sc * TR_SUB, nr = min(TR_SUB, rb - rs);
       const unsigned bytes = (unsigned)round_up(nr * ncol1, 2) * 8u;
+      FDE_ASSERT(nr >= 1 && rs + nr <= rb && (int)(bytes / 8) <= usz);
       double* dst = Ub + (sc % TR_STG) * 2 * usz;
       mbar_expect_tx(qbar + sc % TR_STG, 2 * bytes);
       asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
