@@ -1155,6 +1155,10 @@ static int run_chunk(fde_hodlr* H, int K, double dt, const double* d_plus, const
     ra.split = (long long)B * H->nleaf < 2LL * nsm;
   }
   if (const char* e = fde_dbg_env("FDE_RUN_SPLIT")) ra.split = atoi(e) != 0;   // (diagnostics build)
+  // whole tree units: the projection (B) runs inside the B' task of the same leaf (one V staging,
+  // Q[:, 0] from it); split units keep B separate (its U unit stays off the step chain)
+  ra.fuse = ra.split ? 0 : 1;
+  if (const char* e = fde_dbg_env("FDE_RUN_FUSE")) ra.fuse = !ra.split && atoi(e) != 0;   // (diagnostics)
   long long o = 0, units = 0;
   ra.o_A = o; o += n_leaf;
   ra.o_R = o; o += n_leaf;

@@ -20,8 +20,11 @@ __device__ __forceinline__ void rn_copy(T* dst, const T* src) {
 // B' (and the finals of step K; the k_step finals).  geo: tree geometry; tp = step m-1's tree
 // arguments (X^(m-1), S^(m-1), u^(m-1) output) or null at m = 0; la = step m's leaf arguments
 // or null at m = K.
+// q0 = false (k_run fused BB' task): stop after x0 (left in sm[0, s) and X[:, 0]); the projection
+// that follows computes Q[:, 0] with its staged V.
 __device__ void leaf_rhs_final(const TrArgs& geo, const TrArgs* tp, const LeafArgs* la, double* sm,
-                               int smem_doubles, int inst, int leaf, unsigned long long* prof = nullptr) {
+                               int smem_doubles, int inst, int leaf, unsigned long long* prof = nullptr,
+                               bool q0 = true) {
   const TrArgs& a = geo;
   long long ph_t = clock64();
 #define RN_PH(i) do { if (prof && threadIdx.x == 0) { const long long t_ = clock64(); \
@@ -216,6 +219,12 @@ __device__ void leaf_rhs_final(const TrArgs& geo, const TrArgs* tp, const LeafAr
   RN_PH(5);
   double* X0 = la->X + (long long)inst * la->xstride + r0;
   if (t < s) X0[t] = bs[t];
+  if (!q0) {
+    if (prof) { __syncthreads(); RN_PH(0); }
+    __syncthreads();                                  // (barriers free; x0 stays in bs = sm[0, s))
+    if (t == 0) mbar_inval(rn_bar);
+    return;
+  }
   PanelCol* pcq = reinterpret_cast<PanelCol*>(Ss);   // V-column descriptors (NC - 1)
   for (int j = t; j < NC - 1; j += LEAF_THREADS) pcq[j] = panel_col(*la, inst, leaf, r0, 1 + j, NC);
   __syncthreads();

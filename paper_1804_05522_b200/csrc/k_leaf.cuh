@@ -668,7 +668,8 @@ __device__ __forceinline__ void proj_tile2x2(double (&d)[2][2][2], const double*
 
 __device__ __forceinline__ bool leaf_project_tma(const LeafArgs& a, double* smem, const PanelCol* pcd,
                                                  int c_begin, int NC, int s, int inst, int r0, double* Qo,
-                                                 int c_lo, unsigned long long* prof = nullptr) {
+                                                 int c_lo, unsigned long long* prof = nullptr,
+                                                 const double* x0s = nullptr) {
   __shared__ unsigned long long bars[1 + PB_NB_MAX];   // [0] V, [1..NB] chunk slots "full"
   __shared__ int cnt[PB_NB_MAX];                        // warps done with a chunk slot
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31, gid = lane >> 2, tig = lane & 3;
@@ -795,6 +796,20 @@ __device__ __forceinline__ bool leaf_project_tma(const LeafArgs& a, double* smem
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         issue_chunk(c + NB);
       }
+    }
+  }
+  if (x0s) {
+    // Q[:, 0] = V_all^T x0 with the staged V (fused BB' task): one m-tile per warp item, the
+    // right-hand side in B-fragment column 0 (the other 7 columns zero)
+    __syncthreads();                                  // (V reversal visible; x0s written before entry)
+    const int MT = (NV + 7) >> 3;
+    for (int mt = warp; mt < MT; mt += LEAF_WARPS) {
+      const int j = 8 * mt + gid;
+      const double* ap = Vs + colofs[j < NV ? j : 0] + tig;
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll 8
+      for (int k0 = 0; k0 < s; k0 += 4) dmma884(d0, d1, ap[k0], gid == 0 ? x0s[k0 + tig] : 0.0);
+      if (tig == 0 && j < NV) Qo[(long long)j * NC] = d0;
     }
   }
   ph(6);
@@ -1108,7 +1123,10 @@ k_leaf(const LeafArgs a) {
 
 // The projection Q_leaf = V_all^T X_leaf as a task of its own (k_step.cuh): X is read back from
 // global memory, so it can run on any SM once the leaf's panel is written.
-__device__ __forceinline__ void leaf_proj_task(const LeafArgs& a, double* smem, int leaf, int inst) {
+// q0 (k_run fused BB' task): x0 = X[:, 0] of the leaf sits in smem[0, s) (leaf_rhs_final) and the
+// projection also forms Q[:, 0] = V_all^T x0.
+__device__ __forceinline__ void leaf_proj_task(const LeafArgs& a, double* smem, int leaf, int inst,
+                                               bool q0 = false) {
   double* bs = smem + 32 * 33 + 2 * LEAF_MAX;
   PanelCol* pcd = reinterpret_cast<PanelCol*>(bs + LEAF_MAX);
   const TreeDev& tr = a.tree;
@@ -1118,9 +1136,14 @@ __device__ __forceinline__ void leaf_proj_task(const LeafArgs& a, double* smem, 
     pcd[cc] = panel_col(a, inst, leaf, r0, c_begin + cc, c_end);
   const double* Xi = a.X + (long long)inst * a.xstride + r0;
   double* Qo = a.Q + (long long)inst * a.qinst + (long long)leaf * a.qstride;
+  double* x0s = smem + 512;                           // (clear of the projection's colofs)
+  if (q0)
+    for (int i = threadIdx.x; i < s; i += LEAF_THREADS) x0s[i] = smem[i];
   __syncthreads();                                    // (descriptors visible)
-  if (leaf_project_tma(a, smem, pcd, c_begin, c_end, s, inst, r0, Qo, c_begin, a.prof ? a.prof + 8 : nullptr))
+  if (leaf_project_tma(a, smem, pcd, c_begin, c_end, s, inst, r0, Qo, c_begin, a.prof ? a.prof + 8 : nullptr,
+                       q0 ? x0s : nullptr))
     return;
-  leaf_project(a, smem + LEAF_FRONT, pcd, c_begin, c_end, s, sp, Xi, Qo, c_begin,
+  // (cp.async path: column 0 is projected with the others, read back from X)
+  leaf_project(a, smem + LEAF_FRONT, pcd, c_begin, c_end, s, sp, Xi, Qo, q0 ? 0 : c_begin,
                a.prof ? a.prof + 8 : nullptr);
 }

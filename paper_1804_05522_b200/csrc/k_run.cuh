@@ -7,7 +7,10 @@
 //   B' : u^(m-1) on the leaf's rows = X^(m-1) v^(m-1) (the "final" of step m-1, see k_tree.cuh),
 //        x0 = A_leaf^{-1}(u^(m-1) + dt f^(m)) with the stored LU, X[:, 0] = x0,
 //        Q[:, 0] = V_all^T x0                                             (leaf_rhs_final, k_final.cuh)
-// and the SMW tree units of every level follow (k_tree.cuh tr_unit).  A virtual step K holds
+// and the SMW tree units of every level follow (k_tree.cuh tr_unit).  With whole tree units
+// (fuse = 1, the default unless units are split) B runs inside B' as one task BB': after x0 the
+// projection stages V once (TMA) and forms Q[:, 1:] and Q[:, 0] from it (tickets per step: A, BB').
+// A virtual step K holds
 // the last finals (u^(K-1)).  Only B' and the tree lie on the step-to-step chain; A and B of
 // step m+1 fill the SMs while the tree of step m climbs its latency-bound upper levels.
 //
@@ -52,6 +55,7 @@ struct RunArgs {
   long long o_A, o_R, o_lvl[LMAX];   // A done, B' done [leaf]; R unit done [node of level m]
   long long o_ku[LMAX], o_kr[LMAX];  // release counters of level-m nodes: U (2 inputs), R (3 inputs)
   int split;                         // 1: U / R tree units (one of each per node)
+  int fuse;                          // 1 (whole units only): B runs inside B' (tickets A, BB' per step)
   unsigned long long* trace;     // optional (FDE_TRACE_RUN): [0] count, then [start,end,code,sm]
   unsigned long long* prof;      // optional: B' phase cycle sums [16]
   long long trace_cap;
@@ -61,12 +65,24 @@ __device__ __forceinline__ bool rn_ready(const int* p, int target) { return st_l
 
 // Leaf-queue ticket l: per step A of every leaf, B of every leaf, B' of every leaf; step K:
 // finals.  Are its inputs complete?
+// Ticket l -> (step, kind, leaf index tk): per step A, B, B' of every leaf (fused: A, BB'), then
+// the finals of step K.
+__device__ __forceinline__ int rn_decode(const RunArgs& ra, long long n_leaf, long long l, long long& tk) {
+  const int per = ra.fuse ? 2 : 3;
+  const long long step = l / (per * n_leaf);
+  tk = l - step * per * n_leaf;
+  int kind = step == ra.K ? 3 : (int)(tk / n_leaf);
+  const int slot = kind == 3 ? 0 : kind;
+  if (ra.fuse && kind == 1) kind = 2;
+  tk -= slot * n_leaf;
+  return kind;
+}
+
 __device__ __forceinline__ bool rn_leaf_ready(const RunArgs& ra, long long n_leaf, long long l) {
   const TrArgs& a = ra.tas[0];
-  const long long step = l / (3 * n_leaf);
-  long long tk = l - step * 3 * n_leaf;
-  const int kind = step == ra.K ? 3 : (int)(tk / n_leaf);
-  tk -= (kind == 3 ? 0 : kind) * n_leaf;
+  const long long step = l / ((ra.fuse ? 2 : 3) * n_leaf);
+  long long tk;
+  const int kind = rn_decode(ra, n_leaf, l, tk);
   const int* dn = ra.done + step * ra.per_step;
   const int inst = (int)(tk / a.nleaf);
   if (kind == 0) return step < 2 || rn_ready(dn - ra.per_step + ra.o_R + tk, 1);
@@ -119,7 +135,7 @@ k_run(const RunArgs ra) {
   const long long n_leaf = (long long)a0.batch * nleaf;
   long long Tt = 0;
   for (int m = 0; m < L; ++m) Tt += (long long)a0.batch * (1LL << m) * (ra.split ? 2 : a0.rc[m]);
-  const unsigned tot_t = (unsigned)(Tt * ra.K), tot_l = (unsigned)(3 * n_leaf * ra.K + n_leaf);
+  const unsigned tot_t = (unsigned)(Tt * ra.K), tot_l = (unsigned)((ra.fuse ? 2 : 3) * n_leaf * ra.K + n_leaf);
   volatile unsigned* vh = ra.heads;     // [0] tree units completed, [1] leaf tickets, [2] rq tail, [3] rq head
   long long held = -1;                  // thread 0: leaf ticket not yet runnable
   long long iou = -1;                   // thread 0: ready-queue ticket not yet served
@@ -161,10 +177,9 @@ k_run(const RunArgs ra) {
     if (ra.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     int code;
     if (queue == 1) {                                 // ---- leaf ticket
-      const int step = (int)(task / (3 * n_leaf));
-      long long tk = task - (long long)step * 3 * n_leaf;
-      const int kind = step == ra.K ? 3 : (int)(tk / n_leaf);
-      tk -= (kind == 3 ? 0 : kind) * n_leaf;
+      const int step = (int)(task / ((ra.fuse ? 2 : 3) * n_leaf));
+      long long tk;
+      const int kind = rn_decode(ra, n_leaf, task, tk);
       const int inst = (int)(tk / nleaf), leaf = (int)(tk % nleaf);
       FDE_ASSERT(step >= 0 && step <= ra.K && kind >= 0 && kind <= 3 && (kind == 3) == (step == ra.K));
       FDE_ASSERT(inst >= 0 && inst < a0.batch && leaf >= 0 && leaf < nleaf);
@@ -180,8 +195,12 @@ k_run(const RunArgs ra) {
         const int tps = step > 0 ? step - 1 : 0;
         if (s_tp_step != tps) { rn_copy(&s_tp, &ra.tas[tps]); if (threadIdx.x == 0) s_tp_step = tps; }
         leaf_rhs_final(s_tp, step > 0 ? &s_tp : nullptr, kind == 2 ? &s_la : nullptr,
-                       smem, ra.smem_doubles, inst, leaf, ra.prof);
+                       smem, ra.smem_doubles, inst, leaf, ra.prof, !(ra.fuse && kind == 2));
         if (ra.prof && threadIdx.x == 0) atomicAdd(ra.prof + (kind == 2 ? 7 : 15), 1ULL);
+        if (ra.fuse && kind == 2) {                   // BB': the projection with Q[:, 0] (x0 in smem[0, s))
+          __syncthreads();
+          leaf_proj_task(s_la, smem, leaf, inst, true);
+        }
       }
       __syncthreads();
       if (threadIdx.x == 0 && kind < 3) {
@@ -193,7 +212,7 @@ k_run(const RunArgs ra) {
           if (ra.split) {                           // B -> U of the bottom node; B' -> its R
             if (kind == 1) { if (atomicAdd(dn + ra.o_ku[L - 1] + jj, 1) == 1) rn_ready_unit(ra, step, L - 1, 0, jj, cont); }
             else if (atomicAdd(dn + ra.o_kr[L - 1] + jj, 1) == 2) rn_ready_unit(ra, step, L - 1, 1, jj, cont);
-          } else if (atomicAdd(dn + ra.o_ku[L - 1] + jj, 1) == 3) {
+          } else if (atomicAdd(dn + ra.o_ku[L - 1] + jj, 1) == (ra.fuse ? 1 : 3)) {
             cont = rn_release(ra, step, L - 1, jj);
           }
         }
