@@ -221,10 +221,13 @@ def measure_cfg4(dev, world, rank, steps=16):
                                   first step's solve) + the 15 further solves with the kept factor,
                                   i.e. SURVEY §8(d)'s "factor once" protocol (its roofline: ~2.7e5);
       value_solve_only         -- the 16 steps with an already kept factor (solve phase alone);
-      value_refactor_every_step / _pipelined_run -- d+- treated as new every step."""
+      value_refactor_every_step / _pipelined_run -- d+- treated as new every step;
+      value_factor_once_pipelined_run -- fde1d_run with the coefficients given once: the factor
+                                  is formed at step 0 of the launch, later steps are the rhs
+                                  column alone (k_run inv mode)."""
     import torch
     from paper_1804_05522_b200 import workloads as W
-    from paper_1804_05522_b200.hodlr import Fde1dStepper, FDE_NO_KEEP
+    from paper_1804_05522_b200.hodlr import Fde1dStepper, FDE_NO_KEEP, FDE_REFACTOR
     from paper_1804_05522_b200.shard import ShardedRun
     wl = W.cfg4()
     run = ShardedRun(wl.batch, world, rank)
@@ -266,10 +269,13 @@ def measure_cfg4(dev, world, rank, steps=16):
     v_solve, ms_solve = timed(solve_only)
     v_ref, ms_ref = timed(refactor)
     try:
-        st.run(wl.dt, DP[None], DM[None], F[None], u[0], K=steps)
-        v_run, ms_run = timed(lambda: st.run(wl.dt, DP[None], DM[None], F[None], u[0], K=steps))
+        runf = lambda fl: st.run(wl.dt, DP[None], DM[None], F[None], u[0], K=steps, flags=fl)
+        runf(FDE_REFACTOR)
+        v_run, ms_run = timed(lambda: runf(FDE_REFACTOR))
+        runf(0)
+        v_run1, ms_run1 = timed(lambda: runf(0))     # factor once inside the pipelined launch
     except Exception as e:                          # (memory for the second buffer set)
-        v_run, ms_run = None, str(e)[:120]
+        v_run, ms_run, v_run1, ms_run1 = None, str(e)[:120], None, None
     st.close()
     return {"workload": "cfg4: 512 x n=8192, alpha_i~U(1.1,1.9), 16 steps, leaf 128, tol 1e-13 (R18)",
             "metric": "instance-steps/s",
@@ -277,6 +283,7 @@ def measure_cfg4(dev, world, rank, steps=16):
             "value_solve_only": v_solve, "ms_16_steps_solve_only": ms_solve,
             "value_refactor_every_step": v_ref, "ms_16_steps_refactor": ms_ref,
             "value_refactor_pipelined_run": v_run, "ms_16_steps_refactor_pipelined_run": ms_run,
+            "value_factor_once_pipelined_run": v_run1, "ms_16_steps_factor_once_pipelined_run": ms_run1,
             "survey_roofline_factor_once": 2.7e5,
             "sharding": "%d instances per rank (shard.py), no data-path collective" % run.count}
 
@@ -373,31 +380,43 @@ def measure_cfg3_split(dev, world, rank, steps=16):
 
 def measure_small(dev, name, reps=3):
     """BASELINE configs[0] / configs[1] (latency-bound sizes): the whole K-step trajectory through
-    fde1d_run (refactor every step), CUDA events around the launch after a warm-up run."""
+    fde1d_run, CUDA events around the launch after a warm-up run.  cfg2 (d+-(x, t)) refactors every
+    step; cfg1 (d+- = 1, time-invariant) factors once inside the launch -- `value` -- and
+    is also timed with FDE_REFACTOR (`value_refactor`)."""
     import torch
     from paper_1804_05522_b200 import workloads as W
-    from paper_1804_05522_b200.hodlr import Fde1dStepper
+    from paper_1804_05522_b200.hodlr import Fde1dStepper, FDE_REFACTOR
     wl = getattr(W, name)()
     t = lambda a: torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device=dev)
     DP, DM, F, U0 = t(wl.d_plus), t(wl.d_minus), t(wl.f), t(wl.u0)
     st = Fde1dStepper(wl.n, wl.alpha, wl.h, wl.tol, wl.leaf, batch=wl.batch)
-    st.run(wl.dt, DP, DM, F, U0)
-    torch.cuda.synchronize()
-    best = None
-    for _ in range(reps):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        st.run(wl.dt, DP, DM, F, U0)
-        b.record()
+
+    def best_ms(flags):
+        st.run(wl.dt, DP, DM, F, U0, flags=flags)
         torch.cuda.synchronize()
-        ms = a.elapsed_time(b)
-        best = ms if best is None else min(best, ms)
-    ranks = st.ranks()
+        best = None
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            st.run(wl.dt, DP, DM, F, U0, flags=flags)
+            b.record()
+            torch.cuda.synchronize()
+            ms = a.elapsed_time(b)
+            best = ms if best is None else min(best, ms)
+        return best
+    best = best_ms(0)
+    invariant = wl.d_plus.shape[0] == 1
+    out = {"workload": "%s: n=%d alpha=%g leaf %d tol %g, %d steps (BASELINE configs), %s" % (
+               name, wl.n, float(wl.alpha[0]), wl.leaf, wl.tol, wl.K,
+               "d+- time-invariant: factor once in the launch" if invariant else "refactor every step"),
+           "metric": "time-steps/s", "value": wl.K / (best / 1e3), "us_per_step": 1e3 * best / wl.K,
+           "ranks": st.ranks(), "timing": "CUDA events around one fde1d_run of all K steps, best of %d" % reps}
+    if invariant:
+        best_r = best_ms(FDE_REFACTOR)
+        out["value_refactor"] = wl.K / (best_r / 1e3)
+        out["us_per_step_refactor"] = 1e3 * best_r / wl.K
     st.close()
-    return {"workload": "%s: n=%d alpha=%g leaf %d tol %g, %d steps (BASELINE configs)" % (
-                name, wl.n, float(wl.alpha[0]), wl.leaf, wl.tol, wl.K),
-            "metric": "time-steps/s", "value": wl.K / (best / 1e3), "us_per_step": 1e3 * best / wl.K,
-            "ranks": ranks, "timing": "CUDA events around one fde1d_run of all K steps, best of %d" % reps}
+    return out
 
 
 def task_profile(K=16):

@@ -62,6 +62,8 @@ extern "C" {
 #define FDE_COEFFS_CHANGED 64u /* fde2d_step: the coefficient arrays were rewritten in place since the
                                  operators were factorised: refactorise them (the cache otherwise
                                  refactorises only when dt or the coefficient pointers change) */
+#define FDE_REFACTOR  128u /* fde1d_run: refactorise every step even when coef_stride is 0 (timing and
+                                 checking of the refactor path; the default then factors once) */
 
 /* Compile-time capacities of this build. */
 #define FDE_LEAF_MAX  128 /* largest leaf (dense diagonal block) held in shared memory */
@@ -166,7 +168,11 @@ int fde1d_step_split(int world, int rank, fde_allgather_fn gather, void* ctx, in
  * of step m; only the rhs column waits for u^(m).  Same factorisation as fde1d_step; the rhs
  * column's leaf solve uses the stored LU (results agree with fde1d_step to rounding).
  *   d_plus, d_minus [dev]: step m at d_plus + m * coef_stride (batch*n each; coef_stride = 0:
- *   the same coefficients every step); f [dev] likewise with f_stride; u0 [dev, batch*n];
+ *   the same coefficients every step, so A_m = A for all m and the launch factors once -- leaf
+ *   LUs, U-column panel, projections and the non-rhs tree work at step 0 only; every later step
+ *   is the rhs column alone against that factor ("the LU can be computed only once at
+ *   the beginning"); FDE_REFACTOR in flags refactors every step instead, with bitwise-equal
+ *   results when the run uses split tree units); f [dev] likewise with f_stride; u0 [dev, batch*n];
  *   u_out [dev, K * batch*n] receives every step's solution (step m at u_out + m*batch*n);
  *   u_out must not alias u0 or the coefficient arrays.
  *   `cache`, alpha, h, tol, leaf, stream as in fde1d_step.  Asynchronous unless FDE_SYNC.

@@ -13,6 +13,7 @@ LIB_PATH = os.path.join(HERE, "libfdehodlr_dbg.so" if os.environ.get("FDE_LIB_DE
 FDE_OK, FDE_EDOMAIN, FDE_EDIM, FDE_ESINGULAR, FDE_ENOCONV, FDE_ECUDA, FDE_ENOMEM = range(7)
 FDE_SYNC, FDE_CHECK, FDE_HOST_PTRS, FDE_NO_KEEP, FDE_RECOMPRESS, FDE_COMPRESS_ONLY = 1, 2, 4, 8, 16, 32
 FDE_COEFFS_CHANGED = 64
+FDE_REFACTOR = 128
 FDE_LEAF_MAX, FDE_RANK_MAX = 128, 47
 
 # every symbol the header declares, with its ctypes signature

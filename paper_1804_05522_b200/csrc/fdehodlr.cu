@@ -1115,9 +1115,11 @@ static int tmaps_add_x2(fde_hodlr* H) {
 // C-ABI
 // One k_run launch of K <= RUN_KMAX pipelined steps: u_out[m] = A_m^{-1}(u^(m-1) + dt f^(m)),
 // u^(-1) = u0 (the caller's chunk base pointers).
+// inv: the coefficients are the same every step (coef_stride 0, no FDE_REFACTOR): factor once at
+// step 0, then only the rhs column per step (k_run.cuh, RunArgs::inv).
 static int run_chunk(fde_hodlr* H, int K, double dt, const double* d_plus, const double* d_minus,
                      long long coef_stride, const double* f, long long f_stride, const double* u0,
-                     double* u_out, cudaStream_t s) {
+                     double* u_out, bool inv, cudaStream_t s) {
   const size_t cnt = (size_t)H->batch * H->n;
   const int L = H->L, B = H->batch;
   // second buffer set + stored leaf LUs (allocated once per handle)
@@ -1159,6 +1161,9 @@ static int run_chunk(fde_hodlr* H, int K, double dt, const double* d_plus, const
   // Q[:, 0] from it); split units keep B separate (its U unit stays off the step chain)
   ra.fuse = ra.split ? 0 : 1;
   if (const char* e = fde_dbg_env("FDE_RUN_FUSE")) ra.fuse = !ra.split && atoi(e) != 0;   // (diagnostics)
+  // factor once: the later steps are the rhs column alone, which needs the U / R unit split
+  ra.inv = inv ? 1 : 0;
+  if (inv) { ra.split = 1; ra.fuse = 0; }
   long long o = 0, units = 0;
   ra.o_A = o; o += n_leaf;
   ra.o_R = o; o += n_leaf;
@@ -1213,7 +1218,7 @@ static int run_chunk(fde_hodlr* H, int K, double dt, const double* d_plus, const
   H->run_las.resize(K);
   H->run_tas.resize(K);
   for (int m = 0; m < K; ++m) {
-    const int p = m & 1;
+    const int p = inv ? 0 : (m & 1);                 // (factor once: one buffer set, k_run.cuh)
     LeafArgs& lm = H->run_las[m];
     lm = la;
     lm.dp = d_plus + m * coef_stride; lm.dm = d_minus + m * coef_stride; lm.f = f + m * f_stride;
@@ -1632,14 +1637,17 @@ int fde1d_run(int batch, int n, const double* alpha, double h, double dt, int K,
     return rc;
   }
   if (!H->tree_ok || H->L < 1) {                  // no pipelined path: one fused step at a time
+    const bool once = coef_stride == 0 && !(flags & FDE_REFACTOR);   // (kept factor, LU reuse)
     for (int m = 0; m < K && rc == FDE_OK; ++m)
       rc = fde1d_step(batch, n, alpha, h, dt, d_plus + m * coef_stride, d_minus + m * coef_stride,
-                      f + m * f_stride, m == 0 ? u0 : u_out + (m - 1) * cnt, u_out + m * cnt, tol, leaf, 1,
-                      flags | FDE_NO_KEEP, &H, stream);
+                      f + m * f_stride, m == 0 ? u0 : u_out + (m - 1) * cnt, u_out + m * cnt, tol, leaf,
+                      once ? m == 0 : 1, (flags & ~FDE_REFACTOR) | (once ? 0u : FDE_NO_KEEP), &H, stream);
     if (!cache) hodlr_destroy(H);
     return rc;
   }
   if (H->dt != dt) TRY(set_dt(H, dt, s));
+  // same coefficients every step: factor once per launch
+  const bool inv = coef_stride == 0 && !(flags & FDE_REFACTOR);
   // chunks of at most RUN_KMAX steps per launch (the step index is a 16-bit field of the tree
   // task ids, k_run.cuh rn_tid; the counters and argument blocks are sized per chunk); chunk c
   // starts from the last solution of chunk c-1
@@ -1647,7 +1655,7 @@ int fde1d_run(int batch, int n, const double* alpha, double h, double dt, int K,
     const int Kc = std::min(RUN_KMAX, K - m0);
     rc = run_chunk(H, Kc, dt, d_plus + m0 * coef_stride, d_minus + m0 * coef_stride, coef_stride,
                    f + m0 * f_stride, f_stride, m0 == 0 ? u0 : u_out + (size_t)(m0 - 1) * cnt,
-                   u_out + (size_t)m0 * cnt, s);
+                   u_out + (size_t)m0 * cnt, inv, s);
   }
   if (rc != FDE_OK) { if (!cache) hodlr_destroy(H); return rc; }
   H->last_stream = s;

@@ -10,7 +10,7 @@ import torch
 
 from . import _lib
 from ._lib import (check, FDE_SYNC, FDE_CHECK, FDE_HOST_PTRS, FDE_NO_KEEP, FDE_RECOMPRESS,  # noqa: F401
-                   FDE_COMPRESS_ONLY, FDE_COEFFS_CHANGED)
+                   FDE_COMPRESS_ONLY, FDE_COEFFS_CHANGED, FDE_REFACTOR)
 
 
 def _stream(stream=None):
@@ -125,8 +125,9 @@ class Fde1dStepper:
 
     def run(self, dt, d_plus, d_minus, f, u0, u_out=None, flags=0, stream=None, K=None):
         """K steps in one pipelined launch (fde1d_run).  d_plus, d_minus, f: CUDA float64
-        (K, batch, n) -- or (1, batch, n) for time-invariant data; u0 (batch, n).  K defaults
-        to the largest leading dimension.  Returns u_out (K, batch, n): every step's solution."""
+        (K, batch, n) -- or (1, batch, n) for time-invariant data (coefficients given once: the
+        launch factors once, unless flags has FDE_REFACTOR); u0 (batch, n).  K defaults to the
+        largest leading dimension.  Returns u_out (K, batch, n): every step's solution."""
         cnt = self.batch * self.n
         if K is None:
             K = max(d_plus.shape[0], f.shape[0])

@@ -120,16 +120,19 @@ def test_check_with_host_pointers_matches_device_path():
 
 
 @gpu
-def test_run_longer_than_one_launch_chunk():
+@pytest.mark.parametrize("refactor", [False, True], ids=["factor_once", "refactor"])
+def test_run_longer_than_one_launch_chunk(refactor):
     """fde1d_run splits K > RUN_KMAX steps into several launches; a long cheap run (n = 256,
-    K = 8193 > 8192) matches the fused per-step path at its last steps."""
-    from paper_1804_05522_b200.hodlr import Fde1dStepper, FDE_NO_KEEP
+    K = 8193 > 8192) matches the fused per-step path at its last steps -- with the factor formed
+    once per launch (stride-0 coefficients) and with FDE_REFACTOR."""
+    from paper_1804_05522_b200.hodlr import Fde1dStepper, FDE_NO_KEEP, FDE_REFACTOR
     n, K = 256, 8193
     wl = W.make_1d(n, 1.5, 32, 1e-12, K=1, kind="const")
     dp, dm = wl.coeffs(1)
     f = wl.source(1)
     st = Fde1dStepper(n, wl.alpha, wl.h, wl.tol, wl.leaf)
-    out = st.run(1e-3, _t(dp)[None], _t(dm)[None], _t(f)[None], _t(wl.u0), K=K)
+    out = st.run(1e-3, _t(dp)[None], _t(dm)[None], _t(f)[None], _t(wl.u0), K=K,
+                 flags=FDE_REFACTOR if refactor else 0)
     torch.cuda.synchronize()
     ref = Fde1dStepper(n, wl.alpha, wl.h, wl.tol, wl.leaf)
     u = out[K - 3].clone()

@@ -417,6 +417,59 @@ def test_pipelined_run_invariant_coefficients_and_dt0():
     st.close()
 
 
+FACTOR_ONCE = [  # n, alphas, leaf, K, batch
+    (777, [1.6], 64, 5, 1),                  # split-unit size: refactor path bitwise equal
+    (2000, [1.7, 1.4, 1.55], 16, 4, 3),      # 384 leaves: the refactor run uses whole units
+    (300, [1.3, 1.35], 40, 3, 2),            # ragged leaves, batch
+    (1000, [1.8], 64, 1, 1),                 # K = 1 (factor step only)
+    (513, [1.1], 16, 6, 1),                  # deep tree
+]
+
+
+@gpu
+@pytest.mark.parametrize("n,alphas,leaf,K,batch", FACTOR_ONCE)
+def test_pipelined_run_factor_once(n, alphas, leaf, K, batch):
+    """Time-invariant coefficients (stride 0) make fde1d_run factor once (the LU computed
+    only once at the beginning) and run only the rhs column after step 0 (k_run.cuh, inv).  Every
+    step matches the dense oracle trajectory with one A for all steps (each side propagating its
+    own state), and the FDE_REFACTOR run of the same data to rounding -- bitwise where both runs
+    use split tree units."""
+    from paper_1804_05522_b200.hodlr import FDE_REFACTOR
+    wl = W.make_1d(n, np.array(alphas), leaf, 1e-12, K=K, batch=batch)
+    dp, dm = wl.coeffs(1)
+    f = wl.source(1)
+    st = _stepper(wl)
+    once = st.run(wl.dt, _t(dp)[None], _t(dm)[None], _t(f)[None], _t(wl.u0), K=K).cpu().numpy()
+    ref = st.run(wl.dt, _t(dp)[None], _t(dm)[None], _t(f)[None], _t(wl.u0), K=K,
+                 flags=FDE_REFACTOR).cpu().numpy()
+    split_refactor = batch * -(-n // leaf) < 2 * torch.cuda.get_device_properties(0).multi_processor_count
+    if split_refactor:
+        np.testing.assert_array_equal(once, ref)
+    for b in range(batch):
+        A = assemble_A(float(wl.alpha[b]), n, wl.h, wl.dt, dp[b], dm[b])
+        uo = wl.u0[b]
+        for m in range(K):
+            uo, _ = step_dense(A, uo, f[b], wl.dt)
+            assert _rel(once[m, b], ref[m, b]) <= 1e-12, (m, b, _rel(once[m, b], ref[m, b]))
+            assert _rel(once[m, b], uo) <= 1e-8, (m, b, _rel(once[m, b], uo))
+    st.close()
+
+
+@gpu
+def test_cfg1_factor_once_pipelined_run():
+    """cfg1 (d+- = 1, time-invariant) through fde1d_run: the factor-once launch bench.py times,
+    all 8 steps against the dense oracle trajectory."""
+    wl = W.cfg1()
+    st = _stepper(wl)
+    out = st.run(wl.dt, _t(wl.d_plus), _t(wl.d_minus), _t(wl.f), _t(wl.u0)).cpu().numpy()
+    assert wl.d_plus.shape[0] == 1 and out.shape[0] == wl.K
+    uo = wl.u0
+    for m in range(1, wl.K + 1):
+        uo = _oracle_step(wl, m, uo)[None]
+        assert _rel(out[m - 1, 0], uo[0]) <= 1e-8, (m, _rel(out[m - 1, 0], uo[0]))
+    st.close()
+
+
 @gpu
 def test_cfg3_pipelined_run_backward_error():
     """cfg3 at full size through fde1d_run (the launch bench.py times): eta <= 1e-10 per step."""
