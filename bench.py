@@ -222,9 +222,10 @@ def measure_cfg4(dev, world, rank, steps=16):
                                   i.e. SURVEY §8(d)'s "factor once" protocol (its roofline: ~2.7e5);
       value_solve_only         -- the 16 steps with an already kept factor (solve phase alone);
       value_refactor_every_step / _pipelined_run -- d+- treated as new every step;
-      value_factor_once_pipelined_run -- fde1d_run with the coefficients given once: the factor
-                                  is formed at step 0 of the launch, later steps are the rhs
-                                  column alone (k_run inv mode)."""
+      value_factor_once_run    -- fde1d_run with the coefficients given once (factor once): at
+                                  this size (32768 leaves > 16 per SM) it takes the kept-factor
+                                  path (the pipelined launch's factor-once mode, k_run inv,
+                                  is faster only below ~16 leaves per SM: DESIGN.md)."""
     import torch
     from paper_1804_05522_b200 import workloads as W
     from paper_1804_05522_b200.hodlr import Fde1dStepper, FDE_NO_KEEP, FDE_REFACTOR
@@ -273,7 +274,7 @@ def measure_cfg4(dev, world, rank, steps=16):
         runf(FDE_REFACTOR)
         v_run, ms_run = timed(lambda: runf(FDE_REFACTOR))
         runf(0)
-        v_run1, ms_run1 = timed(lambda: runf(0))     # factor once inside the pipelined launch
+        v_run1, ms_run1 = timed(lambda: runf(0))     # factor once (routed: kept-factor path)
     except Exception as e:                          # (memory for the second buffer set)
         v_run, ms_run, v_run1, ms_run1 = None, str(e)[:120], None, None
     st.close()
@@ -283,7 +284,7 @@ def measure_cfg4(dev, world, rank, steps=16):
             "value_solve_only": v_solve, "ms_16_steps_solve_only": ms_solve,
             "value_refactor_every_step": v_ref, "ms_16_steps_refactor": ms_ref,
             "value_refactor_pipelined_run": v_run, "ms_16_steps_refactor_pipelined_run": ms_run,
-            "value_factor_once_pipelined_run": v_run1, "ms_16_steps_factor_once_pipelined_run": ms_run1,
+            "value_factor_once_run": v_run1, "ms_16_steps_factor_once_run": ms_run1,
             "survey_roofline_factor_once": 2.7e5,
             "sharding": "%d instances per rank (shard.py), no data-path collective" % run.count}
 

@@ -1636,18 +1636,44 @@ int fde1d_run(int batch, int n, const double* alpha, double h, double dt, int K,
     if (cache) *cache = H; else hodlr_destroy(H);
     return rc;
   }
+  // Same coefficients every step (the LU computed once): factor once.  Two factor-once
+  // paths -- the pipelined launch (k_run inv mode: the later steps are B' + R units, latency-bound
+  // per leaf) and the kept-factor per-step path (fde1d_step: factor with step 1, then streaming
+  // solves at HBM rate).  Measured (tools/time_invariant.py, K = 16, ms): 512 leaves 2.0 vs 4.9,
+  // 2048 leaves 7.6 vs 7.9, 8192 leaves 30 vs 21, 32768 leaves 120 vs 75; without the projected
+  // tree the pipelined launch does not exist (n = 65536, alpha 1.5, tol 1e-12: 28.5 ms refactoring
+  // vs 9.8 kept).  Hence the kept path above 16 leaves per SM and without the tree path.
+  const bool once = coef_stride == 0 && !(flags & FDE_REFACTOR);
+  if (once) {
+    int dev = 0, nsm = 148;
+    CU(cudaGetDevice(&dev));
+    CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    if (!H->tree_ok || H->L < 1 || (long long)batch * H->nleaf > 16LL * nsm) {
+      for (int m = 0; m < K && rc == FDE_OK; ++m)
+        rc = fde1d_step(batch, n, alpha, h, dt, d_plus, d_minus, f + m * f_stride,
+                        m == 0 ? u0 : u_out + (m - 1) * cnt, u_out + m * cnt, tol, leaf, m == 0,
+                        flags & ~(FDE_REFACTOR | FDE_NO_KEEP | FDE_SYNC), &H, stream);
+      if (rc == FDE_OK) {
+        H->last_stream = s;
+        if ((flags & FDE_SYNC) || !cache) rc = sync_and_status(H, s);
+        if (!cache) hodlr_destroy(H);
+        return rc;
+      }
+      if (rc != FDE_EDIM) { if (!cache) hodlr_destroy(H); return rc; }
+      rc = FDE_OK;                                  // (kept-factor workspace too large: refactor below)
+      g_last_error.clear();
+    }
+  }
   if (!H->tree_ok || H->L < 1) {                  // no pipelined path: one fused step at a time
-    const bool once = coef_stride == 0 && !(flags & FDE_REFACTOR);   // (kept factor, LU reuse)
     for (int m = 0; m < K && rc == FDE_OK; ++m)
       rc = fde1d_step(batch, n, alpha, h, dt, d_plus + m * coef_stride, d_minus + m * coef_stride,
-                      f + m * f_stride, m == 0 ? u0 : u_out + (m - 1) * cnt, u_out + m * cnt, tol, leaf,
-                      once ? m == 0 : 1, (flags & ~FDE_REFACTOR) | (once ? 0u : FDE_NO_KEEP), &H, stream);
+                      f + m * f_stride, m == 0 ? u0 : u_out + (m - 1) * cnt, u_out + m * cnt, tol, leaf, 1,
+                      (flags & ~FDE_REFACTOR) | FDE_NO_KEEP, &H, stream);
     if (!cache) hodlr_destroy(H);
     return rc;
   }
   if (H->dt != dt) TRY(set_dt(H, dt, s));
-  // same coefficients every step: factor once per launch
-  const bool inv = coef_stride == 0 && !(flags & FDE_REFACTOR);
+  const bool inv = once;                            // (factor once per launch, k_run inv mode)
   // chunks of at most RUN_KMAX steps per launch (the step index is a 16-bit field of the tree
   // task ids, k_run.cuh rn_tid; the counters and argument blocks are sized per chunk); chunk c
   // starts from the last solution of chunk c-1
