@@ -1233,6 +1233,11 @@ static int run_chunk(fde_hodlr* H, int K, double dt, const double* d_plus, const
     // come free from leaf work; measured 630 vs 663 us/step at cfg3
     for (int l = 0; l < L; ++l) tm.rc[l] = 1;
     tm.Q = Qp[p]; tm.Qleaf = Qp[p] + H->qlev[L]; tm.Sst = Sp[p]; tm.X = Xp[p];
+    // B' prefetches X^(m-1) of its leaf into L2 (k_final.cuh) when the X buffer cannot stay
+    // L2-resident for a step (> 48 MB; 126 MB L2 shared with the stored LU, Q, S traffic):
+    // A/B (tools/gpu_s39.sh) cfg3 541 -> 538 us/step, cfg4 pipelined refactor 486 -> 483 ms;
+    // cfg1 (88 KB of X) +1 us/step with it, so small buffers skip it
+    tm.xmap = (double)B * H->xstride * 8.0 > 48e6 ? lm.xmap : nullptr;
     tm.Kr = ra.split ? H->d_Kr[p] : nullptr; tm.krinst = H->krinst;
     for (int l = 0; l < L; ++l) tm.krlev[l] = H->krlev[l];
     tm.u = u_out + m * cnt;

@@ -67,6 +67,16 @@ __device__ void leaf_rhs_final(const TrArgs& geo, const TrArgs* tp, const LeafAr
     cp_async_commit();
   };
   if (tp) {
+    // X^(m-1) of the leaf rows (read by u = X v below, after the v recursion) is mostly out of L2
+    // by now (written a step earlier): L2 prefetch of its 132 x 16 boxes through the TMA engine
+    // (no registers, no shared memory), in flight over the S staging and the v recursion
+#ifndef FDE_NO_XPF
+    if (tp->xmap && t == 0) {
+      for (int c0 = 0; c0 < NC; c0 += 16)
+        asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];"
+                     ::"l"(tp->xmap), "r"(r0), "r"(c0), "r"(inst) : "memory");
+    }
+#endif
     // ---- v = M_{L-1} .. M_0 e_0,  M_m: v[m-cols] = -S_side(m) v[< xc_m]   (k_tree.cuh);
     //      S_side(m) (k x xm, row-major in HBM) is staged transposed: lane q reads row q
     //      conflict-free while the warp walks the columns

@@ -40,6 +40,7 @@ struct TrArgs {
   double* Q;                     // Q store of all levels 1..L
   double* Sst;                   // S store: node (m, j): [S_top (k x xc[m]) | S_bot]
   const double* X; long long xstride; int n;
+  const void* xmap;              // k_run: TMA map of this X buffer (L2 prefetch of X^(m-1) in B'), or null
   const int* leaf_r0; const int* leaf_n;
   double* u;                     // [batch * n] output
   unsigned* bar;
