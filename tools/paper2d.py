@@ -46,8 +46,8 @@ def run(n, alphas, variable):
 
 
 def main():
-    out = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "profiles", "r01_paper2d.json")
-    ns = [int(a) for a in sys.argv[2:]] or [1024, 2048, 4096, 8192, 16384, 32768]
+    out = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "profiles", "r02_paper2d.json")
+    ns = [int(a) for a in sys.argv[2:]] or [1024, 2048, 4096, 8192, 16384, 32768, 65536]
     run(512, (1.3, 1.7), False)                                  # warm-up (module load, JIT-free)
     rows = []
     for variable in (False, True):
@@ -61,6 +61,18 @@ def main():
         json.dump({"protocol": "paper Sec. 5.1 (P:1584-1632): dt = 1, 8 steps, HODLR tol 1e-8, "
                                "EK tol 1e-6, leaf 128; time = host wall clock of all 8 steps incl. "
                                "build + factor of both operators", "runs": rows}, fh, indent=1)
+    with open(os.path.splitext(out)[0] + ".md", "w") as fh:
+        fh.write("# Paper protocol 2D run (Sec. 5.1, P:1584-1632; SURVEY 8(f) NEXT-2)\n\n"
+                 "`tools/paper2d.py` on B200: dt = 1, 8 implicit-Euler steps of the Sylvester form, HODLR tol "
+                 "1e-8, EK tolerance 1e-6, leaf 128; t = host wall clock of all 8 steps including build + "
+                 "factor of both operators; rank = rank of the final X; its = EK iterations per step; "
+                 "qs = max compressed rank + 1 of A1, A2; res = largest reported relative residual.\n\n"
+                 "| coefficients | alpha | N | t (s) | rank | its | qs | res |\n|---|---|---|---|---|---|---|---|\n")
+        for r in rows:
+            fh.write("| %s | (%s, %s) | %d | %.3f | %d | %s | %d/%d | %.1e |\n" % (
+                r["coefficients"], r["alpha"][0], r["alpha"][1], r["n"], r["t_8_steps_s"], r["final_rank"],
+                ",".join(str(i) for i in r["ek_iterations"]), r["qsrank_ops"][0], r["qsrank_ops"][1],
+                max(r["residuals"])))
     print("wrote", out)
 
 
