@@ -24,7 +24,8 @@ def run(n, alphas, variable):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     st = Fde2dStepper(wl.nx, wl.ny, wl.alpha1, wl.alpha2, wl.hx, wl.hy, wl.dt, t(wl.d1p), t(wl.d1m),
-                      t(wl.d2p), t(wl.d2m), wl.tol, ek_tol=wl.ek_tol, leaf=wl.leaf)
+                      t(wl.d2p), t(wl.d2m), wl.tol, ek_tol=wl.ek_tol, ek_maxit=60, leaf=wl.leaf)   # (binding default 30:
+    # the first step from u0 = 0 needs 27-31 EK iterations at N >= 32768 with alpha = (1.7, 1.9))
     Xu = Xv = None
     its, ranks, res = [], [], []
     for m in range(1, wl.K + 1):
