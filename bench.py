@@ -641,7 +641,7 @@ def run_ours(args, world, rank, local):
         except Exception as e:
             extra["cfg5"] = {"error": str(e)[:200]}
 
-    if not args.no_extra and world == 1:
+    if not args.no_extra and world == 1 and not os.environ.get("FDE_BENCH_WATCHDOG"):
         extras()
     elif not args.no_extra:
         # Multi-rank extras contain collectives: a rank that fails alone would leave the others

@@ -1,7 +1,7 @@
 #!/bin/bash
-# quick: k_run timing (cfg3) + task trace (diagnostics library)
+# bench through the watchdog thread (the multi-rank path of the extras) and the default bench.
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
-timeout 120 python tools/time_run.py 16 64 > gpurun_out/t_time.log 2>&1
-FDE_LIB_DEBUG=1 timeout 120 python tools/trace_run.py 16 > gpurun_out/t_trace.log 2>&1
-cat gpurun_out/t_time.log; grep -E "phases|units|span|mean" gpurun_out/t_trace.log | tail -24
+FDE_BENCH_WATCHDOG=1 timeout 900 python bench.py --steps 20 --warmup 3 > gpurun_out/bench_wd.json 2> gpurun_out/bench_wd.err; echo "rc=$?" >> gpurun_out/bench_wd.err
+FDE_BENCH_WATCHDOG=1 FDE_BENCH_EXTRA_TIMEOUT=5 timeout 900 python bench.py --steps 20 --warmup 3 --no-cpu > gpurun_out/bench_wd2.json 2> gpurun_out/bench_wd2.err; echo "rc=$?" >> gpurun_out/bench_wd2.err
+tail -c 600 gpurun_out/bench_wd.json; tail -3 gpurun_out/bench_wd.err; tail -c 400 gpurun_out/bench_wd2.json; tail -3 gpurun_out/bench_wd2.err
