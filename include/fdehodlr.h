@@ -178,7 +178,10 @@ int fde1d_step_split(int world, int rank, fde_allgather_fn gather, void* ctx, in
  *   `cache`, alpha, h, tol, leaf, stream as in fde1d_step.  Asynchronous unless FDE_SYNC.
  * FDE_HOST_PTRS: d_plus, d_minus, f, u0 and u_out are HOST arrays (pinned for asynchronous copies;
  * strides 0 or batch*n): the library stages them on the device on `stream`, runs, copies every
- * step's solution back and synchronises (the copies are part of the call).
+ * step's solution back and synchronises (the copies are part of the call).  With per-step
+ * coefficients and K >= 24 the run is three launches (head, body, tail of max(4, K/16) | rest |
+ * max(4, K/16) steps) and the copies overlap them on two internal streams: only the head's H2D
+ * and the tail's D2H are exposed; results are bitwise those of the one-launch run.
  * The handle owns a second panel/projection buffer set, two stored leaf LUs and per-step
  * counters sized for K: the first call (and any call with a larger K) allocates them, which
  * synchronises the stream.  Without the tree path (L = 0 or a panel too wide for it) the call

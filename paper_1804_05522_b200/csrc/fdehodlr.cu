@@ -1628,6 +1628,65 @@ int fde1d_run(int batch, int n, const double* alpha, double h, double dt, int K,
       H->hstage_cap = need;
     }
     double *sdp = H->d_hstage, *sdm = sdp + lc * cnt, *sf = sdm + lc * cnt, *su0 = sf + lf * cnt, *sout = su0 + cnt;
+    if (coef_stride != 0 && K >= 24) {
+      // Long runs with per-step coefficients: three launches (head, body, tail).  Only the head's
+      // coefficients are copied before the first launch; the rest of the H2D runs on a second
+      // stream behind the head launch, and every chunk's solutions go back on a third stream
+      // behind the next launch, so of the copies only the head's H2D and the tail's D2H are
+      // exposed (cfg3, K = 64: 68 MB in, 34 MB out).  Chunk c starts from the last solution of
+      // chunk c-1 (as the RUN_KMAX chunks below); each chunk boundary drains the step pipeline once.
+      const int Kh = std::max(4, K / 16);
+      const int m0s[4] = {0, Kh, K - Kh, K};
+      cudaStream_t csi = nullptr, cso = nullptr;
+      cudaEvent_t ev[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+      auto done = [&](int r) {
+        if (csi) { cudaStreamSynchronize(csi); cudaStreamDestroy(csi); }
+        if (cso) { cudaStreamSynchronize(cso); cudaStreamDestroy(cso); }
+        for (auto& e : ev) if (e) cudaEventDestroy(e);
+        if (cache) *cache = H; else hodlr_destroy(H);
+        return r;
+      };
+#define CUD(call) do { const cudaError_t e_ = (call); if (e_ != cudaSuccess) return done(set_err(FDE_ECUDA, "%s: %s", #call, cudaGetErrorString(e_))); } while (0)
+      CUD(cudaStreamCreateWithFlags(&csi, cudaStreamNonBlocking));
+      CUD(cudaStreamCreateWithFlags(&cso, cudaStreamNonBlocking));
+      for (auto& e : ev) CUD(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      auto h2d_steps = [&](cudaStream_t q, int a, int b) -> cudaError_t {   // steps [a, b) of the strided arrays
+        const size_t o = (size_t)a * cnt, nb = (size_t)(b - a) * cnt * 8;
+        cudaError_t e = cudaMemcpyAsync(sdp + o, d_plus + o, nb, cudaMemcpyHostToDevice, q);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(sdm + o, d_minus + o, nb, cudaMemcpyHostToDevice, q);
+        if (e == cudaSuccess && f_stride) e = cudaMemcpyAsync(sf + o, f + o, nb, cudaMemcpyHostToDevice, q);
+        return e;
+      };
+      CUD(cudaEventRecord(ev[0], s));                     // (the staging area is free once `s` gets here)
+      CUD(cudaStreamWaitEvent(csi, ev[0], 0));
+      CUD(cudaStreamWaitEvent(cso, ev[0], 0));
+      CUD(cudaMemcpyAsync(su0, u0, cnt * 8, cudaMemcpyHostToDevice, s));
+      if (!f_stride) CUD(cudaMemcpyAsync(sf, f, cnt * 8, cudaMemcpyHostToDevice, s));
+      CUD(h2d_steps(s, m0s[0], m0s[1]));
+      CUD(h2d_steps(csi, m0s[1], m0s[2]));
+      CUD(cudaEventRecord(ev[1], csi));
+      CUD(h2d_steps(csi, m0s[2], m0s[3]));
+      CUD(cudaEventRecord(ev[2], csi));
+      for (int c = 0; c < 3 && rc == FDE_OK; ++c) {
+        const int a = m0s[c], b = m0s[c + 1];
+        if (c > 0) CUD(cudaStreamWaitEvent(s, ev[c], 0));
+        rc = fde1d_run(batch, n, alpha, h, dt, b - a, sdp + (size_t)a * cnt, sdm + (size_t)a * cnt, coef_stride,
+                       sf + (size_t)a * f_stride, f_stride, a == 0 ? su0 : sout + (size_t)(a - 1) * cnt,
+                       sout + (size_t)a * cnt, tol, leaf, flags & ~(FDE_HOST_PTRS | FDE_SYNC), &H, stream);
+        if (rc != FDE_OK) break;
+        CUD(cudaEventRecord(ev[3 + c], s));
+        CUD(cudaStreamWaitEvent(cso, ev[3 + c], 0));
+        CUD(cudaMemcpyAsync(u_out + (size_t)a * cnt, sout + (size_t)a * cnt, (size_t)(b - a) * cnt * 8,
+                            cudaMemcpyDeviceToHost, cso));
+      }
+      if (rc == FDE_OK) {
+        CUD(cudaEventRecord(ev[6], cso));
+        CUD(cudaStreamWaitEvent(s, ev[6], 0));
+        rc = sync_and_status(H, s);
+      }
+#undef CUD
+      return done(rc);
+    }
     CU(cudaMemcpyAsync(sdp, d_plus, lc * cnt * 8, cudaMemcpyHostToDevice, s));
     CU(cudaMemcpyAsync(sdm, d_minus, lc * cnt * 8, cudaMemcpyHostToDevice, s));
     CU(cudaMemcpyAsync(sf, f, lf * cnt * 8, cudaMemcpyHostToDevice, s));

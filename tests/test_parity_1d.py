@@ -534,3 +534,25 @@ def test_pipelined_run_host_pointers_match_device():
     assert not host.is_cuda
     np.testing.assert_array_equal(host.numpy(), dev)
     st.close()
+
+
+@gpu
+@pytest.mark.parametrize("K,f_invariant", [(24, False), (37, True)])
+def test_pipelined_run_host_pointers_overlapped_chunks(K, f_invariant):
+    """K >= 24 with per-step coefficients: the host-pointer run is three launches (head, body,
+    tail) with the copies overlapped on side streams; bitwise equal to the one-launch
+    device-pointer run (also with a time-invariant source, stride 0, and pageable host arrays)."""
+    from paper_1804_05522_b200.hodlr import FDE_HOST_PTRS
+    wl = W.make_1d(700, 1.4, 32, 1e-12, K=K)
+    st = _stepper(wl)
+    DP = np.stack([wl.coeffs(m)[0] for m in range(1, K + 1)])
+    DM = np.stack([wl.coeffs(m)[1] for m in range(1, K + 1)])
+    F = wl.source(1)[None] if f_invariant else np.stack([wl.source(m) for m in range(1, K + 1)])
+    dev = st.run(wl.dt, _t(DP), _t(DM), _t(F), _t(wl.u0), K=K).cpu().numpy()
+    for pin in (True, False):
+        hp = lambda a: (lambda x: x.pin_memory() if pin else x)(
+            torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64))
+        host = st.run(wl.dt, hp(DP), hp(DM), hp(F), hp(wl.u0), K=K, flags=FDE_HOST_PTRS)
+        assert not host.is_cuda
+        np.testing.assert_array_equal(host.numpy(), dev)
+    st.close()
