@@ -347,6 +347,9 @@ static int proj_sylvester(cudaStream_t s, const Ws2d& w, int sa, int sb, double*
     TRY(ts_nn(s, sa, sb, sb, 1.0, T, sa, Bi, sb, 0.0, T2, sa));
     { PROF("k_sign_update"); k_sign_update<<<1, DN_BIG, 0, s>>>(sa, sb, A, Ai, B, Bi, C, T2, w.dv); }
     TRY(dn_check("k_sign_update"));
+    // (the iteration needs ~log2 of the spectrum's spread before it contracts: 9-11 iterations on
+    //  the projected EK operators, so the first four are queued without reading the change back)
+    if (it < 4) continue;
     CU(cudaMemcpyAsync(hout, w.dv, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
     if (fde_dbg_env("FDE_DEBUG2D") && fde_dbg_env("FDE_DEBUG2D")[0] == '2')
