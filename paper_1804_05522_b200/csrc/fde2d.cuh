@@ -273,14 +273,11 @@ static int orth_append(cudaStream_t s, const Ws2d& w, int n, double* W, int b, d
   *nb = 0;
   if (b <= 0 || sb >= smax) return FDE_OK;
   if (b > PO_MAX) return set_err(FDE_EDIM, "block of %d columns exceeds %d", b, PO_MAX);
-  std::vector<double> h(b + 2);
+  // ref = largest squared column norm of the block, kept on the device (w.dv[30]): pass 0's
+  // threshold is dtol^2 * ref inside k_pchol_orth (a zero block keeps no column: nk = 0)
   TRY(ts_tn(s, w, b, b, n, 1.0, W, n, W, n, 0.0, w.G, b));
-  CU(cudaMemcpy2DAsync(h.data(), sizeof(double), w.G, (b + 1) * sizeof(double), sizeof(double), b,
-                       cudaMemcpyDeviceToHost, s));
-  CU(cudaStreamSynchronize(s));
-  double ref = 0.0;
-  for (int i = 0; i < b; ++i) ref = std::max(ref, h[i]);
-  if (!(ref > 0.0)) return FDE_OK;
+  { PROF("k_diag_max"); k_diag_max<<<1, 32, 0, s>>>(b, w.G, w.dv + 30); }
+  TRY(dn_check("k_diag_max"));
   int cur = b;
   double* src = W;
   for (int pass = 0; pass < 2; ++pass) {
@@ -289,8 +286,9 @@ static int orth_append(cudaStream_t s, const Ws2d& w, int n, double* W, int b, d
       TRY(ts_nn(s, n, cur, sb, -1.0, Ub, n, w.M1, sb, 1.0, src, n));      // W -= U H
     }
     TRY(ts_tn(s, w, cur, cur, n, 1.0, src, n, src, n, 0.0, w.G, cur));
-    const double thr = pass == 0 ? (dtol * dtol) * ref : 0.25;
-    { PROF("k_pchol_orth"); k_pchol_orth<<<1, 256, PO_SMEM, s>>>(cur, w.G, thr, std::min(cur, smax - sb), w.S, w.iv); }
+    const double thr = pass == 0 ? dtol * dtol : 0.25;
+    { PROF("k_pchol_orth"); k_pchol_orth<<<1, 256, PO_SMEM, s>>>(cur, w.G, thr, std::min(cur, smax - sb), w.S, w.iv,
+                                                                  pass == 0 ? w.dv + 30 : nullptr); }
     TRY(dn_check("k_pchol_orth"));
     int nk = 0;
     CU(cudaMemcpyAsync(&nk, w.iv, sizeof(int), cudaMemcpyDeviceToHost, s));

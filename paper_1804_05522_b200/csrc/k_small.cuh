@@ -426,9 +426,20 @@ k_gj_inv_cl(const InvJob* __restrict__ jobs, DevStatus* st) {
 // rounding of G), and *nk_out.  One CTA; b <= PO_MAX.  Dynamic shared memory PO_SMEM.
 #define PO_MAX 64
 #define PO_SMEM (2 * PO_MAX * PO_MAX * 8)
+// thr_ref (optional, device): the threshold is thr * *thr_ref (a reference norm left on the device
+// by k_diag_max, so the host does not read it back).
+__global__ void k_diag_max(int b, const double* __restrict__ G, double* __restrict__ out) {
+  double v = 0.0;                                      // (one warp; fixed order)
+  for (int i = threadIdx.x; i < b; i += 32) v = fmax(v, G[(long long)i * b + i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if (threadIdx.x == 0) *out = v;
+}
+
 __global__ void __launch_bounds__(256)
 k_pchol_orth(int b, const double* __restrict__ G, double thr, int nmax, double* __restrict__ Sm,
-             int* __restrict__ nk_out) {
+             int* __restrict__ nk_out, const double* __restrict__ thr_ref = nullptr) {
+  if (thr_ref) thr *= *thr_ref;
   extern __shared__ double po_sm[];
   double* L = po_sm;                                  // L[q * b + i]: column q of the factor
   double* X = po_sm + PO_MAX * PO_MAX;                // X[r * PO_MAX + c] = (R^{-1})[r][c]
