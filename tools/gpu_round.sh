@@ -1,14 +1,8 @@
 #!/bin/bash
-# Round-end style evidence run: tests, smoke, full bench, ncu launch list + full capture of k_run.
+# Round-end check on the final tree: full GPU suite, smoke, default bench (no profiler).
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
-timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
-CMD="python bench.py --steps 16 --warmup 3 --no-e2e --no-cpu --no-extra"
-timeout 300 $CMD > gpurun_out/plain.log 2>&1 && \
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
-echo "ncu launches rc=$?" >> gpurun_out/ncu_launch.log
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_run -s 2 -c 1 -o gpurun_out/prof $CMD > gpurun_out/ncu_full.log 2>&1
-echo "ncu full rc=$?" >> gpurun_out/ncu_full.log
-tail -n 3 gpurun_out/pytest_gpu.log gpurun_out/smoke.log gpurun_out/ncu_full.log
+timeout 2400 python -m pytest tests -q -m gpu > gpurun_out/fin_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/fin_pytest.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/fin_smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/fin_smoke.log
+timeout 900 python bench.py > gpurun_out/fin_bench.json 2> gpurun_out/fin_bench.err; echo "bench rc=$?" >> gpurun_out/fin_bench.err
+tail -n 3 gpurun_out/fin_pytest.log; tail -n 2 gpurun_out/fin_smoke.log; tail -c 200 gpurun_out/fin_bench.err
