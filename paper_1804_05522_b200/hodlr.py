@@ -187,7 +187,7 @@ class Fde2dStepper:
     column-major (n, r))."""
 
     def __init__(self, nx, ny, alpha1, alpha2, hx, hy, dt, d1p, d1m, d2p, d2m, tol, ek_tol=1e-11,
-                 ek_maxit=30, leaf=128, rmax=256):
+                 ek_maxit=60, leaf=128, rmax=256):
         self.nx, self.ny = nx, ny
         self.alpha1, self.alpha2, self.hx, self.hy, self.dt = alpha1, alpha2, hx, hy, dt
         self.coef = [_dev(d1p, "d1p", nx), _dev(d1m, "d1m", nx), _dev(d2p, "d2p", ny), _dev(d2m, "d2m", ny)]

@@ -69,7 +69,7 @@ class SplitSylvesterStepper:
     pair rank 0 and Xv (r, ny) on pair rank 1 (both at pair size 1, as (Xu, Xv))."""
 
     def __init__(self, nx, ny, alpha1, alpha2, hx, hy, dt, d1p, d1m, d2p, d2m, tol, ek_tol=1e-11,
-                 ek_maxit=30, leaf=128, rmax=256, group=None, world=1, rank=0):
+                 ek_maxit=60, leaf=128, rmax=256, group=None, world=1, rank=0):
         from .hodlr import _dev
         self.nx, self.ny, self.world, self.rank, self.group = nx, ny, world, rank, group
         self.alpha1, self.alpha2, self.hx, self.hy, self.dt = alpha1, alpha2, hx, hy, dt
