@@ -1,7 +1,7 @@
 #!/bin/bash
-# ncu --set full of the 2D step's top kernels (cluster Gauss-Jordan inverse, tall-skinny GEMM) at cfg5
+# quick 2D check: parity tests (2D, split, rational Krylov) + smoke
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
-timeout 300 python tools/prof_2d.py 3 > gpurun_out/plain2d.log 2>&1; echo "plain rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gj_inv_cl -s 20 -c 2 -o gpurun_out/prof_2d python tools/prof_2d.py 3 > gpurun_out/ncu_2dfull.log 2>&1; echo "ncu rc=$?"
-tail -2 gpurun_out/ncu_2dfull.log
+timeout 900 python -m pytest tests/test_parity_2d.py tests/test_split2d.py tests/test_rk2d.py -q -m gpu -p no:cacheprovider > gpurun_out/t_2d.log 2>&1; echo "t rc=$?" >> gpurun_out/t_2d.log
+tail -n 4 gpurun_out/t_2d.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -2
